@@ -1,0 +1,301 @@
+"""Benchmark: space-time DoF updates/s per outer iteration (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl b200|reference]
+
+A "step" is one outer iteration of the inverted time-stepping scheme over every
+time step of the workload (residual with previous-step coupling, block
+preconditioner, damped update, per-step residual norms).  Default workload:
+config 3 (2D 512x512 P1-P1, N_t = 1024, kappa=1e-6, S=0), the configuration the
+metric's roofline and 8-GPU efficiency targets are quoted on that fits one GPU
+(DESIGN.md "Measurement").  N > 1: torchrun, one rank per GPU, time slabs of
+N_t/N steps, NCCL send/recv of one slice per step (strong scaling).
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time DoF updates/s per outer iteration; % of HBM/fp64 roofline"
+UNIT = "DoF-updates/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--precond", type=int, default=2)
+    ap.add_argument("--omega", type=float, default=0.5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.05)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def load_traffic(cid):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        return json.load(open(p)).get(f"config{cid}")
+    except Exception:
+        return None
+
+
+def cpu_baseline(prob, precond, omega, budget_s=12.0, window=64):
+    """The oracle as it stands, on all host cores, over a bounded sample of the workload."""
+    import oracle
+    S = oracle.OracleSystem(prob)
+    cores = os.cpu_count() or 1
+    w = min(window, prob.n_t)
+    X = np.zeros((w + 1, S.ndof))
+    s = np.ones(w)
+    passes, t0 = 0, time.perf_counter()
+    while True:
+        S.iterate(X, s, 1, precond, omega, history=True, nthreads=cores)
+        passes += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or passes >= 200:
+            break
+    value = S.ndof * w * passes / el
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{passes} outer iteration(s) over a {w}-step window of the full "
+                      f"{prob.coords.shape[0]}-node mesh, P~{precond}, omega={omega} "
+                      f"(oracle assembly excluded), {el:.1f} s wall"}
+
+
+def workload_config(args, prob, world):
+    from workloads import DESCRIPTIONS
+    ws_gb = 2 * prob.n_dof * prob.n_t * 8 / 1e9
+    return {"workload": f"config{args.config}: {DESCRIPTIONS[args.config]}",
+            "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
+            "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
+            "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
+            "l2": f"inputs larger than L2 (x panels {ws_gb:.1f} GB vs 126 MB L2); no flush needed",
+            "inputs": "x^0 = 0, s_n = 1 (BJ metric inputs), synthetic mesh/material"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from workloads import config_problem
+    prob = config_problem(args.config)
+    import oracle
+    S = oracle.OracleSystem(prob)
+    cores = os.cpu_count() or 1
+    w = min(16, prob.n_t)
+    X = np.zeros((w + 1, S.ndof))
+    s = np.ones(w)
+    S.iterate(X, s, 1, args.precond, args.omega, nthreads=cores)     # warm-up pass
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        S.iterate(X, s, 1, args.precond, args.omega, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+        if sum(times) > 150:
+            break
+    tot = sum(times)
+    value = S.ndof * w * len(times) / tot
+    sample = (f"each step = 1 outer iteration of the oracle over a {w}-step window of the full "
+              f"{prob.coords.shape[0]}-node mesh (bounded sample of the workload)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(args, prob, 1),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    from paper_2310_10430_b200 import BiotSolver, nccl_unique_id
+    from workloads import config_problem
+
+    prob = config_problem(args.config)
+    nccl_id = None
+    if world > 1:
+        buf = torch.zeros(128, dtype=torch.uint8)
+        if rank == 0:
+            buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(buf, 0)
+        nccl_id = bytes(buf.numpy().tobytes())
+    stream = torch.cuda.current_stream()
+    g = BiotSolver(prob, precond=args.precond, omega=args.omega, device=local, rank=rank, world=world,
+                   nccl_id=nccl_id, stream=stream.cuda_stream, history=max(1024, args.steps + args.warmup + 8))
+    info = g.info
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (untimed)
+    g.iterate(max(args.warmup, 3))
+    barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    ev0.record(stream)
+    g.iterate(args.steps)              # K outer iterations, one library call, no host sync inside
+    ev1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    sweep_ms = float(g.last_timing()[1])   # dominant kernel, CUDA events on the launching stream
+    t = torch.tensor([ms, sweep_ms], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, sweep_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+    value = prob.n_dof * prob.n_t * args.steps / (ms / 1e3)
+
+    # end to end through the public API with host buffers: every step uploads its
+    # inputs (the load scales s_n) from pinned host memory and reads back the
+    # step's result (per-step residual norms)
+    s_host = torch.ones(prob.n_t, dtype=torch.float64).pin_memory()
+    out_host = torch.empty((info.n_t_local, 2), dtype=torch.float64).pin_memory()
+    s_np, out_np = s_host.numpy(), out_host.numpy()
+    from paper_2310_10430_b200 import _lib
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.e2e_steps):
+        g.set_load_scale(s_np)
+        g.iterate(1)
+        _lib.check(g.lib.biot_residual_history(g.ctx, g.get_info().iterations - 1, _lib.ptr(out_np)), g.ctx)
+    e1.record(stream)
+    barrier()
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = prob.n_dof * prob.n_t * args.e2e_steps / (float(e2e_ms[0]) / 1e3)
+
+    if rank == 0:
+        pk = peaks()
+        hbm = pk["hbm_gbs"] if pk else 6650.0
+        algo_bytes = info.bytes_per_iter          # per launch of the sweep kernel (this rank)
+        achieved_gbs = algo_bytes / (sweep_ms / 1e3) / 1e9
+        sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
+        fp64_peak_tf = 148 * 64 * 2 * sm_max * 1e6 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop
+        achieved_tf = info.flops_per_iter / (sweep_ms / 1e3) / 1e12
+        if prob.dim == 2:
+            roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm, "traffic": load_traffic(args.config),
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
+                    "fp64_tflops": achieved_tf, "fp64_peak_tflops_nominal": fp64_peak_tf}
+        else:
+            roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_peak_tf, "unit": "TFLOP/s",
+                    "frac": achieved_tf / fp64_peak_tf, "traffic": load_traffic(args.config),
+                    "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
+                    "hbm_gbs": achieved_gbs, "hbm_peak": hbm}
+        roof["kernel"] = "biot sweep_kernel (fused residual + P~ + update + norms)"
+        roof["kernel_ms"] = sweep_ms
+        per_step = 2 if args.precond == 2 else 3
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload_config(args, prob, world), "roofline": roof,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * prob.n_t),
+                        "d2h_bytes_per_step": int(16 * info.n_t_local),
+                        "what": "per step: biot_set_load_scale (host s_n) + biot_iterate(1) + "
+                                "biot_residual_history readback, host sync each step"},
+                "gpu_launches": per_step * args.steps,
+                "clocks": clocks}
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(prob, args.precond, args.omega)
+        print(json.dumps(line), flush=True)
+    g.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,186 @@
+/*
+ * biot_pit.h -- C-ABI of the B200-native parallel-in-time Biot solver
+ * (arXiv 2310.10430, "A Parallel-in-time Method Based on Preconditioner for
+ * Biot's Model").  Library: paper_2310_10430_b200/libbiot_pit.so (sm_100a).
+ *
+ * What one outer iteration computes (the hot path), for every local time
+ * step n at once (Jacobi in time, BASELINE.json north star; PAPER.md L290-302
+ * Algorithm 2 with the damped preconditioned update, R1-R4):
+ *
+ *     r_n       = A' x_{n-1}^k + s_n f - AA x_n^k
+ *     x_n^{k+1} = x_n^k + omega * P^{-1} r_n               (L298; R3 damping)
+ *     rho_n     = ( ||r_{n,u}||_2 , ||r_{n,p}||_2 )          (R12)
+ *
+ * with the stabilised P1-P1 backward-Euler operators (PAPER.md L146-231,
+ * eqs. fullysystem/axb; storage S per R8, per-cell kappa per R9):
+ *     AA = [[A, B], [B^T, -(S M + dt C_kappa + beta L)]]
+ *     A' = [[0, 0], [B^T, -(S M + beta L)]],  f = [F; 0]
+ * and the paper's block preconditioners built on the approximate Schur
+ * complement S~p = S M + dt C_kappa + beta L (eqs. p1/p2),
+ * whose inner inverses A^{-1}, S~p^{-1} are realised by their diagonals (R2):
+ *     P~1 = [[A, 0], [B^T, -S~p]]   (block lower triangular)
+ *     P~2 = [[A, 0], [0,  -S~p]]    (block diagonal)
+ *
+ * Conventions
+ *  - Vectors exchanged through this ABI are node-interleaved fp64:
+ *    x[node*(d+1) + c], c = 0..d-1 displacement, c = d pressure (R20).
+ *  - Time steps are global and 1-based: n = 1..n_t; x_0 is the fixed state at
+ *    t = 0.  With world > 1, rank r owns steps n in (r*n_t/world, (r+1)*n_t/world].
+ *  - All host inputs are copied during biot_setup; the caller may free them on
+ *    return.  Output buffers are caller-allocated host memory.
+ *  - Every call returns a biot_status; nothing aborts or throws across the
+ *    ABI.  On error, biot_last_error(ctx) (or biot_last_error(NULL) for
+ *    errors before a context exists) holds a message.
+ *  - A context is not thread-safe.  With world > 1, biot_setup, biot_iterate
+ *    and biot_destroy are collective: every rank calls them in the same order.
+ *  - biot_iterate is additive: iterate(a); iterate(b) == iterate(a+b), bitwise.
+ *  - Results are bitwise reproducible run to run, and the iterates x^k are
+ *    bitwise independent of world (time-slab count).
+ */
+#ifndef BIOT_PIT_H
+#define BIOT_PIT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BIOT_PIT_ABI_VERSION 1
+
+typedef struct biot_ctx biot_ctx;   /* opaque; owned by the library until biot_destroy */
+
+typedef enum {
+    BIOT_OK = 0,
+    BIOT_E_INVALID = 1,     /* bad argument; no state changed                      */
+    BIOT_E_NOMEM = 2,       /* host or device allocation failed                    */
+    BIOT_E_CUDA = 3,        /* CUDA runtime error (no device, launch failure, ...) */
+    BIOT_E_NCCL = 4,        /* NCCL missing or failed                              */
+    BIOT_E_STATE = 5,       /* call not valid in the current state                 */
+    BIOT_E_NONFINITE = 6    /* a residual norm became NaN/Inf                      */
+} biot_status;
+
+/* Simplicial mesh (3D per BASELINE.json configs 4-5). */
+typedef struct {
+    int32_t dim;             /* 2 (triangles) or 3 (tetrahedra)                          */
+    int64_t n_nodes;
+    const double *coords;    /* host, n_nodes*dim                                        */
+    int64_t n_cells;
+    const int32_t *cells;    /* host, n_cells*(dim+1), positively oriented; a degenerate
+                                or inverted cell -> BIOT_E_INVALID                        */
+} biot_mesh;
+
+/* Material (R5, R8, R9). */
+typedef struct {
+    double lambda, mu;       /* Lame coefficients, mu > 0, lambda >= 0                   */
+    double alpha;            /* Biot-Willis constant                                     */
+    double storage;          /* S >= 0 (storage coefficient, R8)                         */
+    const double *kappa;     /* host, per-cell permeability (n_cells), or NULL           */
+    double kappa_uniform;    /* used when kappa == NULL; must be > 0                     */
+    double beta;             /* stabilisation factor; < 0 => h / (4 (lambda + 2 mu))     */
+    double h;                /* mesh size entering beta (R6), > 0 if beta < 0    */
+} biot_material;
+
+/* Boundary data of the column problem (R11, R16). */
+typedef struct {
+    const uint8_t *dirichlet;        /* host, n_nodes*(dim+1), 1 = homogeneous Dirichlet DoF */
+    int64_t n_traction_facets;
+    const int32_t *traction_facets;  /* host, n_facets*dim node ids of boundary facets      */
+    double traction[3];              /* constant traction on those facets (first dim used)  */
+    const double *load_scale;        /* host, n_t values s_n (n = 1..n_t), or NULL => 1      */
+    const double *x_initial;         /* host, x_0 (n_nodes*(dim+1)), or NULL => 0            */
+} biot_bc;
+
+#define BIOT_FLAG_MANUAL_HALO 1u     /* world > 1 without NCCL: caller moves the halo with
+                                        biot_last_slice / biot_set_ghost (tests, emulation) */
+#define BIOT_FLAG_NO_GRAPH    2u     /* launch kernels directly instead of a CUDA graph     */
+
+typedef struct {
+    int32_t precond;         /* 1 = P~1, 2 = P~2                                          */
+    double omega;            /* damping, > 0 (R3; default 0.5)                            */
+    int32_t device;          /* CUDA device ordinal                                       */
+    int32_t rank, world;     /* time-slab partition, 0 <= rank < world; n_t % world == 0  */
+    const void *nccl_id;     /* world > 1 (no MANUAL_HALO): 128-byte ncclUniqueId made by
+                                biot_nccl_unique_id on rank 0 and broadcast by the caller */
+    void *stream;            /* cudaStream_t to run on, or NULL => library-owned stream   */
+    uint32_t flags;          /* BIOT_FLAG_*                                               */
+    int32_t history;         /* iterations of residual history retained (>= 0; 0 => 1024) */
+} biot_opts;
+
+/* Read-only facts about a context. */
+typedef struct {
+    int32_t dim, n_comp;             /* d, d+1                                          */
+    int64_t n_nodes, n_dof;          /* N, N*(d+1)                                      */
+    int32_t n_t, n_t_local, first_step; /* global N_t; owned steps first_step..+n_t_local-1 */
+    int64_t iterations;              /* outer iterations done since setup               */
+    int32_t kernel_path;             /* 1 = BDIA stencil-offset, 2 = ELL explicit columns */
+    int32_t n_slots;                 /* neighbour slots per node                        */
+    double beta;                     /* the beta actually used                          */
+    double bytes_per_iter;           /* algorithmic bytes per outer iteration (this rank) */
+    double flops_per_iter;           /* algorithmic flops per outer iteration (this rank) */
+    double device_bytes;             /* device memory held by the context               */
+} biot_info;
+
+/* Build the operators on the host, upload, allocate the space-time panels
+ * (x^0 = 0 for all owned steps).  Collective for world > 1. */
+biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const biot_bc *bc,
+                       double dt, int32_t n_t, const biot_opts *opts, biot_ctx **out);
+
+/* Set x_n^0 for `count` consecutive owned steps starting at global step n
+ * (host, [count][n_dof] node-interleaved).  Dirichlet entries are forced to 0. */
+biot_status biot_set_iterate(biot_ctx *ctx, int32_t n, int32_t count, const double *x);
+
+/* Replace the load scales s_n (host, n_t values, global steps 1..n_t). */
+biot_status biot_set_load_scale(biot_ctx *ctx, const double *s);
+
+/* K outer iterations (K >= 0; K = 0 is a no-op).  Collective for world > 1. */
+biot_status biot_iterate(biot_ctx *ctx, int32_t K);
+
+/* Residual norms at the current iterate: out[n_t_local][2] = ||r_u||, ||r_p||
+ * of the owned steps (a residual-only pass, no update). */
+biot_status biot_residual_norms(biot_ctx *ctx, double *out);
+
+/* Norms of r(x^k) computed inside iteration k (k = 0-based count since setup):
+ * out[n_t_local][2].  BIOT_E_STATE if k was not run or is no longer retained. */
+biot_status biot_residual_history(biot_ctx *ctx, int64_t k, double *out);
+
+/* Current iterate of `count` consecutive owned steps from global step n
+ * (n = 0 returns x_0 on rank 0): out[count][n_dof] node-interleaved. */
+biot_status biot_solution(biot_ctx *ctx, int32_t n, int32_t count, double *out);
+
+/* Manual halo (BIOT_FLAG_MANUAL_HALO): copy the current iterate of the last
+ * owned step out (host, n_dof), and set the ghost (step first_step-1) in. */
+biot_status biot_last_slice(biot_ctx *ctx, double *out);
+biot_status biot_set_ghost(biot_ctx *ctx, const double *x);
+
+/* Host-only: the assembled per-step operators in node-interleaved global
+ * numbering, for inspection and tests (no device needed).  COO triplets of AA
+ * and A' restricted to free DoFs (explicit zeros dropped), the load f, and the
+ * inverse preconditioner diagonals (0 on Dirichlet DoFs).  Pass NULL arrays
+ * to query the counts first. */
+biot_status biot_assemble_host(const biot_mesh *mesh, const biot_material *mat,
+                               const biot_bc *bc, double dt,
+                               int64_t *nnz_AA, int64_t *AA_i, int64_t *AA_j, double *AA_v,
+                               int64_t *nnz_AP, int64_t *AP_i, int64_t *AP_j, double *AP_v,
+                               double *f, double *dinv);
+
+biot_status biot_get_info(const biot_ctx *ctx, biot_info *out);
+
+/* Device time of the kernels of the last biot_iterate call, per iteration,
+ * measured with CUDA events on the compute stream: out[0] = whole iteration,
+ * out[1] = the fused sweep kernel alone (ms). */
+biot_status biot_last_timing(const biot_ctx *ctx, double *out_ms);
+
+/* Fill out[128] with a fresh ncclUniqueId (rank 0 only; dlopens libnccl.so.2). */
+biot_status biot_nccl_unique_id(void *out);
+
+void biot_destroy(biot_ctx *ctx);
+const char *biot_last_error(const biot_ctx *ctx);
+const char *biot_status_string(biot_status s);
+int32_t biot_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BIOT_PIT_H */

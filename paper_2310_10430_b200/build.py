@@ -1,0 +1,71 @@
+"""Build libbiot_pit.so in-tree for sm_100a (nvcc cross-compiles without a GPU).
+
+    python -m paper_2310_10430_b200.build [--force]
+
+Writes paper_2310_10430_b200/libbiot_pit.so and the ptxas resource report
+paper_2310_10430_b200/build/ptxas.txt (registers / spills per kernel).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+OUT = os.path.join(HERE, "libbiot_pit.so")
+BUILD = os.path.join(HERE, "build")
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+SOURCES = ["host_assembly.cpp", "sweep_kernels.cu", "biot_api.cu"]
+HEADERS = ["host_assembly.h", "sweep_kernels.cuh"]
+
+
+def _stale() -> bool:
+    if not os.path.exists(OUT):
+        return True
+    t = os.path.getmtime(OUT)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    deps.append(os.path.join(HERE, "..", "include", "biot_pit.h"))
+    deps.append(os.path.abspath(__file__))
+    return any(os.path.getmtime(p) > t for p in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return OUT
+    os.makedirs(BUILD, exist_ok=True)
+    objs = []
+    report = []
+    for src in SOURCES:
+        path = os.path.join(CSRC, src)
+        obj = os.path.join(BUILD, src + ".o")
+        if src.endswith(".cu"):
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                   "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", path, "-o", obj]
+        else:
+            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-c", path, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        report.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError(f"compile failed: {src}")
+        objs.append(obj)
+    tmp = OUT + f".tmp{os.getpid()}"
+    cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
+           "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    report.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("link failed")
+    os.replace(tmp, OUT)
+    with open(os.path.join(BUILD, "ptxas.txt"), "w") as f:
+        f.write("\n".join(report))
+    if verbose:
+        print("\n".join(report))
+    return OUT
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -1,0 +1,680 @@
+// C-ABI of the B200 Biot solver (declared in include/biot_pit.h).
+//
+// One context per rank.  setup: host assembly (host_assembly.cpp) -> upload ->
+// two ping-pong space-time panels.  iterate(K): per outer iteration, optional
+// NCCL halo (ncclSend of the last local slice to rank+1, ncclRecv of the ghost
+// from rank-1; BASELINE.json north star (d), replacing the paper's MPI
+// Send/Recv pipeline of Algorithm 5), then the fused sweep
+// kernel (+ the P~1 second pass), then the deterministic norm finalize.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/biot_pit.h"
+#include "host_assembly.h"
+#include "sweep_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+// ---------------- NCCL, loaded at run time ----------------
+struct NcclApi {
+    void *h = nullptr;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi *nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *n : names) {
+            api.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+            if (api.h) break;
+        }
+        if (api.h) {
+            api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(api.h, "ncclGetUniqueId");
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(api.h, "ncclCommInitRank");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(api.h, "ncclCommDestroy");
+            api.Send = (decltype(api.Send))dlsym(api.h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(api.h, "ncclRecv");
+            api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+            if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.GroupStart ||
+                !api.GroupEnd || !api.CommDestroy)
+                api.h = nullptr;
+        }
+    }
+    return api.h ? &api : nullptr;
+}
+
+// panel gather/scatter between [count][N*nc] host-order staging and the panel
+__global__ void scatter_steps_kernel(const double *__restrict__ src, double *__restrict__ panel,
+                                     const uint8_t *__restrict__ fixed, int64_t nrows, int64_t pitch,
+                                     int t_first, int count) {
+    const int64_t total = nrows * count;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tt = k / nrows, row = k % nrows;
+        panel[row * pitch + t_first + tt] = fixed[row] ? 0.0 : src[k];
+    }
+}
+
+__global__ void gather_steps_kernel(const double *__restrict__ panel, double *__restrict__ dst,
+                                    int64_t nrows, int64_t pitch, int t_first, int count) {
+    const int64_t total = nrows * count;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t tt = k / nrows, row = k % nrows;
+        dst[k] = panel[row * pitch + t_first + tt];
+    }
+}
+
+}  // namespace
+
+struct biot_ctx {
+    std::string err;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int d = 0, nc = 0;
+    int64_t N = 0, pad = 0, rows_alloc = 0;
+    int S = 0, path = 0;
+    int32_t n_t = 0, n_tl = 0, first_step = 1, rank = 0, world = 1;
+    int64_t pitch = 0;
+    uint32_t flags = 0;
+    int precond = 2;
+    double omega = 0.5;
+    double beta = 0.0;
+    int64_t nnz_AA = 0, nnz_AP = 0;
+    std::vector<int64_t> offsets;
+
+    double *xbase[2] = {nullptr, nullptr};
+    double *x[2] = {nullptr, nullptr};        // at node 0
+    double *zbase = nullptr, *z = nullptr;
+    double *ghost_base = nullptr, *ghost = nullptr;
+    double *blk = nullptr;
+    int32_t *cols = nullptr;
+    double *load = nullptr, *dinv = nullptr, *s = nullptr;
+    uint8_t *fixed = nullptr;
+    double *sendbuf = nullptr;
+    double *partial = nullptr;
+    double *hist = nullptr, *norms = nullptr;
+    int *nonfinite = nullptr;
+    double *staging = nullptr;
+    int64_t staging_steps = 0;
+    int cur = 0;
+    bool send_dirty = true;
+    int64_t iterations = 0;
+    int hist_cap = 1024;
+    biot::LaunchShape shape{0, 0};
+    int tw = 8, node_block = 8;
+    size_t device_bytes = 0;
+    ncclComm_t comm = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    std::vector<cudaEvent_t> ev_s;                 // 2 per iteration of the current call
+    double last_ms_iter = 0.0, last_ms_sweep = 0.0;
+};
+
+namespace {
+
+biot_status fail(biot_ctx *c, biot_status s, const std::string &m) {
+    if (c) c->err = m;
+    g_err = m;
+    return s;
+}
+
+#define CU(call)                                                                          \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(ctx, BIOT_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+biot_status dev_alloc(biot_ctx *ctx, void **p, size_t bytes) {
+    cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, BIOT_E_NOMEM, "cudaMalloc(" + std::to_string(bytes) + " B) failed: " +
+                                          cudaGetErrorString(e));
+    }
+    ctx->device_bytes += bytes;
+    return BIOT_OK;
+}
+
+#define ALLOC(ptr, bytes)                                                  \
+    do {                                                                   \
+        biot_status s_ = dev_alloc(ctx, (void **)&(ptr), (size_t)(bytes)); \
+        if (s_ != BIOT_OK) return s_;                                      \
+    } while (0)
+
+void free_all(biot_ctx *c) {
+    cudaSetDevice(c->device);
+    for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
+                    (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->dinv, (void *)c->s,
+                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
+                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging})
+        if (p) cudaFree(p);
+    for (cudaEvent_t e : {c->ev_a, c->ev_b})
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->ev_s) cudaEventDestroy(e);
+    if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+}
+
+biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xout) {
+    biot::SweepArgs a{};
+    a.x = xin;
+    a.xn = xout;
+    a.ghost = c->ghost;
+    a.blk = c->blk;
+    a.cols = c->cols;
+    a.load = c->load;
+    a.dinv = c->dinv;
+    a.s = c->s;
+    a.zbuf = c->z;
+    a.sendbuf = (c->world > 1 && mode != biot::MODE_RESIDUAL) ? c->sendbuf : nullptr;
+    a.partial = c->partial;
+    a.n_nodes = c->N;
+    a.pitch = c->pitch;
+    a.n_tl = c->n_tl;
+    a.tw = c->tw;
+    a.node_block = c->node_block;
+    a.mode = mode;
+    a.omega = c->omega;
+    for (int s = 0; s < 32; ++s) a.off[s] = s < (int)c->offsets.size() ? c->offsets[s] : 0;
+    return a;
+}
+
+biot_status pack_send(biot_ctx *ctx) {
+    // last local step of the current iterate -> contiguous send buffer
+    CU(cudaMemcpy2DAsync(ctx->sendbuf, sizeof(double), ctx->x[ctx->cur] + (ctx->n_tl - 1),
+                         ctx->pitch * sizeof(double), sizeof(double), (size_t)ctx->N * ctx->nc,
+                         cudaMemcpyDeviceToDevice, ctx->stream));
+    ctx->send_dirty = false;
+    return BIOT_OK;
+}
+
+biot_status halo_exchange(biot_ctx *ctx) {
+    if (ctx->world == 1 || (ctx->flags & BIOT_FLAG_MANUAL_HALO)) return BIOT_OK;
+    NcclApi *api = nccl();
+    if (!api || !ctx->comm) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
+    if (ctx->send_dirty) {
+        biot_status s = pack_send(ctx);
+        if (s != BIOT_OK) return s;
+    }
+    const size_t n = (size_t)ctx->N * ctx->nc;
+    ncclResult_t r = api->GroupStart();
+    if (r == ncclSuccess && ctx->rank + 1 < ctx->world)
+        r = api->Send(ctx->sendbuf, n, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->stream);
+    if (r == ncclSuccess && ctx->rank > 0)
+        r = api->Recv(ctx->ghost, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream);
+    ncclResult_t r2 = api->GroupEnd();
+    if (r != ncclSuccess || r2 != ncclSuccess)
+        return fail(ctx, BIOT_E_NCCL, std::string("NCCL halo exchange failed: ") +
+                                          (api->GetErrorString ? api->GetErrorString(r != ncclSuccess ? r : r2) : "?"));
+    return BIOT_OK;
+}
+
+biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
+    const bool timing = e0 != nullptr;
+    biot_status st = halo_exchange(ctx);
+    if (st != BIOT_OK) return st;
+    const double *xin = ctx->x[ctx->cur];
+    double *xout = ctx->x[1 - ctx->cur];
+    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+    biot::SweepArgs a = sweep_args(ctx, mode, xin, xout);
+    if (timing) CU(cudaEventRecord(e0, ctx->stream));
+    CU(biot::launch_sweep(ctx->d, ctx->path, ctx->S, a, ctx->shape, ctx->stream));
+    if (timing) CU(cudaEventRecord(e1, ctx->stream));
+    if (ctx->precond == 1) {
+        biot::Pass2Args p{};
+        p.x = xin;
+        p.xn = xout;
+        p.zbuf = ctx->z;
+        p.blk = ctx->blk;
+        p.cols = ctx->cols;
+        p.dinv = ctx->dinv;
+        p.sendbuf = a.sendbuf;
+        p.n_nodes = ctx->N;
+        p.pitch = ctx->pitch;
+        p.n_tl = ctx->n_tl;
+        p.tw = ctx->tw;
+        p.node_block = ctx->node_block;
+        p.omega = ctx->omega;
+        for (int s = 0; s < 32; ++s) p.off[s] = a.off[s];
+        CU(biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->shape.grid, ctx->stream));
+    }
+    double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
+    CU(biot::launch_finalize(ctx->partial, ctx->shape.grid, ctx->n_tl, hslot, ctx->nonfinite,
+                             ctx->stream));
+    ctx->cur = 1 - ctx->cur;
+    ctx->iterations++;
+    return BIOT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t biot_abi_version(void) { return BIOT_PIT_ABI_VERSION; }
+
+const char *biot_status_string(biot_status s) {
+    switch (s) {
+        case BIOT_OK: return "ok";
+        case BIOT_E_INVALID: return "invalid argument";
+        case BIOT_E_NOMEM: return "out of memory";
+        case BIOT_E_CUDA: return "CUDA error";
+        case BIOT_E_NCCL: return "NCCL error";
+        case BIOT_E_STATE: return "invalid state";
+        case BIOT_E_NONFINITE: return "non-finite residual";
+    }
+    return "unknown status";
+}
+
+const char *biot_last_error(const biot_ctx *ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+biot_status biot_nccl_unique_id(void *out) {
+    if (!out) return fail(nullptr, BIOT_E_INVALID, "out is NULL");
+    NcclApi *api = nccl();
+    if (!api) return fail(nullptr, BIOT_E_NCCL, "libnccl.so.2 could not be loaded");
+    ncclUniqueId id;
+    ncclResult_t r = api->GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, BIOT_E_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+    return BIOT_OK;
+}
+
+biot_status biot_assemble_host(const biot_mesh *mesh, const biot_material *mat, const biot_bc *bc,
+                               double dt, int64_t *nnz_AA, int64_t *AA_i, int64_t *AA_j,
+                               double *AA_v, int64_t *nnz_AP, int64_t *AP_i, int64_t *AP_j,
+                               double *AP_v, double *f, double *dinv) {
+    if (!mesh || !mat || !bc || !nnz_AA || !nnz_AP)
+        return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    biot::HostOperator op;
+    std::string m = biot::assemble(*mesh, *mat, *bc, dt, op);
+    if (!m.empty()) return fail(nullptr, BIOT_E_INVALID, m);
+    *nnz_AA = op.nnz_AA;
+    *nnz_AP = op.nnz_AP;
+    const int nc = op.nc, d = op.d, S = op.n_slots, W = biot::block_width(nc);
+    if (AA_i && AA_j && AA_v && AP_i && AP_j && AP_v) {
+        int64_t ka = 0, kp = 0;
+        for (int64_t i = 0; i < op.n_nodes; ++i)
+            for (int s = 0; s < S; ++s) {
+                int64_t j = op.path == biot::PATH_BDIA ? i + op.offsets[s] : op.cols[(size_t)i * S + s];
+                if (j < 0 || j >= op.n_nodes) continue;
+                if (op.path == biot::PATH_BDIA) {   // skip duplicate padding slots
+                    bool dup = false;
+                    for (int s2 = 0; s2 < s; ++s2) dup |= (op.offsets[s2] == op.offsets[s]);
+                    if (dup) continue;
+                } else {
+                    bool dup = false;
+                    for (int s2 = 0; s2 < s; ++s2) dup |= (op.cols[(size_t)i * S + s2] == j);
+                    if (dup) continue;
+                }
+                const double *b = op.blk.data() + ((size_t)i * S + s) * W;
+                for (int c = 0; c < nc; ++c)
+                    for (int cc = 0; cc < nc; ++cc)
+                        if (b[c * nc + cc] != 0.0) {
+                            AA_i[ka] = i * nc + c;
+                            AA_j[ka] = j * nc + cc;
+                            AA_v[ka] = b[c * nc + cc];
+                            ka++;
+                        }
+                for (int cc = 0; cc < d; ++cc)
+                    if (b[d * nc + cc] != 0.0) {
+                        AP_i[kp] = i * nc + d;
+                        AP_j[kp] = j * nc + cc;
+                        AP_v[kp] = b[d * nc + cc];
+                        kp++;
+                    }
+                if (b[nc * nc] != 0.0) {
+                    AP_i[kp] = i * nc + d;
+                    AP_j[kp] = j * nc + d;
+                    AP_v[kp] = b[nc * nc];
+                    kp++;
+                }
+            }
+    }
+    if (f) std::memcpy(f, op.load.data(), op.load.size() * sizeof(double));
+    if (dinv) std::memcpy(dinv, op.dinv.data(), op.dinv.size() * sizeof(double));
+    return BIOT_OK;
+}
+
+biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const biot_bc *bc, double dt,
+                       int32_t n_t, const biot_opts *opts, biot_ctx **out) {
+    if (!out) return fail(nullptr, BIOT_E_INVALID, "out is NULL");
+    *out = nullptr;
+    if (!mesh || !mat || !bc || !opts) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    if (n_t < 1) return fail(nullptr, BIOT_E_INVALID, "n_t must be >= 1");
+    if (opts->precond != 1 && opts->precond != 2)
+        return fail(nullptr, BIOT_E_INVALID, "precond must be 1 (P~1) or 2 (P~2)");
+    if (!(opts->omega > 0.0) || !std::isfinite(opts->omega))
+        return fail(nullptr, BIOT_E_INVALID, "omega must be > 0");
+    if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world)
+        return fail(nullptr, BIOT_E_INVALID, "need 0 <= rank < world");
+    if (n_t % opts->world != 0)
+        return fail(nullptr, BIOT_E_INVALID, "n_t must be divisible by world (time slabs)");
+    if (opts->world > 1 && !(opts->flags & BIOT_FLAG_MANUAL_HALO) && !opts->nccl_id)
+        return fail(nullptr, BIOT_E_INVALID, "world > 1 needs nccl_id (or BIOT_FLAG_MANUAL_HALO)");
+    if (opts->history < 0) return fail(nullptr, BIOT_E_INVALID, "history must be >= 0");
+    if (bc->load_scale)
+        for (int32_t n = 0; n < n_t; ++n)
+            if (!std::isfinite(bc->load_scale[n]))
+                return fail(nullptr, BIOT_E_INVALID, "load_scale must be finite");
+
+    auto op = std::make_unique<biot::HostOperator>();
+    std::string m = biot::assemble(*mesh, *mat, *bc, dt, *op);
+    if (!m.empty()) return fail(nullptr, BIOT_E_INVALID, m);
+
+    std::unique_ptr<biot_ctx> holder(new biot_ctx());
+    biot_ctx *ctx = holder.get();
+    // any early return below releases what was acquired so far
+    struct Guard {
+        std::unique_ptr<biot_ctx> &h;
+        bool armed = true;
+        ~Guard() { if (armed && h) free_all(h.get()); }
+    } guard{holder};
+    ctx->device = opts->device;
+    CU(cudaSetDevice(ctx->device));
+    int cc_major = 0;
+    CU(cudaDeviceGetAttribute(&cc_major, cudaDevAttrComputeCapabilityMajor, ctx->device));
+    if (cc_major != 10)
+        return fail(ctx, BIOT_E_CUDA, "this build targets sm_100a (B200); device has CC major " +
+                                          std::to_string(cc_major));
+    ctx->d = op->d;
+    ctx->nc = op->nc;
+    ctx->N = op->n_nodes;
+    ctx->S = op->n_slots;
+    ctx->path = op->path;
+    ctx->offsets = op->offsets;
+    ctx->pad = op->path == biot::PATH_BDIA ? op->max_abs_offset : 0;
+    ctx->n_t = n_t;
+    ctx->rank = opts->rank;
+    ctx->world = opts->world;
+    ctx->n_tl = n_t / opts->world;
+    ctx->first_step = ctx->rank * ctx->n_tl + 1;
+    ctx->flags = opts->flags;
+    ctx->precond = opts->precond;
+    ctx->omega = opts->omega;
+    ctx->beta = op->beta;
+    ctx->nnz_AA = op->nnz_AA;
+    ctx->nnz_AP = op->nnz_AP;
+    ctx->hist_cap = opts->history > 0 ? opts->history : 1024;
+    ctx->pitch = ((int64_t)ctx->n_tl + biot::kChunk - 1) / biot::kChunk * biot::kChunk;
+    const int64_t nchunks = ctx->pitch / biot::kChunk;
+    ctx->tw = 1;
+    while (ctx->tw < 8 && ctx->tw < nchunks) ctx->tw *= 2;
+    ctx->node_block = 8;
+
+    if (opts->stream) {
+        ctx->stream = (cudaStream_t)opts->stream;
+    } else {
+        CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+        ctx->own_stream = true;
+    }
+    CU(cudaEventCreate(&ctx->ev_a));
+    CU(cudaEventCreate(&ctx->ev_b));
+
+    const int nc = ctx->nc;
+    const int W = biot::block_width(nc);
+    ctx->rows_alloc = (ctx->N + 2 * ctx->pad) * nc;
+    const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
+    for (int k = 0; k < 2; ++k) {
+        ALLOC(ctx->xbase[k], panel_bytes);
+        CU(cudaMemsetAsync(ctx->xbase[k], 0, panel_bytes, ctx->stream));
+        ctx->x[k] = ctx->xbase[k] + ctx->pad * nc * ctx->pitch;
+    }
+    if (ctx->precond == 1) {
+        ALLOC(ctx->zbase, panel_bytes);
+        CU(cudaMemsetAsync(ctx->zbase, 0, panel_bytes, ctx->stream));
+        ctx->z = ctx->zbase + ctx->pad * nc * ctx->pitch;
+    }
+    const size_t vec_bytes = (size_t)ctx->N * nc * sizeof(double);
+    ALLOC(ctx->ghost_base, (size_t)ctx->rows_alloc * sizeof(double));
+    CU(cudaMemsetAsync(ctx->ghost_base, 0, (size_t)ctx->rows_alloc * sizeof(double), ctx->stream));
+    ctx->ghost = ctx->ghost_base + ctx->pad * nc;
+    if (bc->x_initial && ctx->rank == 0) {
+        std::vector<double> x0(bc->x_initial, bc->x_initial + (size_t)ctx->N * nc);
+        for (size_t q = 0; q < x0.size(); ++q)
+            if (op->fixed[q]) x0[q] = 0.0;
+        CU(cudaMemcpy(ctx->ghost, x0.data(), vec_bytes, cudaMemcpyHostToDevice));
+    }
+    ALLOC(ctx->blk, op->blk.size() * sizeof(double));
+    CU(cudaMemcpy(ctx->blk, op->blk.data(), op->blk.size() * sizeof(double), cudaMemcpyHostToDevice));
+    if (ctx->path == biot::PATH_ELL) {
+        ALLOC(ctx->cols, op->cols.size() * sizeof(int32_t));
+        CU(cudaMemcpy(ctx->cols, op->cols.data(), op->cols.size() * sizeof(int32_t),
+                      cudaMemcpyHostToDevice));
+    }
+    ALLOC(ctx->load, vec_bytes);
+    CU(cudaMemcpy(ctx->load, op->load.data(), vec_bytes, cudaMemcpyHostToDevice));
+    ALLOC(ctx->dinv, vec_bytes);
+    CU(cudaMemcpy(ctx->dinv, op->dinv.data(), vec_bytes, cudaMemcpyHostToDevice));
+    ALLOC(ctx->fixed, (size_t)ctx->N * nc);
+    CU(cudaMemcpy(ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc, cudaMemcpyHostToDevice));
+    {
+        std::vector<double> sl(ctx->pitch, 0.0);
+        for (int32_t t = 0; t < ctx->n_tl; ++t)
+            sl[t] = bc->load_scale ? bc->load_scale[ctx->first_step - 1 + t] : 1.0;
+        ALLOC(ctx->s, sl.size() * sizeof(double));
+        CU(cudaMemcpy(ctx->s, sl.data(), sl.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    ALLOC(ctx->sendbuf, vec_bytes);
+    CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
+
+    const int nwp = 8 / ctx->tw;
+    ctx->shape.smem = (size_t)nwp * ctx->pitch * 2 * sizeof(double);
+    CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));
+    ALLOC(ctx->partial, (size_t)ctx->shape.grid * ctx->n_tl * 2 * sizeof(double));
+    ALLOC(ctx->hist, (size_t)ctx->hist_cap * ctx->n_tl * 2 * sizeof(double));
+    ALLOC(ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double));
+    ALLOC(ctx->nonfinite, sizeof(int));
+    CU(cudaMemsetAsync(ctx->nonfinite, 0, sizeof(int), ctx->stream));
+    ctx->staging_steps = std::max<int64_t>(1, std::min<int64_t>(ctx->n_tl, (256ll << 20) / (int64_t)vec_bytes));
+    ALLOC(ctx->staging, (size_t)ctx->staging_steps * vec_bytes);
+
+    if (ctx->world > 1 && !(ctx->flags & BIOT_FLAG_MANUAL_HALO)) {
+        NcclApi *api = nccl();
+        if (!api) return fail(ctx, BIOT_E_NCCL, "libnccl.so.2 could not be loaded");
+        ncclUniqueId id;
+        std::memcpy(&id, opts->nccl_id, sizeof(id));
+        ncclResult_t r = api->CommInitRank(&ctx->comm, ctx->world, id, ctx->rank);
+        if (r != ncclSuccess)
+            return fail(ctx, BIOT_E_NCCL, std::string("ncclCommInitRank: ") +
+                                              (api->GetErrorString ? api->GetErrorString(r) : "?"));
+    }
+    CU(cudaStreamSynchronize(ctx->stream));
+    guard.armed = false;
+    *out = holder.release();
+    return BIOT_OK;
+}
+
+biot_status biot_set_iterate(biot_ctx *ctx, int32_t n, int32_t count, const double *x) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!x || count < 0) return fail(ctx, BIOT_E_INVALID, "x is NULL or count < 0");
+    if (n < ctx->first_step || n + count > ctx->first_step + ctx->n_tl)
+        return fail(ctx, BIOT_E_INVALID, "steps outside the owned slab");
+    CU(cudaSetDevice(ctx->device));
+    const int64_t rows = ctx->N * ctx->nc;
+    const size_t vb = (size_t)rows * sizeof(double);
+    for (int32_t done = 0; done < count;) {
+        const int32_t m = (int32_t)std::min<int64_t>(ctx->staging_steps, count - done);
+        CU(cudaMemcpyAsync(ctx->staging, x + (size_t)done * rows, (size_t)m * vb, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        const int t_first = n - ctx->first_step + done;
+        scatter_steps_kernel<<<1184, 256, 0, ctx->stream>>>(ctx->staging, ctx->x[ctx->cur], ctx->fixed,
+                                                            rows, ctx->pitch, t_first, m);
+        CU(cudaGetLastError());
+        done += m;
+    }
+    ctx->send_dirty = true;
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BIOT_OK;
+}
+
+biot_status biot_set_load_scale(biot_ctx *ctx, const double *s) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!s) return fail(ctx, BIOT_E_INVALID, "s is NULL");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpyAsync(ctx->s, s + (ctx->first_step - 1), (size_t)ctx->n_tl * sizeof(double),
+                       cudaMemcpyHostToDevice, ctx->stream));
+    return BIOT_OK;
+}
+
+biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
+    if (K == 0) return BIOT_OK;
+    CU(cudaSetDevice(ctx->device));
+    while ((int32_t)ctx->ev_s.size() < 2 * K) {
+        cudaEvent_t e;
+        CU(cudaEventCreate(&e));
+        ctx->ev_s.push_back(e);
+    }
+    CU(cudaEventRecord(ctx->ev_a, ctx->stream));
+    for (int32_t k = 0; k < K; ++k) {
+        biot_status s = one_iteration(ctx, ctx->ev_s[2 * k], ctx->ev_s[2 * k + 1]);
+        if (s != BIOT_OK) return s;
+    }
+    CU(cudaEventRecord(ctx->ev_b, ctx->stream));
+    CU(cudaEventSynchronize(ctx->ev_b));
+    float tot = 0.f;
+    CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
+    double sweep_ms = 0.0;
+    for (int32_t k = 0; k < K; ++k) {
+        float ms = 0.f;
+        CU(cudaEventElapsedTime(&ms, ctx->ev_s[2 * k], ctx->ev_s[2 * k + 1]));
+        sweep_ms += ms;
+    }
+    ctx->last_ms_iter = tot / K;
+    ctx->last_ms_sweep = sweep_ms / K;
+    int nf = 0;
+    CU(cudaMemcpy(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+    if (nf) return fail(ctx, BIOT_E_NONFINITE, "a residual norm became non-finite");
+    return BIOT_OK;
+}
+
+biot_status biot_residual_norms(biot_ctx *ctx, double *out) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!out) return fail(ctx, BIOT_E_INVALID, "out is NULL");
+    CU(cudaSetDevice(ctx->device));
+    biot_status st = halo_exchange(ctx);
+    if (st != BIOT_OK) return st;
+    biot::SweepArgs a = sweep_args(ctx, biot::MODE_RESIDUAL, ctx->x[ctx->cur], nullptr);
+    CU(biot::launch_sweep(ctx->d, ctx->path, ctx->S, a, ctx->shape, ctx->stream));
+    CU(biot::launch_finalize(ctx->partial, ctx->shape.grid, ctx->n_tl, ctx->norms, ctx->nonfinite,
+                             ctx->stream));
+    CU(cudaMemcpyAsync(out, ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BIOT_OK;
+}
+
+biot_status biot_residual_history(biot_ctx *ctx, int64_t k, double *out) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!out) return fail(ctx, BIOT_E_INVALID, "out is NULL");
+    if (k < 0 || k >= ctx->iterations || k < ctx->iterations - ctx->hist_cap)
+        return fail(ctx, BIOT_E_STATE, "iteration " + std::to_string(k) + " not retained");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpyAsync(out, ctx->hist + (size_t)(k % ctx->hist_cap) * ctx->n_tl * 2,
+                       (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BIOT_OK;
+}
+
+biot_status biot_solution(biot_ctx *ctx, int32_t n, int32_t count, double *out) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!out || count < 0) return fail(ctx, BIOT_E_INVALID, "out is NULL or count < 0");
+    CU(cudaSetDevice(ctx->device));
+    const int64_t rows = ctx->N * ctx->nc;
+    const size_t vb = (size_t)rows * sizeof(double);
+    if (n == ctx->first_step - 1 && count == 1) {   // the ghost / x_0
+        CU(cudaMemcpyAsync(out, ctx->ghost, vb, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return BIOT_OK;
+    }
+    if (n < ctx->first_step || n + count > ctx->first_step + ctx->n_tl)
+        return fail(ctx, BIOT_E_INVALID, "steps outside the owned slab");
+    for (int32_t done = 0; done < count;) {
+        const int32_t m = (int32_t)std::min<int64_t>(ctx->staging_steps, count - done);
+        const int t_first = n - ctx->first_step + done;
+        gather_steps_kernel<<<1184, 256, 0, ctx->stream>>>(ctx->x[ctx->cur], ctx->staging, rows,
+                                                           ctx->pitch, t_first, m);
+        CU(cudaGetLastError());
+        CU(cudaMemcpyAsync(out + (size_t)done * rows, ctx->staging, (size_t)m * vb, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        done += m;
+    }
+    return BIOT_OK;
+}
+
+biot_status biot_last_slice(biot_ctx *ctx, double *out) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    return biot_solution(ctx, ctx->first_step + ctx->n_tl - 1, 1, out);
+}
+
+biot_status biot_set_ghost(biot_ctx *ctx, const double *x) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!x) return fail(ctx, BIOT_E_INVALID, "x is NULL");
+    if (ctx->rank == 0 && ctx->world > 1)
+        return fail(ctx, BIOT_E_STATE, "rank 0's ghost is x_0 (fixed)");
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMemcpyAsync(ctx->ghost, x, (size_t)ctx->N * ctx->nc * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    return BIOT_OK;
+}
+
+biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
+    if (!ctx || !o) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    o->dim = ctx->d;
+    o->n_comp = ctx->nc;
+    o->n_nodes = ctx->N;
+    o->n_dof = ctx->N * ctx->nc;
+    o->n_t = ctx->n_t;
+    o->n_t_local = ctx->n_tl;
+    o->first_step = ctx->first_step;
+    o->iterations = ctx->iterations;
+    o->kernel_path = ctx->path;
+    o->n_slots = ctx->S;
+    o->beta = ctx->beta;
+    const double st = (double)ctx->N * ctx->nc * ctx->n_tl;
+    o->bytes_per_iter = 16.0 * st + 8.0 * (double)(ctx->nnz_AA + ctx->nnz_AP);
+    o->flops_per_iter = 2.0 * (double)(ctx->nnz_AA + ctx->nnz_AP) * ctx->n_tl;
+    o->device_bytes = (double)ctx->device_bytes;
+    return BIOT_OK;
+}
+
+biot_status biot_last_timing(const biot_ctx *ctx, double *out_ms) {
+    if (!ctx || !out_ms) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    out_ms[0] = ctx->last_ms_iter;
+    out_ms[1] = ctx->last_ms_sweep;
+    return BIOT_OK;
+}
+
+void biot_destroy(biot_ctx *ctx) {
+    if (!ctx) return;
+    free_all(ctx);
+    delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,375 @@
+// Hot-path kernels: one outer iteration of the inverted time-stepping scheme
+// over all local time steps at once (Algorithm 2, Jacobi in
+// time per BASELINE.json), fused with the block preconditioner (L238-262), the
+// damped update and the per-step residual-norm reduction.  sm_100a, fp64.
+//
+// Data layout (HBM): the space-time iterate is a "panel" with one row per
+// (node, component) and the local time steps contiguous in the row:
+//     x[(i*nc + c)*pitch + t]
+// so each operator entry multiplies a contiguous, 16-B-vectorised, coalesced run
+// of time steps (lane l of a warp owns steps t0..t0+3, t0 = chunk*128 + 4l).
+// The operator is stored as (d+1)x(d+1) node blocks per neighbour slot, read
+// with warp-uniform loads (one L1 transaction serves all 32 lanes); every
+// gathered x value feeds d+2 FMAs (d+1 block rows + the previous-step row).
+//
+// Previous-step coupling A' x_{n-1} is fused without reloading x at t-1: each
+// lane accumulates q(t) = (A' x_t)_p for its own steps and the output at t uses
+// q(t-1), taken from the neighbouring lane by one shuffle; lane 0 recomputes
+// q(t0-1) in the same FMA order (bitwise identical), reading the ghost step
+// (the last step of the previous time slab, or x_0) when t0 = 0.
+#include "sweep_kernels.cuh"
+
+#include <cmath>
+
+
+namespace biot {
+
+namespace {
+
+constexpr int kSlotUnroll = 1;   // slot loop kept rolled: bounded registers, no spills
+
+template <int S, bool ELL>
+__device__ __forceinline__ int64_t column(const int32_t *__restrict__ cols, const int64_t *off,
+                                          int64_t i, int s) {
+    if constexpr (ELL) return (int64_t)__ldg(cols + i * S + s);
+    else return i + off[s];
+}
+
+template <int D, int S, bool ELL>
+__device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, int t0, int lane,
+                                            const double (&sv)[kT], double (&nu)[kT],
+                                            double (&npn)[kT]) {
+    constexpr int NC = D + 1;
+    constexpr int W = NC * NC + 1;
+    const int64_t P = a.pitch;
+    const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
+
+    double acc[NC][kT], q[kT];
+#pragma unroll
+    for (int tt = 0; tt < kT; ++tt) {
+        q[tt] = 0.0;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c][tt] = 0.0;
+    }
+
+#pragma unroll(kSlotUnroll)
+    for (int s = 0; s < S; ++s) {
+        const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
+        const double *__restrict__ xj = a.x + j * NC * P + t0;
+        double cf[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) cf[k] = __ldg(bp + s * W + k);
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+            const double2 v01 = __ldg(reinterpret_cast<const double2 *>(xj + cc * P));
+            const double2 v23 = __ldg(reinterpret_cast<const double2 *>(xj + cc * P + 2));
+            const double v[kT] = {v01.x, v01.y, v23.x, v23.y};
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf[c * NC + cc], v[tt], acc[c][tt]);
+            const double qc = (cc < D) ? cf[D * NC + cc] : cf[NC * NC];
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(qc, v[tt], q[tt]);
+        }
+    }
+
+    // previous-step coupling for the lane's first step
+    double qprev = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
+    if (lane == 0) {
+        double qg = 0.0;
+        const bool use_ghost = (t0 == 0);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
+            const double *src = use_ghost ? (a.ghost + j * NC) : (a.x + j * NC * P + (t0 - 1));
+            const int64_t stride = use_ghost ? 1 : P;
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc) {
+                const double qc = (cc < D) ? __ldg(bp + s * W + D * NC + cc) : __ldg(bp + s * W + NC * NC);
+                qg = fma(qc, __ldg(src + cc * stride), qg);
+            }
+        }
+        qprev = qg;
+    }
+
+    double F[NC], Dv[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        F[c] = __ldg(a.load + i * NC + c);
+        Dv[c] = __ldg(a.dinv + i * NC + c);
+    }
+    const int mode = a.mode;
+    const double omega = a.omega;
+    double xs[NC][kT];   // own x_i(t0..t0+3): reloaded (L1 hit) instead of held across the slot loop
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        const double *src = a.x + (i * NC + c) * P + t0;
+        const double2 v01 = __ldg(reinterpret_cast<const double2 *>(src));
+        const double2 v23 = __ldg(reinterpret_cast<const double2 *>(src + 2));
+        xs[c][0] = v01.x; xs[c][1] = v01.y; xs[c][2] = v23.x; xs[c][3] = v23.y;
+    }
+    double outx[NC][kT], outz[NC][kT];
+#pragma unroll
+    for (int tt = 0; tt < kT; ++tt) {
+        const double qp = (tt == 0) ? qprev : q[tt - 1];
+        double r[NC];
+#pragma unroll
+        for (int c = 0; c < D; ++c) r[c] = sv[tt] * F[c] - acc[c][tt];
+        r[D] = (sv[tt] * F[D] + qp) - acc[D][tt];
+        double su = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) su = fma(r[c], r[c], su);
+        nu[tt] += su;
+        npn[tt] = fma(r[D], r[D], npn[tt]);
+        double z[NC];
+#pragma unroll
+        for (int c = 0; c < D; ++c) z[c] = Dv[c] * r[c];
+        z[D] = -(Dv[D] * r[D]);   // P~2 pressure part; P~1 finishes it in pass 2
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            outx[c][tt] = fma(omega, z[c], xs[c][tt]);
+            outz[c][tt] = (c < D) ? z[c] : r[D];
+        }
+    }
+    if (mode == MODE_RESIDUAL) return;
+
+    const int n_tl = a.n_tl;
+    const int ncw = (mode == MODE_UPDATE_P2) ? NC : D;   // P~1: pressure written by pass 2
+    const bool full = (t0 + kT <= n_tl);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        if (c >= ncw) break;
+        double *dst = a.xn + (i * NC + c) * P + t0;
+        if (full) {
+            *reinterpret_cast<double2 *>(dst) = make_double2(outx[c][0], outx[c][1]);
+            *reinterpret_cast<double2 *>(dst + 2) = make_double2(outx[c][2], outx[c][3]);
+        } else {
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt)
+                if (t0 + tt < n_tl) dst[tt] = outx[c][tt];
+        }
+    }
+    if (mode == MODE_P1_PASS1) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            double *dst = a.zbuf + (i * NC + c) * P + t0;
+            if (full) {
+                *reinterpret_cast<double2 *>(dst) = make_double2(outz[c][0], outz[c][1]);
+                *reinterpret_cast<double2 *>(dst + 2) = make_double2(outz[c][2], outz[c][3]);
+            } else {
+#pragma unroll
+                for (int tt = 0; tt < kT; ++tt)
+                    if (t0 + tt < n_tl) dst[tt] = outz[c][tt];
+            }
+        }
+    }
+    if (a.sendbuf) {
+        const int tl = n_tl - 1 - t0;
+        if (tl >= 0 && tl < kT) {
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt)
+                if (tt == tl)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+                        if (c < ncw) a.sendbuf[i * NC + c] = outx[c][tt];
+        }
+    }
+}
+
+template <int D, int S, bool ELL>
+__global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const SweepArgs a) {
+    extern __shared__ double red[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tw = a.tw, nwp = (kThreads / 32) / tw;
+    const int cw = warp % tw, nw = warp / tw;
+    const int n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    const int n_tlp = n_chunks * kChunk;
+    const int64_t N = a.n_nodes;
+    const int64_t nb = a.node_block;
+
+    for (int chunk = cw; chunk < n_chunks; chunk += tw) {
+        const int t0 = chunk * kChunk + lane * kT;
+        double nu[kT], npn[kT], sv[kT];
+#pragma unroll
+        for (int tt = 0; tt < kT; ++tt) {
+            nu[tt] = 0.0;
+            npn[tt] = 0.0;
+            sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
+        }
+        for (int64_t b = blockIdx.x; b * nb < N; b += gridDim.x) {
+            const int64_t i_end = min(N, (b + 1) * nb);
+            for (int64_t i = b * nb + nw; i < i_end; i += nwp)
+                node_update<D, S, ELL>(a, i, t0, lane, sv, nu, npn);
+        }
+#pragma unroll
+        for (int tt = 0; tt < kT; ++tt) {
+            red[((int64_t)nw * n_tlp + t0 + tt) * 2 + 0] = nu[tt];
+            red[((int64_t)nw * n_tlp + t0 + tt) * 2 + 1] = npn[tt];
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < a.n_tl; t += kThreads) {
+        double su = 0.0, sp = 0.0;
+        for (int w = 0; w < nwp; ++w) {
+            su += red[((int64_t)w * n_tlp + t) * 2 + 0];
+            sp += red[((int64_t)w * n_tlp + t) * 2 + 1];
+        }
+        a.partial[((int64_t)blockIdx.x * a.n_tl + t) * 2 + 0] = su;
+        a.partial[((int64_t)blockIdx.x * a.n_tl + t) * 2 + 1] = sp;
+    }
+}
+
+// P~1 second pass (PAPER.md eq. p1: z_p = S~p^{-1} (B^T z_u - r_p)).
+template <int D, int S, bool ELL>
+__global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
+    constexpr int NC = D + 1;
+    constexpr int W = NC * NC + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tw = a.tw, nwp = (kThreads / 32) / tw;
+    const int cw = warp % tw, nw = warp / tw;
+    const int n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    const int64_t N = a.n_nodes, P = a.pitch, nb = a.node_block;
+    const int n_tl = a.n_tl;
+    for (int chunk = cw; chunk < n_chunks; chunk += tw) {
+        const int t0 = chunk * kChunk + lane * kT;
+        for (int64_t b = blockIdx.x; b * nb < N; b += gridDim.x) {
+            const int64_t i_end = min(N, (b + 1) * nb);
+            for (int64_t i = b * nb + nw; i < i_end; i += nwp) {
+                const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
+                double bt[kT] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
+#pragma unroll
+                    for (int cc = 0; cc < D; ++cc) {
+                        const double cf = __ldg(bp + s * W + D * NC + cc);
+                        const double *src = a.zbuf + (j * NC + cc) * P + t0;
+                        const double2 v01 = __ldg(reinterpret_cast<const double2 *>(src));
+                        const double2 v23 = __ldg(reinterpret_cast<const double2 *>(src + 2));
+                        bt[0] = fma(cf, v01.x, bt[0]);
+                        bt[1] = fma(cf, v01.y, bt[1]);
+                        bt[2] = fma(cf, v23.x, bt[2]);
+                        bt[3] = fma(cf, v23.y, bt[3]);
+                    }
+                }
+                const double dv = __ldg(a.dinv + i * NC + D);
+                const double *rp = a.zbuf + (i * NC + D) * P + t0;
+                const double *xp = a.x + (i * NC + D) * P + t0;
+                double *dst = a.xn + (i * NC + D) * P + t0;
+#pragma unroll
+                for (int tt = 0; tt < kT; ++tt) {
+                    if (t0 + tt < n_tl) {
+                        const double zp = dv * (bt[tt] - rp[tt]);
+                        const double v = fma(a.omega, zp, xp[tt]);
+                        dst[tt] = v;
+                        if (a.sendbuf && t0 + tt == n_tl - 1) a.sendbuf[i * NC + D] = v;
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Deterministic second stage of the norm reduction: fixed split of the groups
+// over 8 y-lanes, then a fixed-order sum of the 8 lane totals.
+__global__ void finalize_kernel(const double *__restrict__ partial, int groups, int n_tl,
+                                double *__restrict__ norms, int *nonfinite) {
+    __shared__ double sm[8][32][2];
+    const int t = blockIdx.x * 32 + threadIdx.x;
+    const int y = threadIdx.y;
+    double su = 0.0, sp = 0.0;
+    if (t < n_tl) {
+        for (int g = y; g < groups; g += 8) {
+            su += partial[((int64_t)g * n_tl + t) * 2 + 0];
+            sp += partial[((int64_t)g * n_tl + t) * 2 + 1];
+        }
+    }
+    sm[y][threadIdx.x][0] = su;
+    sm[y][threadIdx.x][1] = sp;
+    __syncthreads();
+    if (y == 0 && t < n_tl) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            a += sm[k][threadIdx.x][0];
+            b += sm[k][threadIdx.x][1];
+        }
+        a = sqrt(a);
+        b = sqrt(b);
+        norms[t * 2 + 0] = a;
+        norms[t * 2 + 1] = b;
+        if (!isfinite(a) || !isfinite(b)) atomicOr(nonfinite, 1);
+    }
+}
+
+using SweepFn = void (*)(const SweepArgs);
+using Pass2Fn = void (*)(const Pass2Args);
+
+bool pick(int dim, int path, int S, SweepFn *sf, Pass2Fn *pf) {
+#define BIOT_CASE(D_, S_, ELL_)              \
+    if (dim == D_ && S == S_ && (path == 2) == ELL_) { \
+        *sf = sweep_kernel<D_, S_, ELL_>;   \
+        *pf = pass2_kernel<D_, S_, ELL_>;   \
+        return true;                          \
+    }
+    BIOT_CASE(2, 7, false)
+    BIOT_CASE(3, 15, false)
+    BIOT_CASE(2, 8, true)
+    BIOT_CASE(2, 16, true)
+    BIOT_CASE(2, 32, true)
+    BIOT_CASE(3, 8, true)
+    BIOT_CASE(3, 16, true)
+    BIOT_CASE(3, 32, true)
+#undef BIOT_CASE
+    return false;
+}
+
+}  // namespace
+
+cudaError_t sweep_shape(int dim, int path, int n_slots, int device, LaunchShape *out) {
+    SweepFn sf;
+    Pass2Fn pf;
+    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    int sms = 0;
+    cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (e != cudaSuccess) return e;
+    const size_t smem = out->smem;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sf, kThreads, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    out->grid = sms * per_sm;
+    return cudaSuccess;
+}
+
+cudaError_t launch_sweep(int dim, int path, int n_slots, const SweepArgs &a, const LaunchShape &sh,
+                         cudaStream_t st) {
+    SweepFn sf;
+    Pass2Fn pf;
+    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    sf<<<sh.grid, kThreads, sh.smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int grid,
+                         cudaStream_t st) {
+    SweepFn sf;
+    Pass2Fn pf;
+    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    pf<<<grid, kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
+                            int *nonfinite, cudaStream_t st) {
+    dim3 block(32, 8);
+    dim3 grid((n_tl + 31) / 32);
+    finalize_kernel<<<grid, block, 0, st>>>(partial, groups, n_tl, norms, nonfinite);
+    return cudaGetLastError();
+}
+
+}  // namespace biot

@@ -1,0 +1,70 @@
+// Hot-path kernels of the B200 Biot solver (sm_100a, fp64, no tensor cores).
+// Internal header shared by sweep_kernels.cu and biot_api.cu.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace biot {
+
+constexpr int kThreads = 256;   // 8 warps per CTA
+constexpr int kT = 4;           // consecutive time steps per lane (2 x 16-B loads)
+constexpr int kChunk = 32 * kT; // time steps per warp chunk
+
+enum SweepMode : int {
+    MODE_UPDATE_P2 = 0,   // fused residual + P~2 + update + norms
+    MODE_P1_PASS1 = 1,    // residual, x_u update, Z = (z_u, r_p), norms
+    MODE_RESIDUAL = 2,    // residual norms only (no writes)
+};
+
+struct SweepArgs {
+    const double *x;        // panel of x^k at node 0: x[(i*nc + c)*pitch + t]; padded nodes around
+    double *xn;             // panel of x^{k+1} (same layout)
+    const double *ghost;    // x_{first-1}^k, [i*nc + c] at node 0 (padded)
+    const double *blk;      // operator blocks [i][slot][W]
+    const int32_t *cols;    // ELL columns [i][slot] (null for BDIA)
+    const double *load;     // f [i*nc + c]
+    const double *dinv;     // inverse preconditioner diagonals [i*nc + c]
+    const double *s;        // load scales of the local steps [n_tl]
+    double *zbuf;           // P~1: Z panel (z_u in u rows, r_p in p row)
+    double *sendbuf;        // x^{k+1} of the last local step [i*nc + c] (null: not needed)
+    double *partial;        // per-CTA norm partials [gridDim.x][n_tl][2]
+    int64_t n_nodes;
+    int64_t pitch;          // doubles per (node, component) row; multiple of kChunk
+    int32_t n_tl;           // local time steps
+    int32_t tw;             // chunk-warps per CTA (power of two dividing 8)
+    int32_t node_block;     // consecutive nodes per CTA work block
+    int32_t mode;
+    double omega;
+    int64_t off[32];        // BDIA column offsets (slot 0 = self)
+};
+
+struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
+    const double *x;
+    double *xn;
+    const double *zbuf;
+    const double *blk;
+    const int32_t *cols;
+    const double *dinv;
+    double *sendbuf;
+    int64_t n_nodes, pitch;
+    int32_t n_tl, tw, node_block;
+    double omega;
+    int64_t off[32];
+};
+
+struct LaunchShape {
+    int grid;
+    size_t smem;
+};
+
+// dim in {2,3}; path 1 = BDIA, 2 = ELL; n_slots must match the instantiations.
+cudaError_t sweep_shape(int dim, int path, int n_slots, int device, LaunchShape *out);
+cudaError_t launch_sweep(int dim, int path, int n_slots, const SweepArgs &a, const LaunchShape &sh,
+                         cudaStream_t st);
+cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int grid,
+                         cudaStream_t st);
+// norms[t][k] = sqrt(sum_g partial[g][t][k]) in fixed g order; flags non-finite values
+cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
+                            int *nonfinite, cudaStream_t st);
+
+}  // namespace biot

@@ -1,0 +1,98 @@
+"""GPU properties that hold at any size (needs a B200).
+
+* iterate(a); iterate(b) == iterate(a+b) bitwise; run-to-run bitwise;
+* time-slab decomposition (world = 2, 4, 8 contexts, halo moved by the host)
+  gives x^K bitwise equal to one slab -- the multi-GPU contract checked on one
+  GPU without kernels that wait on each other;
+* front invariant at full size (config 3): x^0 = 0, s = 1 -> x_n^K == x_K^K, n >= K;
+* monotone residual history at full size with metric inputs;
+* degenerate inputs: K = 0, all DoFs Dirichlet, S = 0.
+"""
+import numpy as np
+import pytest
+
+from paper_2310_10430_b200 import BiotSolver, FLAG_MANUAL_HALO
+from workloads import config_problem, make_problem, initial_iterate, load_scales
+
+pytestmark = pytest.mark.gpu
+
+
+def _seeded(prob, nt, **kw):
+    s = load_scales(nt, parity=True)
+    g = BiotSolver(prob, n_t=nt, load_scale=s, **kw)
+    g.set_iterate(g.first_step, initial_iterate(prob.dirichlet, np.arange(g.first_step, g.first_step + g.n_tl),
+                                                prob.x0_seed))
+    return g
+
+
+@pytest.mark.parametrize("precond", [1, 2])
+def test_additive_and_deterministic(precond):
+    prob = config_problem(2)
+    g1 = _seeded(prob, prob.n_t, precond=precond)
+    g1.iterate(3); g1.iterate(4)
+    g2 = _seeded(prob, prob.n_t, precond=precond)
+    g2.iterate(7)
+    assert np.array_equal(g1.solution(), g2.solution())
+    for k in range(7):
+        assert np.array_equal(g1.residual_history(k), g2.residual_history(k))
+    assert np.array_equal(g1.residual_norms(), g2.residual_norms())
+    g0 = _seeded(prob, prob.n_t, precond=precond)
+    x_before = g0.solution()
+    g0.iterate(0)
+    assert np.array_equal(g0.solution(), x_before)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("precond", [2, 1])
+def test_time_slabs_bitwise(world, precond):
+    prob = config_problem(2)
+    nt, K = prob.n_t, 9
+    ref = _seeded(prob, nt, precond=precond)
+    ref.iterate(K)
+    xr = ref.solution()
+    ranks = [_seeded(prob, nt, precond=precond, rank=r, world=world, flags=FLAG_MANUAL_HALO)
+             for r in range(world)]
+    for _ in range(K):
+        slices = [g.last_slice() for g in ranks]
+        for r in range(1, world):
+            ranks[r].set_ghost(slices[r - 1])
+        for g in ranks:
+            g.iterate(1)
+    xs = np.concatenate([g.solution() for g in ranks])
+    assert np.array_equal(xs, xr)
+    # norms agree to rounding (reduction grouping depends on the slab length)
+    hs = np.concatenate([g.residual_history(K - 1) for g in ranks])
+    assert np.allclose(hs, ref.residual_history(K - 1), rtol=1e-12, atol=0)
+
+
+def test_front_invariant_full_config3():
+    prob = config_problem(3)
+    g = BiotSolver(prob, precond=2, omega=0.5)
+    K = 5
+    g.iterate(K)
+    x = g.solution(K, 40)
+    for r in range(1, 40):
+        assert np.array_equal(x[r], x[0])
+    xl = g.solution(prob.n_t - 3, 4)
+    assert np.array_equal(xl[-1], x[0])
+    assert not np.array_equal(g.solution(K - 1, 1)[0], x[0])
+
+
+@pytest.mark.parametrize("cid", [2, 3])
+def test_monotone_history_metric_inputs(cid):
+    prob = config_problem(cid)
+    g = BiotSolver(prob, precond=2, omega=0.5)
+    g.iterate(prob.K)
+    tot = np.array([np.sqrt((g.residual_history(k) ** 2).sum()) for k in range(prob.K)])
+    assert np.all(np.diff(tot) <= 0) and tot[-1] < 0.5 * tot[0]
+    fin = np.sqrt((g.residual_norms() ** 2).sum())
+    assert fin <= tot[-1]
+
+
+def test_all_dirichlet_and_zero_storage():
+    prob = make_problem(2, 6, 8, 0.1, 3, storage=0.0)
+    prob.dirichlet = np.ones_like(prob.dirichlet)
+    g = _seeded(prob, 8)
+    g.iterate(3)
+    assert np.abs(g.solution()).max() == 0.0
+    assert np.abs(g.residual_norms()).max() == 0.0

@@ -1,0 +1,173 @@
+"""GPU (libbiot_pit.so, sm_100a) vs oracle parity -- needs a B200.
+
+Tolerance: 1e-9 max relative error per field (BASELINE.json north star,
+normwise per reading R17) on x^K, the fused residual history and the
+residual norms at x^K.  Inputs: seeded x^0 ~ N(0,1) on free DoFs and
+s_n = 1 + 0.1 sin n (DESIGN.md input recipe), both preconditioners and two
+values of omega.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2310_10430_b200 import BiotSolver, FLAG_MANUAL_HALO
+from workloads import config_problem, make_problem, initial_iterate, load_scales
+
+from _parity import TOL, field_errors, norm_errors, subbox, oracle_window
+
+pytestmark = pytest.mark.gpu
+
+
+def _x0(prob, steps):
+    return initial_iterate(prob.dirichlet, steps, prob.x0_seed)
+
+
+def _run_full(prob, K, precond, omega, nt=None):
+    nt = prob.n_t if nt is None else nt
+    s = load_scales(nt, parity=True)
+    x0 = _x0(prob, np.arange(1, nt + 1))
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega, load_scale=s)
+    g.set_iterate(1, x0)
+    g.iterate(K)
+    xg = g.solution()
+    hg = np.stack([g.residual_history(k) for k in range(K)])
+    rg = g.residual_norms()
+    xo, ho, S = oracle.run(prob, x0, s, K, precond, omega)
+    ro = S.residual_norms(np.vstack([np.zeros(S.ndof), S.to_paper(xo)]), s)
+    return (xg, hg, rg), (xo, ho, ro)
+
+
+@pytest.mark.parametrize("precond", [2, 1])
+@pytest.mark.parametrize("omega", [0.5, 0.3])
+def test_parity_config1_full(precond, omega):
+    prob = config_problem(1)
+    (xg, hg, rg), (xo, ho, ro) = _run_full(prob, prob.K, precond, omega)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+    assert norm_errors(rg, ro).max() < TOL
+
+
+@pytest.mark.parametrize("precond,omega,K", [(2, 0.5, 100), (1, 0.3, 20)])
+def test_parity_config2_full(precond, omega, K):
+    prob = config_problem(2)
+    (xg, hg, rg), (xo, ho, ro) = _run_full(prob, K, precond, omega)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+    assert norm_errors(rg, ro).max() < TOL
+
+
+def _windows(nt, K, world=8, w=12):
+    """Step windows covering the first/last K+8 steps and every 8-GPU slab boundary."""
+    slab = nt // world
+    wins = [(1, min(nt, K + 8)), (max(1, nt - K - 7), nt)]
+    for r in range(1, world):
+        b = r * slab
+        wins.append((b - w // 2 + 1, b + w // 2))
+    return wins
+
+
+def _gpu_windowed(prob, K, precond, omega, wins):
+    nt = prob.n_t
+    s = load_scales(nt, parity=True)
+    g = BiotSolver(prob, precond=precond, omega=omega, load_scale=s)
+    for (a, b) in wins:
+        lo = max(1, a - K)
+        g.set_iterate(lo, _x0(prob, np.arange(lo, b + 1)))
+    g.iterate(K)
+    return g, s
+
+
+@pytest.mark.parametrize("precond", [2, 1])
+def test_parity_config3_windows(precond):
+    """2D 512^2, N_t=1024 at full size; oracle on space-time windows (whole mesh)."""
+    prob = config_problem(3)
+    K, omega = 6, 0.5 if precond == 2 else 0.3
+    wins = _windows(prob.n_t, K)
+    g, s = _gpu_windowed(prob, K, precond, omega, wins)
+    S = oracle.OracleSystem(prob)
+    for (a, b) in wins:
+        xo = oracle_window(S, lambda st: _x0(prob, st), s, a, b, K, precond, omega)
+        xg = g.solution(a, b - a + 1)
+        assert field_errors(xg, xo, 2).max() < TOL, (a, b)
+
+
+def _box_check(prob, g, s, K, precond, omega, lo, hi, wins, x0cache):
+    sub, nodes, idx = subbox(prob, lo, hi)
+    S = oracle.OracleSystem(sub)
+    d, nc = prob.dim, prob.dim + 1
+    n = prob.n
+    # exact region: graph distance > K from every cut face of the box
+    ok = np.ones(nodes.size, bool)
+    for k in range(d):
+        if lo[k] > 0:
+            ok &= idx[:, k] > lo[k] + K
+        if hi[k] < n:
+            ok &= idx[:, k] < hi[k] - K
+    assert ok.sum() > 0
+    cols = (nodes[ok][:, None] * nc + np.arange(nc)).ravel()
+    subcols = (np.nonzero(ok)[0][:, None] * nc + np.arange(nc)).ravel()
+    for (a, b) in wins:
+        full = x0cache[(a, b)]            # x^0 of steps max(1,a-K)..b, whole mesh
+        first = max(1, a - K)
+        x0f = lambda st: full[st - first].reshape(len(st), -1, nc)[:, nodes, :].reshape(len(st), -1)
+        xo = oracle_window(S, x0f, s, a, b, K, precond, omega)
+        xg = g.solution(a, b - a + 1)
+        assert field_errors(xg[:, cols], xo[:, subcols], d).max() < TOL, (lo, hi, a, b)
+
+
+@pytest.mark.parametrize("cid", [4, 5])
+def test_parity_3d_spacetime_windows(cid):
+    """3D configs at full size; oracle on space-time boxes (corner at the loaded top,
+    an interior box, and the fixed bottom), windows at slab boundaries."""
+    prob = config_problem(cid)
+    K, precond, omega = 4, 2, 0.5
+    wins = _windows(prob.n_t, K, w=8)
+    if cid == 5:
+        wins = wins[:3]
+    g, s = _gpu_windowed(prob, K, precond, omega, wins)
+    n = prob.n
+    m = 2 * K + 6
+    boxes = [((n - m, n - m, n - m), (n, n, n)),
+             ((n // 2 - m // 2,) * 3, (n // 2 + m // 2,) * 3),
+             ((0, 0, 0), (m, m, m))]
+    x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
+    for lo, hi in boxes:
+        _box_check(prob, g, s, K, precond, omega, np.array(lo), np.array(hi), wins, x0cache)
+    g.close()
+
+
+def test_parity_config4_p1_box():
+    prob = config_problem(4)
+    K, precond, omega = 3, 1, 0.3
+    wins = _windows(prob.n_t, K, w=6)[:3]
+    g, s = _gpu_windowed(prob, K, precond, omega, wins)
+    n, m = prob.n, 14
+    x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
+    _box_check(prob, g, s, K, precond, omega, np.array((n - m,) * 3), np.array((n,) * 3), wins,
+               x0cache)
+    g.close()
+
+
+def test_parity_ell_path_renumbered_mesh():
+    """A randomly renumbered mesh takes the explicit-column (ELL) kernel."""
+    prob = make_problem(2, 12, 16, 1 / 16, 10, storage=1e-3, kappa_median=1e-2, x0_seed=4)
+    perm = np.random.default_rng(0).permutation(prob.coords.shape[0])
+    inv = np.argsort(perm)
+    prob.coords = prob.coords[perm]
+    prob.cells = inv[prob.cells].astype(np.int32)
+    prob.facets = inv[prob.facets].astype(np.int32)
+    prob.dirichlet = prob.dirichlet.reshape(-1, 3)[perm].reshape(-1).copy()
+    for pc in (1, 2):
+        (xg, hg, rg), (xo, ho, ro) = _run_full(prob, 10, pc, 0.5)
+        assert field_errors(xg, xo, 2).max() < TOL
+        assert norm_errors(hg, ho).max() < TOL
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_parity_ragged_and_small(dim):
+    """n_t not a multiple of the 128-step warp chunk (ragged tail), N_t = 1, tiny meshes."""
+    for nt in (1, 5, 130):
+        prob = make_problem(dim, 3 if dim == 3 else 5, nt, 0.01, 7, x0_seed=8)
+        (xg, hg, rg), (xo, ho, ro) = _run_full(prob, 7, 2, 0.5)
+        assert field_errors(xg, xo, dim).max() < TOL, nt
+        assert norm_errors(hg, ho).max() < TOL, nt
