@@ -114,7 +114,10 @@ typedef struct {
     int64_t n_nodes, n_dof;          /* N, N*(d+1)                                      */
     int32_t n_t, n_t_local, first_step; /* global N_t; owned steps first_step..+n_t_local-1 */
     int64_t iterations;              /* outer iterations done since setup               */
-    int32_t kernel_path;             /* 1 = BDIA stencil-offset, 2 = ELL explicit columns */
+    int32_t kernel_path;             /* 1 = BDIA offsets, 2 = ELL explicit columns,
+                                        3 = register-blocked structured stencil,
+                                        4 = 2D row-march (L1-reuse) kernel,
+                                        5 = 2D TMA-pipelined tile kernel             */
     int32_t n_slots;                 /* neighbour slots per node                        */
     double beta;                     /* the beta actually used                          */
     double bytes_per_iter;           /* algorithmic bytes per outer iteration (this rank) */

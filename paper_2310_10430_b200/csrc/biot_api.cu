@@ -6,12 +6,14 @@
 // from rank-1; BASELINE.json north star (d), replacing the paper's MPI
 // Send/Recv pipeline of Algorithm 5), then the fused sweep
 // kernel (+ the P~1 second pass), then the deterministic norm finalize.
+#include <cudaTypedefs.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -126,6 +128,23 @@ struct biot_ctx {
     int hist_cap = 1024;
     biot::LaunchShape shape{0, 0};
     int tw = 8, node_block = 8;
+    // kernel choice: 1 generic BDIA/ELL sweep, 2 register-blocked stencil, 3 2D march
+    int kern = 1;
+    bool stencil = false;             // detect_stencil() succeeded (structured offsets)
+    int mT = 2;                       // march: time steps per lane
+    int64_t row_w = 0;
+    int32_t n_rows = 0, rows_per_tile = 0;
+    int64_t groups = 0;               // norm-partial groups of the active kernel
+    // 4: TMA-pipelined 2D tile kernel
+    double *aux = nullptr;
+    double tmpl[7][10] = {{0}};
+    CUtensorMap tmap[2];
+    int64_t n_interior = 0;
+    int sR = 4, sT = 2;
+    int64_t gbase[8] = {0};
+    int32_t slot[8][3] = {{0}};
+    int64_t n_alloc = 0;              // nodes allocated in operator arrays (>= N, multiple of 8)
+    int pass2_grid = 0;
     size_t device_bytes = 0;
     ncclComm_t comm = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
@@ -170,7 +189,7 @@ void free_all(biot_ctx *c) {
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->dinv, (void *)c->s,
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
-                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging})
+                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux})
         if (p) cudaFree(p);
     for (cudaEvent_t e : {c->ev_a, c->ev_b})
         if (e) cudaEventDestroy(e);
@@ -200,6 +219,9 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.mode = mode;
     a.omega = c->omega;
     for (int s = 0; s < 32; ++s) a.off[s] = s < (int)c->offsets.size() ? c->offsets[s] : 0;
+    a.row_w = c->row_w;
+    a.n_rows = c->n_rows;
+    a.rows_per_tile = c->rows_per_tile;
     return a;
 }
 
@@ -233,6 +255,79 @@ biot_status halo_exchange(biot_ctx *ctx) {
     return BIOT_OK;
 }
 
+// Recognise the BDIA offset sets of the structured meshes (2D right triangles,
+// 3D Kuhn tetrahedra) and fill the run tables of the register-blocked kernel.
+bool detect_stencil(biot_ctx *c) {
+    if (c->path != biot::PATH_BDIA) return false;
+    std::vector<int64_t> o(c->offsets.begin(), c->offsets.end());
+    std::sort(o.begin(), o.end());
+    o.erase(std::unique(o.begin(), o.end()), o.end());
+    auto idx = [&](int64_t off) -> int {
+        for (size_t s = 0; s < c->offsets.size(); ++s)
+            if (c->offsets[s] == off) return (int)s;
+        return -1;
+    };
+    std::vector<int64_t> bases;
+    std::vector<std::pair<int, int>> ranges;
+    if (c->d == 2) {
+        if (o.size() != 7) return false;
+        const int64_t W = o.back() - 1;
+        std::vector<int64_t> want = {-W - 1, -W, -1, 0, 1, W, W + 1};
+        if (W < 3 || o != want) return false;
+        bases = {-W, 0, W};
+        ranges = {{-1, 0}, {-1, 1}, {0, 1}};
+    } else {
+        if (o.size() != 15) return false;
+        int64_t W = 0;
+        for (int64_t v : o)
+            if (v > 1) { W = v; break; }
+        const int64_t V = W * W;
+        std::vector<int64_t> want = {0, 1, -1, W, -W, V, -V, 1 + W, -1 - W, 1 + V, -1 - V,
+                                     W + V, -W - V, 1 + W + V, -1 - W - V};
+        std::sort(want.begin(), want.end());
+        if (W < 3 || o != want) return false;
+        bases = {-W - V, -V, -W, 0, W, V, W + V};
+        ranges = {{-1, 0}, {-1, 0}, {-1, 0}, {-1, 1}, {0, 1}, {0, 1}, {0, 1}};
+    }
+    for (size_t g = 0; g < bases.size(); ++g) {
+        c->gbase[g] = bases[g];
+        for (int a = ranges[g].first; a <= ranges[g].second; ++a) {
+            const int s = idx(bases[g] + a);
+            if (s < 0) return false;
+            c->slot[g][a - ranges[g].first] = s;
+        }
+    }
+    return true;
+}
+
+biot::StencilArgs stencil_args(biot_ctx *c, int mode, const double *xin, double *xout) {
+    biot::StencilArgs a{};
+    static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
+    for (int g = 0; g < 8; ++g) {
+        a.gbase[g] = c->gbase[g];
+        for (int k = 0; k < 3; ++k) a.slot[g][k] = c->slot[g][k];
+    }
+    return a;
+}
+
+cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) {
+    if (c->kern == 2) {
+        biot::StencilArgs a = stencil_args(c, mode, xin, xout);
+        return biot::launch_stencil(c->d, c->sR, c->sT, a, c->shape, c->stream);
+    }
+    if (c->kern == 4) {
+        biot::Tile2dArgs a{};
+        static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
+        std::memcpy(a.tmpl, c->tmpl, sizeof(a.tmpl));
+        a.aux = c->aux;
+        a.pad_nodes = c->pad;
+        return biot::launch_tile2d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
+    }
+    biot::SweepArgs a = sweep_args(c, mode, xin, xout);
+    if (c->kern == 3) return biot::launch_march(c->mT, a, c->shape, c->stream);
+    return biot::launch_sweep(c->d, c->path, c->S, a, c->shape, c->stream);
+}
+
 biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     const bool timing = e0 != nullptr;
     biot_status st = halo_exchange(ctx);
@@ -242,7 +337,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
     biot::SweepArgs a = sweep_args(ctx, mode, xin, xout);
     if (timing) CU(cudaEventRecord(e0, ctx->stream));
-    CU(biot::launch_sweep(ctx->d, ctx->path, ctx->S, a, ctx->shape, ctx->stream));
+    CU(launch_main(ctx, mode, xin, xout));
     if (timing) CU(cudaEventRecord(e1, ctx->stream));
     if (ctx->precond == 1) {
         biot::Pass2Args p{};
@@ -260,10 +355,10 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
         p.node_block = ctx->node_block;
         p.omega = ctx->omega;
         for (int s = 0; s < 32; ++s) p.off[s] = a.off[s];
-        CU(biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->shape.grid, ctx->stream));
+        CU(biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream));
     }
     double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
-    CU(biot::launch_finalize(ctx->partial, ctx->shape.grid, ctx->n_tl, hslot, ctx->nonfinite,
+    CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
                              ctx->stream));
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
@@ -419,10 +514,41 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->nnz_AP = op->nnz_AP;
     ctx->hist_cap = opts->history > 0 ? opts->history : 1024;
     ctx->pitch = ((int64_t)ctx->n_tl + biot::kChunk - 1) / biot::kChunk * biot::kChunk;
-    const int64_t nchunks = ctx->pitch / biot::kChunk;
+    ctx->node_block = 8;
+    {
+        const char *kenv = std::getenv("BIOT_KERNEL");
+        const bool force_generic = kenv && std::string(kenv) == "generic";
+        if (const char *e = std::getenv("BIOT_STENCIL_R")) ctx->sR = std::atoi(e);
+        else ctx->sR = ctx->d == 2 ? 4 : 2;
+        if (const char *e = std::getenv("BIOT_STENCIL_T")) ctx->sT = std::atoi(e);
+        else ctx->sT = 2;
+        ctx->stencil = detect_stencil(ctx);
+        if (const char *e = std::getenv("BIOT_MARCH_T")) ctx->mT = std::atoi(e);
+        std::string want = kenv ? std::string(kenv) : std::string();
+        if (force_generic || !ctx->stencil) {
+            ctx->kern = 1;
+        } else if (want == "stencil") {
+            ctx->kern = biot::stencil_supported(ctx->d, ctx->sR, ctx->sT) ? 2 : 1;
+        } else if (ctx->d == 2) {
+            ctx->row_w = -ctx->gbase[0];              // W
+            ctx->n_rows = (int32_t)(ctx->N / ctx->row_w);
+            const std::vector<int64_t> order = {0, -ctx->row_w - 1, -ctx->row_w, -1, 1, ctx->row_w, ctx->row_w + 1};
+            const bool grid_ok = ctx->row_w * ctx->n_rows == ctx->N;
+            if (!grid_ok) ctx->kern = 1;
+            else if (want == "march") ctx->kern = (ctx->mT == 2 || ctx->mT == 4) ? 3 : 1;
+            else ctx->kern = (ctx->offsets == order) ? 4 : 3;
+        } else {
+            ctx->kern = 1;
+        }
+    }
+    const int64_t chunk = ctx->kern == 2 ? 32 * ctx->sT
+                        : ctx->kern == 3 ? 32 * ctx->mT
+                        : ctx->kern == 4 ? biot::tile2d_chunk()
+                                         : biot::kChunk;
+    const int64_t nchunks = (ctx->n_tl + chunk - 1) / chunk;
     ctx->tw = 1;
     while (ctx->tw < 8 && ctx->tw < nchunks) ctx->tw *= 2;
-    ctx->node_block = 8;
+    ctx->n_alloc = (ctx->N + 7) / 8 * 8;
 
     if (opts->stream) {
         ctx->stream = (cudaStream_t)opts->stream;
@@ -435,7 +561,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
 
     const int nc = ctx->nc;
     const int W = biot::block_width(nc);
-    ctx->rows_alloc = (ctx->N + 2 * ctx->pad) * nc;
+    // nodes: [pad | N | pad + 8]; the blocked kernel may touch up to 7 dummy rows past N
+    ctx->rows_alloc = (ctx->N + 2 * ctx->pad + 8) * nc;
     const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
     for (int k = 0; k < 2; ++k) {
         ALLOC(ctx->xbase[k], panel_bytes);
@@ -457,16 +584,22 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             if (op->fixed[q]) x0[q] = 0.0;
         CU(cudaMemcpy(ctx->ghost, x0.data(), vec_bytes, cudaMemcpyHostToDevice));
     }
-    ALLOC(ctx->blk, op->blk.size() * sizeof(double));
+    // operator arrays padded to n_alloc nodes with zeros (dummy rows of the blocked kernel)
+    const size_t blk_bytes = (size_t)ctx->n_alloc * ctx->S * W * sizeof(double);
+    ALLOC(ctx->blk, blk_bytes);
+    CU(cudaMemsetAsync(ctx->blk, 0, blk_bytes, ctx->stream));
     CU(cudaMemcpy(ctx->blk, op->blk.data(), op->blk.size() * sizeof(double), cudaMemcpyHostToDevice));
     if (ctx->path == biot::PATH_ELL) {
         ALLOC(ctx->cols, op->cols.size() * sizeof(int32_t));
         CU(cudaMemcpy(ctx->cols, op->cols.data(), op->cols.size() * sizeof(int32_t),
                       cudaMemcpyHostToDevice));
     }
-    ALLOC(ctx->load, vec_bytes);
+    const size_t vec_alloc = (size_t)ctx->n_alloc * nc * sizeof(double);
+    ALLOC(ctx->load, vec_alloc);
+    CU(cudaMemsetAsync(ctx->load, 0, vec_alloc, ctx->stream));
     CU(cudaMemcpy(ctx->load, op->load.data(), vec_bytes, cudaMemcpyHostToDevice));
-    ALLOC(ctx->dinv, vec_bytes);
+    ALLOC(ctx->dinv, vec_alloc);
+    CU(cudaMemsetAsync(ctx->dinv, 0, vec_alloc, ctx->stream));
     CU(cudaMemcpy(ctx->dinv, op->dinv.data(), vec_bytes, cudaMemcpyHostToDevice));
     ALLOC(ctx->fixed, (size_t)ctx->N * nc);
     CU(cudaMemcpy(ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc, cudaMemcpyHostToDevice));
@@ -481,9 +614,94 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
 
     const int nwp = 8 / ctx->tw;
-    ctx->shape.smem = (size_t)nwp * ctx->pitch * 2 * sizeof(double);
-    CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));
-    ALLOC(ctx->partial, (size_t)ctx->shape.grid * ctx->n_tl * 2 * sizeof(double));
+    ctx->shape.smem = (size_t)nwp * (nchunks * chunk) * 2 * sizeof(double);
+    if (ctx->kern == 2) {
+        CU(biot::stencil_shape(ctx->d, ctx->sR, ctx->sT, ctx->device, &ctx->shape));
+        ctx->groups = ctx->shape.grid;
+    } else if (ctx->kern == 3) {
+        CU(biot::march_shape(ctx->mT, ctx->device, &ctx->shape));
+        // rows per tile: enough tiles for ~8 waves, at least 16 rows per tile
+        const int64_t n_seg = (ctx->row_w + 7) / 8;
+        int64_t rpt = ctx->n_rows;
+        while (rpt > 16 && n_seg * ((ctx->n_rows + rpt - 1) / rpt) * nchunks < 8 * (int64_t)ctx->shape.grid)
+            rpt = (rpt + 1) / 2;
+        if (const char *e = std::getenv("BIOT_MARCH_ROWS")) rpt = std::max(1, std::atoi(e));
+        ctx->rows_per_tile = (int32_t)rpt;
+        biot::SweepArgs tmp = sweep_args(ctx, biot::MODE_RESIDUAL, nullptr, nullptr);
+        ctx->groups = biot::march_groups(tmp);
+    } else if (ctx->kern == 4) {
+        CU(biot::tile2d_shape(ctx->device, &ctx->shape));
+        const int64_t n_seg = (ctx->row_w + 7) / 8;
+        int64_t rpt = ctx->n_rows;
+        while (rpt > 16 && n_seg * ((ctx->n_rows + rpt - 1) / rpt) * nchunks < 8 * (int64_t)ctx->shape.grid)
+            rpt = (rpt + 1) / 2;
+        if (const char *e = std::getenv("BIOT_MARCH_ROWS")) rpt = std::max(1, std::atoi(e));
+        ctx->rows_per_tile = (int32_t)rpt;
+        biot::Tile2dArgs tmp{};
+        tmp.row_w = ctx->row_w;
+        tmp.n_rows = ctx->n_rows;
+        tmp.rows_per_tile = ctx->rows_per_tile;
+        ctx->groups = biot::tile2d_groups(tmp);
+        // interior template + per-node aux records
+        const int S = 7, WB = 10, KA = biot::Tile2dArgs::kAux;
+        const int64_t tnode = (int64_t)(ctx->n_rows / 2) * ctx->row_w + ctx->row_w / 2;
+        const double *tb = op->blk.data() + (size_t)tnode * S * WB;
+        for (int q = 0; q < S; ++q)
+            for (int k = 0; k < WB; ++k) ctx->tmpl[q][k] = tb[q * WB + k];
+        std::vector<double> aux((size_t)ctx->n_alloc * KA, 0.0);
+        int64_t n_int = 0;
+        for (int64_t i = 0; i < ctx->N; ++i) {
+            const double *b = op->blk.data() + (size_t)i * S * WB;
+            bool same = true;
+            for (int q = 0; q < S && same; ++q)
+                for (int k = 0; k < WB; ++k)
+                    if (k != 8 && std::memcmp(&b[q * WB + k], &tb[q * WB + k], sizeof(double)) != 0) {
+                        same = false;
+                        break;
+                    }
+            double *r = aux.data() + (size_t)i * KA;
+            for (int q = 0; q < S; ++q) r[q] = b[q * WB + 8];
+            for (int c = 0; c < 3; ++c) {
+                r[7 + c] = op->load[(size_t)i * 3 + c];
+                r[10 + c] = op->dinv[(size_t)i * 3 + c];
+            }
+            r[13] = same ? 1.0 : 0.0;
+            n_int += same;
+        }
+        ctx->n_interior = n_int;
+        ALLOC(ctx->aux, aux.size() * sizeof(double));
+        CU(cudaMemcpy(ctx->aux, aux.data(), aux.size() * sizeof(double), cudaMemcpyHostToDevice));
+        // TMA tensor maps of the two panels: {time (pitch), panel rows}
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qres;
+        CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
+        if (!fn || qres != cudaDriverEntryPointSuccess)
+            return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled not available");
+        auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        uint32_t box[2];
+        biot::tile2d_box(box);
+        for (int k = 0; k < 2; ++k) {
+            cuuint64_t dims[2] = {(cuuint64_t)ctx->pitch, (cuuint64_t)ctx->rows_alloc};
+            cuuint64_t strides[1] = {(cuuint64_t)ctx->pitch * sizeof(double)};
+            cuuint32_t bx[2] = {box[0], box[1]};
+            cuuint32_t es[2] = {1, 1};
+            CUresult r = encode(&ctx->tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ctx->xbase[k], dims, strides,
+                                bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        }
+    } else {
+        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));
+        ctx->groups = ctx->shape.grid;
+    }
+    // P~1 pass 2 uses the generic shape
+    {
+        biot::LaunchShape p2{0, 0};
+        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &p2));
+        ctx->pass2_grid = p2.grid;
+    }
+    ALLOC(ctx->partial, (size_t)ctx->groups * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->hist, (size_t)ctx->hist_cap * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->nonfinite, sizeof(int));
@@ -578,9 +796,8 @@ biot_status biot_residual_norms(biot_ctx *ctx, double *out) {
     CU(cudaSetDevice(ctx->device));
     biot_status st = halo_exchange(ctx);
     if (st != BIOT_OK) return st;
-    biot::SweepArgs a = sweep_args(ctx, biot::MODE_RESIDUAL, ctx->x[ctx->cur], nullptr);
-    CU(biot::launch_sweep(ctx->d, ctx->path, ctx->S, a, ctx->shape, ctx->stream));
-    CU(biot::launch_finalize(ctx->partial, ctx->shape.grid, ctx->n_tl, ctx->norms, ctx->nonfinite,
+    CU(launch_main(ctx, biot::MODE_RESIDUAL, ctx->x[ctx->cur], nullptr));
+    CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, ctx->norms, ctx->nonfinite,
                              ctx->stream));
     CU(cudaMemcpyAsync(out, ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
@@ -654,7 +871,7 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->n_t_local = ctx->n_tl;
     o->first_step = ctx->first_step;
     o->iterations = ctx->iterations;
-    o->kernel_path = ctx->path;
+    o->kernel_path = ctx->kern == 1 ? ctx->path : ctx->kern + 1;   // 3 stencil, 4 march, 5 tile2d
     o->n_slots = ctx->S;
     o->beta = ctx->beta;
     const double st = (double)ctx->N * ctx->nc * ctx->n_tl;

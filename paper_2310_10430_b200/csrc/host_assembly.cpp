@@ -24,7 +24,7 @@
 
 namespace biot {
 
-int block_width(int nc) { return nc * nc + 1; }
+int block_width(int nc) { return (nc * nc + 2) / 2 * 2; }   // (d+1)^2 + 1, padded to 16 B
 
 namespace {
 
@@ -66,11 +66,6 @@ double simplex_gradients(int d, const double *const *X, double g[4][3]) {
         for (int k = 0; k < d; ++k) g[a][k] = V[1 + k][n + a];
     return det / (d == 2 ? 2.0 : 6.0);
 }
-
-struct SlotMap {
-    // BDIA: offset -> slot
-    std::unordered_map<int64_t, int> off2slot;
-};
 
 }  // namespace
 

@@ -16,7 +16,7 @@ enum Path : int { PATH_BDIA = 1, PATH_ELL = 2 };
 // Per-node neighbour blocks.  For node i and slot s (column node j):
 //   blk[((i*S)+s)*W + c*NC + cc]  = AA[(i,c),(j,cc)]          (c, cc < NC)
 //   blk[((i*S)+s)*W + NC*NC]      = A'[(i,p),(j,p)] = -H_ij    (pressure of A')
-// where W = NC*NC + 1; A'[(i,p),(j,u_e)] equals AA[(i,p),(j,u_e)] (both B^T) and is
+// where W = NC*NC + 1 rounded up to even (16-B aligned blocks); A'[(i,p),(j,u_e)] equals AA[(i,p),(j,u_e)] (both B^T) and is
 // read from the AA block.  BDIA: j = i + offsets[s]; ELL: j = cols[i*S+s].
 struct HostOperator {
     int d = 0, nc = 0;
@@ -26,7 +26,7 @@ struct HostOperator {
     int64_t max_abs_offset = 0;
     std::vector<int64_t> offsets;   // BDIA, offsets[0] == 0 (self)
     std::vector<int32_t> cols;      // ELL, self in slot 0, padding repeats self with zero blocks
-    std::vector<double> blk;        // n_nodes * S * (nc*nc + 1)
+    std::vector<double> blk;        // n_nodes * S * block_width(nc)
     std::vector<double> load;       // f, n_nodes * nc
     std::vector<double> dinv;       // n_nodes * nc; 1/diag(A), 1/diag(S~p) on free DoFs, else 0
     std::vector<uint8_t> fixed;     // n_nodes * nc

@@ -18,6 +18,7 @@
 // q(t0-1) in the same FMA order (bitwise identical), reading the ghost step
 // (the last step of the previous time slab, or x_0) when t0 = 0.
 #include "sweep_kernels.cuh"
+#include "node_update.cuh"
 
 #include <cmath>
 
@@ -26,156 +27,7 @@ namespace biot {
 
 namespace {
 
-constexpr int kSlotUnroll = 1;   // slot loop kept rolled: bounded registers, no spills
-
-template <int S, bool ELL>
-__device__ __forceinline__ int64_t column(const int32_t *__restrict__ cols, const int64_t *off,
-                                          int64_t i, int s) {
-    if constexpr (ELL) return (int64_t)__ldg(cols + i * S + s);
-    else return i + off[s];
-}
-
-template <int D, int S, bool ELL>
-__device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, int t0, int lane,
-                                            const double (&sv)[kT], double (&nu)[kT],
-                                            double (&npn)[kT]) {
-    constexpr int NC = D + 1;
-    constexpr int W = NC * NC + 1;
-    const int64_t P = a.pitch;
-    const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
-
-    double acc[NC][kT], q[kT];
-#pragma unroll
-    for (int tt = 0; tt < kT; ++tt) {
-        q[tt] = 0.0;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c][tt] = 0.0;
-    }
-
-#pragma unroll(kSlotUnroll)
-    for (int s = 0; s < S; ++s) {
-        const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
-        const double *__restrict__ xj = a.x + j * NC * P + t0;
-        double cf[W];
-#pragma unroll
-        for (int k = 0; k < W; ++k) cf[k] = __ldg(bp + s * W + k);
-#pragma unroll
-        for (int cc = 0; cc < NC; ++cc) {
-            const double2 v01 = __ldg(reinterpret_cast<const double2 *>(xj + cc * P));
-            const double2 v23 = __ldg(reinterpret_cast<const double2 *>(xj + cc * P + 2));
-            const double v[kT] = {v01.x, v01.y, v23.x, v23.y};
-#pragma unroll
-            for (int c = 0; c < NC; ++c)
-#pragma unroll
-                for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf[c * NC + cc], v[tt], acc[c][tt]);
-            const double qc = (cc < D) ? cf[D * NC + cc] : cf[NC * NC];
-#pragma unroll
-            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(qc, v[tt], q[tt]);
-        }
-    }
-
-    // previous-step coupling for the lane's first step
-    double qprev = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
-    if (lane == 0) {
-        double qg = 0.0;
-        const bool use_ghost = (t0 == 0);
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
-            const double *src = use_ghost ? (a.ghost + j * NC) : (a.x + j * NC * P + (t0 - 1));
-            const int64_t stride = use_ghost ? 1 : P;
-#pragma unroll
-            for (int cc = 0; cc < NC; ++cc) {
-                const double qc = (cc < D) ? __ldg(bp + s * W + D * NC + cc) : __ldg(bp + s * W + NC * NC);
-                qg = fma(qc, __ldg(src + cc * stride), qg);
-            }
-        }
-        qprev = qg;
-    }
-
-    double F[NC], Dv[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        F[c] = __ldg(a.load + i * NC + c);
-        Dv[c] = __ldg(a.dinv + i * NC + c);
-    }
-    const int mode = a.mode;
-    const double omega = a.omega;
-    double xs[NC][kT];   // own x_i(t0..t0+3): reloaded (L1 hit) instead of held across the slot loop
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        const double *src = a.x + (i * NC + c) * P + t0;
-        const double2 v01 = __ldg(reinterpret_cast<const double2 *>(src));
-        const double2 v23 = __ldg(reinterpret_cast<const double2 *>(src + 2));
-        xs[c][0] = v01.x; xs[c][1] = v01.y; xs[c][2] = v23.x; xs[c][3] = v23.y;
-    }
-    double outx[NC][kT], outz[NC][kT];
-#pragma unroll
-    for (int tt = 0; tt < kT; ++tt) {
-        const double qp = (tt == 0) ? qprev : q[tt - 1];
-        double r[NC];
-#pragma unroll
-        for (int c = 0; c < D; ++c) r[c] = sv[tt] * F[c] - acc[c][tt];
-        r[D] = (sv[tt] * F[D] + qp) - acc[D][tt];
-        double su = 0.0;
-#pragma unroll
-        for (int c = 0; c < D; ++c) su = fma(r[c], r[c], su);
-        nu[tt] += su;
-        npn[tt] = fma(r[D], r[D], npn[tt]);
-        double z[NC];
-#pragma unroll
-        for (int c = 0; c < D; ++c) z[c] = Dv[c] * r[c];
-        z[D] = -(Dv[D] * r[D]);   // P~2 pressure part; P~1 finishes it in pass 2
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            outx[c][tt] = fma(omega, z[c], xs[c][tt]);
-            outz[c][tt] = (c < D) ? z[c] : r[D];
-        }
-    }
-    if (mode == MODE_RESIDUAL) return;
-
-    const int n_tl = a.n_tl;
-    const int ncw = (mode == MODE_UPDATE_P2) ? NC : D;   // P~1: pressure written by pass 2
-    const bool full = (t0 + kT <= n_tl);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-        if (c >= ncw) break;
-        double *dst = a.xn + (i * NC + c) * P + t0;
-        if (full) {
-            *reinterpret_cast<double2 *>(dst) = make_double2(outx[c][0], outx[c][1]);
-            *reinterpret_cast<double2 *>(dst + 2) = make_double2(outx[c][2], outx[c][3]);
-        } else {
-#pragma unroll
-            for (int tt = 0; tt < kT; ++tt)
-                if (t0 + tt < n_tl) dst[tt] = outx[c][tt];
-        }
-    }
-    if (mode == MODE_P1_PASS1) {
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            double *dst = a.zbuf + (i * NC + c) * P + t0;
-            if (full) {
-                *reinterpret_cast<double2 *>(dst) = make_double2(outz[c][0], outz[c][1]);
-                *reinterpret_cast<double2 *>(dst + 2) = make_double2(outz[c][2], outz[c][3]);
-            } else {
-#pragma unroll
-                for (int tt = 0; tt < kT; ++tt)
-                    if (t0 + tt < n_tl) dst[tt] = outz[c][tt];
-            }
-        }
-    }
-    if (a.sendbuf) {
-        const int tl = n_tl - 1 - t0;
-        if (tl >= 0 && tl < kT) {
-#pragma unroll
-            for (int tt = 0; tt < kT; ++tt)
-                if (tt == tl)
-#pragma unroll
-                    for (int c = 0; c < NC; ++c)
-                        if (c < ncw) a.sendbuf[i * NC + c] = outx[c][tt];
-        }
-    }
-}
+using namespace dev;
 
 template <int D, int S, bool ELL>
 __global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const SweepArgs a) {
@@ -200,7 +52,8 @@ __global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const
         for (int64_t b = blockIdx.x; b * nb < N; b += gridDim.x) {
             const int64_t i_end = min(N, (b + 1) * nb);
             for (int64_t i = b * nb + nw; i < i_end; i += nwp)
-                node_update<D, S, ELL>(a, i, t0, lane, sv, nu, npn);
+                node_update<D, S, ELL, kT, false>(a, i, a.blk + i * (int64_t)(S * block_pitch<D>()), t0,
+                                                  lane, sv, nu, npn);
         }
 #pragma unroll
         for (int tt = 0; tt < kT; ++tt) {
@@ -220,11 +73,12 @@ __global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const
     }
 }
 
+
 // P~1 second pass (PAPER.md eq. p1: z_p = S~p^{-1} (B^T z_u - r_p)).
 template <int D, int S, bool ELL>
 __global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
     constexpr int NC = D + 1;
-    constexpr int W = NC * NC + 1;
+    constexpr int W = (NC * NC + 2) / 2 * 2;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int tw = a.tw, nwp = (kThreads / 32) / tw;
     const int cw = warp % tw, nw = warp / tw;

@@ -2,6 +2,7 @@
 // Internal header shared by sweep_kernels.cu and biot_api.cu.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace biot {
@@ -36,6 +37,10 @@ struct SweepArgs {
     int32_t mode;
     double omega;
     int64_t off[32];        // BDIA column offsets (slot 0 = self)
+    // 2D march kernel (structured right-triangle mesh): node = j * row_w + i
+    int64_t row_w;          // nodes per grid row (n+1)
+    int32_t n_rows;         // grid rows (n+1)
+    int32_t rows_per_tile;  // rows marched by one tile
 };
 
 struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
@@ -52,6 +57,22 @@ struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_
     int64_t off[32];
 };
 
+// Arguments of the register-blocked structured-stencil sweep (stencil_kernels.cu).
+struct StencilArgs : SweepArgs {
+    template <int D>
+    static constexpr int kBlockPitch = D == 2 ? 10 : 18;   // (d+1)^2 + 1, padded to 16 B
+    int64_t gbase[8];       // base offset of each run of consecutive column offsets
+    int32_t slot[8][3];     // BDIA slot of (run g, offset a - amin(g))
+};
+
+// Arguments of the TMA-pipelined 2D tile kernel (tile2d_kernels.cu).
+struct Tile2dArgs : SweepArgs {
+    static constexpr int kAux = 16;   // per-node record: AA_pp per slot [7], f [3], dinv [3], interior flag
+    double tmpl[7][10];               // interior stencil blocks (slot order), pp entry unused
+    const double *aux;                // [n_alloc][kAux]
+    int64_t pad_nodes;                // panel rows start at node -pad_nodes
+};
+
 struct LaunchShape {
     int grid;
     size_t smem;
@@ -64,6 +85,28 @@ cudaError_t launch_sweep(int dim, int path, int n_slots, const SweepArgs &a, con
 cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int grid,
                          cudaStream_t st);
 // norms[t][k] = sqrt(sum_g partial[g][t][k]) in fixed g order; flags non-finite values
+// 2D march kernel: CTA = 8-node row segment x (32*T)-step chunk, marching rows.
+cudaError_t march_shape(int T, int device, LaunchShape *out);
+cudaError_t launch_march(int T, const SweepArgs &a, const LaunchShape &sh, cudaStream_t st);
+// norm-partial groups of the march kernel (segments x row ranges)
+inline int64_t march_groups(const SweepArgs &a) {
+    const int64_t n_seg = (a.row_w + 7) / 8;
+    const int64_t n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
+    return n_seg * n_jr;
+}
+
+// 2D TMA tile kernel: x boxes {time, rows} of the panel tensor map
+int64_t tile2d_groups(const Tile2dArgs &a);
+int tile2d_chunk();
+void tile2d_box(uint32_t *box);
+cudaError_t tile2d_shape(int device, LaunchShape *out);
+cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
+                          cudaStream_t st);
+
+bool stencil_supported(int dim, int R, int T);
+cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);
+cudaError_t launch_stencil(int dim, int R, int T, const StencilArgs &a, const LaunchShape &sh,
+                           cudaStream_t st);
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
                             int *nonfinite, cudaStream_t st);
 

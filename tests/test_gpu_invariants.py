@@ -96,3 +96,23 @@ def test_all_dirichlet_and_zero_storage():
     g.iterate(3)
     assert np.abs(g.solution()).max() == 0.0
     assert np.abs(g.residual_norms()).max() == 0.0
+
+
+@pytest.mark.parametrize("cid", [1, 2])
+@pytest.mark.parametrize("precond", [2, 1])
+def test_kernel_variants_bitwise(cid, precond, monkeypatch):
+    """Every sweep kernel (generic BDIA, 2D row-march, TMA tile) shares dev::node_epilogue
+    and the same FMA order: their iterates are bitwise identical."""
+    prob = config_problem(cid)
+    K = 6
+    res = {}
+    for kern in ("generic", "march", "tile"):
+        monkeypatch.setenv("BIOT_KERNEL", kern)
+        g = _seeded(prob, prob.n_t, precond=precond)
+        g.iterate(K)
+        res[kern] = (g.solution(), g.residual_history(K - 1), g.info.kernel_path)
+        g.close()
+    assert res["generic"][2] == 1 and res["march"][2] == 4 and res["tile"][2] == 5
+    for kern in ("march", "tile"):
+        assert np.array_equal(res[kern][0], res["generic"][0]), kern
+        assert np.allclose(res[kern][1], res["generic"][1], rtol=1e-12, atol=0), kern

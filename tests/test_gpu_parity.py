@@ -96,13 +96,16 @@ def _box_check(prob, g, s, K, precond, omega, lo, hi, wins, x0cache):
     S = oracle.OracleSystem(sub)
     d, nc = prob.dim, prob.dim + 1
     n = prob.n
-    # exact region: graph distance > K from every cut face of the box
+    # exact region: graph distance > reach*K from every cut face of the box; one
+    # iteration reaches one node ring with P~2 and two with P~1 (B^T z_u gathers z_u,
+    # itself a residual of the neighbours)
+    reach = K * (2 if precond == 1 else 1)
     ok = np.ones(nodes.size, bool)
     for k in range(d):
         if lo[k] > 0:
-            ok &= idx[:, k] > lo[k] + K
+            ok &= idx[:, k] > lo[k] + reach
         if hi[k] < n:
-            ok &= idx[:, k] < hi[k] - K
+            ok &= idx[:, k] < hi[k] - reach
     assert ok.sum() > 0
     cols = (nodes[ok][:, None] * nc + np.arange(nc)).ravel()
     subcols = (np.nonzero(ok)[0][:, None] * nc + np.arange(nc)).ravel()
