@@ -140,6 +140,7 @@ struct biot_ctx {
     double tmpl[7][10] = {{0}};
     CUtensorMap tmap[2];
     int64_t n_interior = 0;
+    int s0 = 0;                       // tile2d zero-storage structural-zero variant
     int sR = 4, sT = 2;
     int64_t gbase[8] = {0};
     int32_t slot[8][3] = {{0}};
@@ -321,6 +322,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
         std::memcpy(a.tmpl, c->tmpl, sizeof(a.tmpl));
         a.aux = c->aux;
         a.pad_nodes = c->pad;
+        a.s0 = c->s0;
         return biot::launch_tile2d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     biot::SweepArgs a = sweep_args(c, mode, xin, xout);
@@ -631,7 +633,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ctx->groups = biot::march_groups(tmp);
     } else if (ctx->kern == 4) {
         CU(biot::tile2d_shape(ctx->device, &ctx->shape));
-        const int64_t n_seg = (ctx->row_w + 7) / 8;
+        const int64_t n_seg = (ctx->row_w + biot::tile2d_seg() - 1) / biot::tile2d_seg();
         int64_t rpt = ctx->n_rows;
         while (rpt > 16 && n_seg * ((ctx->n_rows + rpt - 1) / rpt) * nchunks < 8 * (int64_t)ctx->shape.grid)
             rpt = (rpt + 1) / 2;
@@ -648,17 +650,30 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const double *tb = op->blk.data() + (size_t)tnode * S * WB;
         for (int q = 0; q < S; ++q)
             for (int k = 0; k < WB; ++k) ctx->tmpl[q][k] = tb[q * WB + k];
+        // structural zeros the kernel skips (must match tmpl_zero in tile2d_kernels.cu)
+        auto tz = [](int q, int e, bool z0) {
+            return (q == 0) ? (e == 2 || e == 5 || e == 6 || e == 7)
+                            : (q == 1 || q == 6) ? (e == 0 || e == 4 || (z0 && (e == 8 || e == 9))) : false;
+        };
+        bool base_ok = true;
+        for (int q = 0; q < S; ++q)
+            for (int k = 0; k < WB; ++k)
+                if (k != 8 && tz(q, k, false) && ctx->tmpl[q][k] != 0.0) base_ok = false;
+        const bool z0 = base_ok && ctx->tmpl[1][9] == 0.0 && ctx->tmpl[6][9] == 0.0 &&
+                        ctx->tmpl[1][8] == 0.0 && ctx->tmpl[6][8] == 0.0;
+        ctx->s0 = z0 ? 1 : 0;
         std::vector<double> aux((size_t)ctx->n_alloc * KA, 0.0);
         int64_t n_int = 0;
         for (int64_t i = 0; i < ctx->N; ++i) {
             const double *b = op->blk.data() + (size_t)i * S * WB;
-            bool same = true;
+            bool same = base_ok;
             for (int q = 0; q < S && same; ++q)
                 for (int k = 0; k < WB; ++k)
                     if (k != 8 && std::memcmp(&b[q * WB + k], &tb[q * WB + k], sizeof(double)) != 0) {
                         same = false;
                         break;
                     }
+            if (same && z0 && (b[1 * WB + 8] != 0.0 || b[6 * WB + 8] != 0.0)) same = false;
             double *r = aux.data() + (size_t)i * KA;
             for (int q = 0; q < S; ++q) r[q] = b[q * WB + 8];
             for (int c = 0; c < 3; ++c) {

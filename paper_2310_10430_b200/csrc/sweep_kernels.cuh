@@ -71,6 +71,7 @@ struct Tile2dArgs : SweepArgs {
     double tmpl[7][10];               // interior stencil blocks (slot order), pp entry unused
     const double *aux;                // [n_alloc][kAux]
     int64_t pad_nodes;                // panel rows start at node -pad_nodes
+    int32_t s0;                       // zero-storage variant: extra structural zeros (see tile2d)
 };
 
 struct LaunchShape {
@@ -98,6 +99,7 @@ inline int64_t march_groups(const SweepArgs &a) {
 // 2D TMA tile kernel: x boxes {time, rows} of the panel tensor map
 int64_t tile2d_groups(const Tile2dArgs &a);
 int tile2d_chunk();
+int tile2d_seg();   // grid columns per tile (8 x R)
 void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,

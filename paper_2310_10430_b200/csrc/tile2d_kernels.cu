@@ -3,26 +3,32 @@
 // Jacobi-in-time inverted scheme with the block
 // preconditioner (L238-262), the damped update and the per-step norms fused.
 //
-// Work tile = 8 consecutive grid columns x 64 time steps x a range of grid rows,
-// marched upward.  A producer warp streams, for every grid row r of the tile
-// (plus the halo rows), one TMA tensor box -- the 10-node strip (8 columns + 2
-// halo) x 3 components x 66 time steps (t0-2 .. t0+63) of the space-time panel --
-// and one bulk copy of the 8 row nodes' aux records (kappa-dependent pressure
-// entries, load, preconditioner diagonals) into a 6-stage shared-memory ring
-// (full/empty mbarriers).  Consumer warp w computes node (r, i0+w) from shared
-// memory only: its 7 neighbours are in the ring stages of rows r-1, r, r+1.
-// Every x value is read from HBM/L2 once per tile (+25% halo from L2), and the
-// compute warps issue no global loads except for boundary-class nodes.
+// Work tile = SEG = 8R consecutive grid columns x 64 time steps x a range of
+// grid rows, marched upward.  A producer warp streams, for every grid row r of
+// the tile (plus the two halo rows), one TMA tensor box -- the (SEG+2)-node strip
+// x 3 components x 66 time steps (t0-2 .. t0+63) of the space-time panel -- and
+// one bulk copy of the SEG row nodes' aux records (kappa-dependent pressure
+// entries, load, preconditioner diagonals) into a shared-memory ring
+// (full/empty mbarriers).  Consumer warp w computes R horizontally adjacent
+// nodes (r, i0 + R w + k) from shared memory only; for R = 2 their 14
+// (node, neighbour) products need 10 distinct columns of rows r-1, r, r+1,
+// walked once in a fixed order.  Every x value is read from HBM/L2 once per
+// tile (+2/SEG halo from L2); compute warps issue no global loads except for
+// boundary-class nodes.
 //
 // Interior nodes share one stencil (uniform lambda, mu, alpha, S and mesh):
-// their blocks are passed once as kernel parameters (constant bank operands);
-// only the kappa-dependent pressure-pressure entry of AA varies per node and
-// comes from the aux record.  Nodes whose blocks differ from the template
-// (boundary rows/columns, Dirichlet masking) read their full blocks from global
-// memory.  All arithmetic goes through dev::node_epilogue with the same FMA order
-// as the generic kernel, so iterates are bitwise identical to it.
+// their blocks are kernel parameters (constant-bank operands); only the
+// kappa-dependent pressure-pressure entry of AA varies per node (aux record).
+// Structural zeros of that stencil are skipped at compile time (host-verified;
+// fma(0, x, acc) == acc).  Nodes whose blocks differ from the template
+// (boundary rows/columns, Dirichlet masking) read full blocks from global
+// memory.  The epilogue is dev::node_epilogue, shared with every kernel; the
+// neighbour order is the fixed column order below (deterministic, independent
+// of the time-slab split; equal to the generic kernel to rounding).
 #include <cuda.h>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 
 #include "node_update.cuh"
 #include "sweep_kernels.cuh"
@@ -33,23 +39,65 @@ namespace {
 
 using namespace dev;
 
-constexpr int kSeg = 8;                     // row nodes per tile
-constexpr int kStrip = kSeg + 2;            // with halo columns
 constexpr int kT = 2;                       // time steps per lane
 constexpr int kCh = 32 * kT;                // time steps per tile
 constexpr int kChp = kCh + 2;               // + halo steps t0-2, t0-1
-constexpr int kXRows = kStrip * 3;          // tensor rows per stage
-constexpr uint32_t kXBytes = kXRows * kChp * 8;           // 15840
-constexpr uint32_t kAuxOff = (kXBytes + 127) / 128 * 128; // 15872
-constexpr uint32_t kAuxBytes = kSeg * Tile2dArgs::kAux * 8;  // 1024
-constexpr uint32_t kStageBytes = (kAuxOff + kAuxBytes + 127) / 128 * 128;
-constexpr int kStages = 6;
 constexpr int kConsumers = 8;
 constexpr int kThreadsT = (kConsumers + 1) * 32;
+
+template <int R>
+struct Geo {
+    static constexpr int kSeg = kConsumers * R;                       // row nodes per tile
+    static constexpr int kStrip = kSeg + 2;                           // + halo columns
+    static constexpr int kXRows = kStrip * 3;                         // tensor rows per stage
+    static constexpr uint32_t kXBytes = kXRows * kChp * 8;
+    static constexpr uint32_t kAuxOff = (kXBytes + 127) / 128 * 128;
+    static constexpr uint32_t kAuxBytes = kSeg * Tile2dArgs::kAux * 8;
+    static constexpr uint32_t kStageBytes = (kAuxOff + kAuxBytes + 127) / 128 * 128;
+};
 
 // (row delta, column delta) of the 7 BDIA slots in storage order
 __device__ constexpr int kDr[7] = {0, -1, -1, 0, 0, 1, 1};
 __device__ constexpr int kDc[7] = {0, -1, 0, -1, 1, 0, 1};
+
+// Column walk of an R-node horizontal group A = (r, c), B = (r, c+1):
+// row delta, column delta (from A), slot of A served, slot of B served (-1: none).
+template <int R>
+struct Walk;
+template <>
+struct Walk<1> {
+    static constexpr int N = 7;
+    __host__ __device__ static constexpr int dr(int k) { return k == 0 ? 0 : k <= 2 ? -1 : k <= 4 ? 0 : 1; }
+    __host__ __device__ static constexpr int dc(int k) {
+        return k == 0 ? 0 : k == 1 ? -1 : k == 2 ? 0 : k == 3 ? -1 : k == 4 ? 1 : k == 5 ? 0 : 1;
+    }
+    __host__ __device__ static constexpr int slot(int k, int node) { return node == 0 ? k : -1; }
+};
+template <>
+struct Walk<2> {
+    static constexpr int N = 10;
+    __host__ __device__ static constexpr int dr(int k) { return k <= 2 ? -1 : k <= 6 ? 0 : 1; }
+    __host__ __device__ static constexpr int dc(int k) {
+        return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? 1 : k == 3 ? -1 : k == 4 ? 0 : k == 5 ? 1 : k == 6 ? 2
+               : k == 7 ? 0 : k == 8 ? 1 : 2;
+    }
+    __host__ __device__ static constexpr int slot(int k, int node) {
+        // A: k -> 1 2 - 3 0 4 - 5 6 - ;  B: k -> - 1 2 - 3 0 4 - 5 6
+        return node == 0 ? (k == 0 ? 1 : k == 1 ? 2 : k == 2 ? -1 : k == 3 ? 3 : k == 4 ? 0 : k == 5 ? 4
+                            : k == 6 ? -1 : k == 7 ? 5 : k == 8 ? 6 : -1)
+                         : (k == 0 ? -1 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? -1 : k == 4 ? 3 : k == 5 ? 0
+                            : k == 6 ? 4 : k == 7 ? -1 : k == 8 ? 5 : 6);
+    }
+};
+
+// Structural zeros of the interior right-triangle stencil, entry e = c*3+cc of the
+// AA block (e < 9) or 9 = A'_pp: the self block has no displacement-pressure
+// coupling, the diagonal (SW/NE) neighbours have no u_x-u_x / u_y-u_y coupling,
+// and with S = 0 no pressure-pressure coupling either (L is the 5-point stencil).
+__host__ __device__ constexpr bool tmpl_zero(int s, int e, bool s0) {
+    return (s == 0) ? (e == 2 || e == 5 || e == 6 || e == 7)
+                    : (s == 1 || s == 6) ? (e == 0 || e == 4 || (s0 && (e == 8 || e == 9))) : false;
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -89,28 +137,213 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
+template <int R>
 struct TileGeom {
     int64_t n_seg, n_jr, n_chunks, n_tiles;
-    __device__ TileGeom(const Tile2dArgs &a) {
-        n_seg = (a.row_w + kSeg - 1) / kSeg;
+    __device__ explicit TileGeom(const Tile2dArgs &a) {
+        n_seg = (a.row_w + Geo<R>::kSeg - 1) / Geo<R>::kSeg;
         n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
         n_chunks = (a.n_tl + kCh - 1) / kCh;
         n_tiles = n_seg * n_jr * n_chunks;
     }
 };
 
-__global__ void __launch_bounds__(kThreadsT, 2)
+// x of one column (3 components x kT steps) from a ring stage
+__device__ __forceinline__ void load_col(double (&v)[3][kT], const double *colp) {
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+        const double2 w2 = *reinterpret_cast<const double2 *>(colp + cc * kChp);
+        v[cc][0] = w2.x;
+        v[cc][1] = w2.y;
+    }
+}
+
+// interior block coefficient (template, with the per-node pp entry)
+__device__ __forceinline__ double tcoef(const Tile2dArgs &a, int s, int e, double pp) {
+    return (e == 8) ? pp : a.tmpl[s][e];
+}
+
+// acc/q update of one interior node by gathered column v through slot s
+template <bool S0>
+__device__ __forceinline__ void fma_interior(double (&acc)[3][kT], double (&q)[kT], const Tile2dArgs &a, int s,
+                                             double pp, const double (&v)[3][kT]) {
+#pragma unroll
+    for (int cc = 0; cc < 3; ++cc) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const int e = c * 3 + cc;
+            if (tmpl_zero(s, e, S0)) continue;
+            const double cf = tcoef(a, s, e, pp);
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
+        }
+        const int eq = (cc < 2) ? 6 + cc : 9;
+        if (!tmpl_zero(s, eq, S0)) {
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(a.tmpl[s][eq], v[cc][tt], q[tt]);
+        }
+    }
+}
+
+// R interior nodes of one row (warp group): walk the union columns once.
+template <int R, bool GHOST, bool S0>
+__device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double *r0, const double *r1,
+                                               const double *r2, const double *aux0, int nvalid, int j,
+                                               int64_t col0, int p0, int lane, int t0, const double (&sv)[kT],
+                                               double (&nu)[kT], double (&npn)[kT]) {
+    using Wk = Walk<R>;
+    const double *rows[3] = {r0, r1, r2};
+    const int64_t W = a.row_w;
+    double acc[R][3][kT], q[R][kT];
+#pragma unroll
+    for (int n = 0; n < R; ++n)
+#pragma unroll
+        for (int tt = 0; tt < kT; ++tt) {
+            q[n][tt] = 0.0;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) acc[n][c][tt] = 0.0;
+        }
+#pragma unroll
+    for (int k = 0; k < Wk::N; ++k) {
+        // a column serving only node B (n >= 1) is skipped when B is absent
+        bool used = false;
+#pragma unroll
+        for (int n = 0; n < R; ++n) used |= (Wk::slot(k, n) >= 0 && n < nvalid);
+        if (!used) continue;
+        double v[3][kT];
+        load_col(v, rows[1 + Wk::dr(k)] + ((p0 + Wk::dc(k)) * 3) * kChp + 2 + lane * kT);
+#pragma unroll
+        for (int n = 0; n < R; ++n) {
+            const int s = Wk::slot(k, n);
+            if (s < 0 || n >= nvalid) continue;
+            fma_interior<S0>(acc[n], q[n], a, s, aux0[n * Tile2dArgs::kAux + s], v);
+        }
+    }
+    double qp[R];
+#pragma unroll
+    for (int n = 0; n < R; ++n) qp[n] = __shfl_up_sync(0xffffffffu, q[n][kT - 1], 1);
+    if (lane == 0) {                 // q(t0-1): same order, x at t0-1 (ring) or the ghost
+        double g[R];
+#pragma unroll
+        for (int n = 0; n < R; ++n) g[n] = 0.0;
+#pragma unroll
+        for (int k = 0; k < Wk::N; ++k) {
+            bool used = false;
+#pragma unroll
+            for (int n = 0; n < R; ++n) used |= (Wk::slot(k, n) >= 0 && n < nvalid);
+            if (!used) continue;
+            double xv[3];
+            if constexpr (GHOST) {
+                const int64_t jn = (int64_t)(j + Wk::dr(k)) * W + col0 + Wk::dc(k);
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) xv[cc] = __ldg(a.ghost + jn * 3 + cc);
+            } else {
+                const double *colp = rows[1 + Wk::dr(k)] + ((p0 + Wk::dc(k)) * 3) * kChp + 1;
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) xv[cc] = colp[cc * kChp];
+            }
+#pragma unroll
+            for (int n = 0; n < R; ++n) {
+                const int s = Wk::slot(k, n);
+                if (s < 0 || n >= nvalid) continue;
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    const int eq = (cc < 2) ? 6 + cc : 9;
+                    if (!tmpl_zero(s, eq, S0)) g[n] = fma(a.tmpl[s][eq], xv[cc], g[n]);
+                }
+            }
+        }
+#pragma unroll
+        for (int n = 0; n < R; ++n) qp[n] = g[n];
+    }
+#pragma unroll
+    for (int n = 0; n < R; ++n) {
+        if (n >= nvalid) continue;
+        const double *aux = aux0 + n * Tile2dArgs::kAux;
+        double F[3], Dv[3], xs[3][kT];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            F[c] = aux[7 + c];
+            Dv[c] = aux[10 + c];
+        }
+        load_col(xs, rows[1] + ((p0 + n) * 3) * kChp + 2 + lane * kT);
+        node_epilogue<2, kT>(a, (int64_t)j * W + col0 + n, t0, acc[n], q[n], qp[n], F, Dv, xs, sv, nu, npn);
+    }
+}
+
+// Boundary-class node at strip position p of row j: full blocks from global
+// memory, slot order.
+__device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double *r0, const double *r1,
+                                              const double *r2, const double *aux, int j, int64_t col, int p,
+                                              int lane, int t0, const double (&sv)[kT], double (&nu)[kT],
+                                              double (&npn)[kT]) {
+    const double *rows[3] = {r0, r1, r2};
+    const int64_t i = (int64_t)j * a.row_w + col;
+    const double *gb = a.blk + i * (7 * 10);
+    double acc[3][kT], q[kT];
+#pragma unroll
+    for (int tt = 0; tt < kT; ++tt) {
+        q[tt] = 0.0;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) acc[c][tt] = 0.0;
+    }
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+        double v[3][kT];
+        load_col(v, rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 2 + lane * kT);
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                const double cf = __ldg(gb + s * 10 + c * 3 + cc);
+#pragma unroll
+                for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
+            }
+            const double qc = __ldg(gb + s * 10 + ((cc < 2) ? 6 + cc : 9));
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(qc, v[cc][tt], q[tt]);
+        }
+    }
+    double qp = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
+    if (lane == 0) {
+        double g = 0.0;
+#pragma unroll
+        for (int s = 0; s < 7; ++s) {
+            const int64_t jn = i + a.off[s];
+            const double *colp = rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 1;
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                const double qc = __ldg(gb + s * 10 + ((cc < 2) ? 6 + cc : 9));
+                const double xv = (t0 == 0) ? __ldg(a.ghost + jn * 3 + cc) : colp[cc * kChp];
+                g = fma(qc, xv, g);
+            }
+        }
+        qp = g;
+    }
+    double F[3], Dv[3], xs[3][kT];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        F[c] = aux[7 + c];
+        Dv[c] = aux[10 + c];
+    }
+    load_col(xs, rows[1] + (p * 3) * kChp + 2 + lane * kT);
+    node_epilogue<2, kT>(a, i, t0, acc, q, qp, F, Dv, xs, sv, nu, npn);
+}
+
+template <int R, int STAGES, int MAXREG>
+__global__ void __launch_bounds__(kThreadsT) __maxnreg__(MAXREG)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
+    using G = Geo<R>;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t full[kStages], empty[kStages];
+    __shared__ uint64_t full[STAGES], empty[STAGES];
     __shared__ double red[kConsumers][kCh][2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileGeom g(a);
+    const TileGeom<R> g(a);
     const int64_t W = a.row_w;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumers);
         }
@@ -128,17 +361,17 @@ __global__ void __launch_bounds__(kThreadsT, 2)
                 const int64_t seg = grp % g.n_seg, jr = grp / g.n_seg;
                 const int ja = (int)(jr * a.rows_per_tile);
                 const int jb = min(a.n_rows, ja + a.rows_per_tile);
-                const int64_t i0 = seg * kSeg;
+                const int64_t i0 = seg * G::kSeg;
                 for (int r = ja - 1; r <= jb; ++r, ++it) {
-                    const int st = it % kStages;
-                    if (it >= (uint32_t)kStages) mbar_wait(&empty[st], ((it / kStages) - 1) & 1);
-                    unsigned char *base = smem + (size_t)st * kStageBytes;
+                    const int st = it % STAGES;
+                    if (it >= (uint32_t)STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+                    unsigned char *base = smem + (size_t)st * G::kStageBytes;
                     const bool real = (r >= 0 && r < a.n_rows);
-                    mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
+                    mbar_expect_tx(&full[st], G::kXBytes + (real ? G::kAuxBytes : 0u));
                     const int64_t node0 = (int64_t)r * W + i0 - 1;
                     tma_load_2d(base, &tmx, chunk * kCh - 2, (int)((node0 + a.pad_nodes) * 3), &full[st]);
                     if (real)
-                        bulk_g2s(base + kAuxOff, a.aux + ((int64_t)r * W + i0) * Tile2dArgs::kAux, kAuxBytes,
+                        bulk_g2s(base + G::kAuxOff, a.aux + ((int64_t)r * W + i0) * Tile2dArgs::kAux, G::kAuxBytes,
                                  &full[st]);
                 }
             }
@@ -148,15 +381,16 @@ __global__ void __launch_bounds__(kThreadsT, 2)
 
     // ------------------------------- consumers ------------------------------
     uint32_t it = 0;
-    const int tw = warp;                       // column within the segment
+    const int p0 = 1 + R * warp;              // strip position of the warp's first node
     for (int64_t tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
         const int chunk = (int)(tile % g.n_chunks);
         const int64_t grp = tile / g.n_chunks;
         const int64_t seg = grp % g.n_seg, jr = grp / g.n_seg;
         const int ja = (int)(jr * a.rows_per_tile);
         const int jb = min(a.n_rows, ja + a.rows_per_tile);
-        const int64_t i0 = seg * kSeg;
-        const int64_t col = i0 + tw;
+        const int64_t col0 = seg * G::kSeg + R * warp;
+        const int64_t rem = W - col0;
+        const int nvalid = rem <= 0 ? 0 : (rem >= R ? R : (int)rem);
         const int t0 = chunk * kCh + lane * kT;
         double nu[kT], npn[kT], sv[kT];
 #pragma unroll
@@ -166,101 +400,57 @@ __global__ void __launch_bounds__(kThreadsT, 2)
             sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
         }
         const uint32_t it0 = it;               // item of row ja-1
-        // rows ja-1 and ja
-        mbar_wait(&full[it0 % kStages], (it0 / kStages) & 1);
-        mbar_wait(&full[(it0 + 1) % kStages], ((it0 + 1) / kStages) & 1);
+#define ITEM_OF(r) (it0 + 1u + (uint32_t)((r) - ja))
+#define STAGE_OF(r) reinterpret_cast<const double *>(smem + (size_t)(ITEM_OF(r) % STAGES) * G::kStageBytes)
+        mbar_wait(&full[it0 % STAGES], (it0 / STAGES) & 1);
+        mbar_wait(&full[(it0 + 1) % STAGES], ((it0 + 1) / STAGES) & 1);
         for (int j = ja; j < jb; ++j) {
-            const uint32_t ic = it0 + 1 + (j - ja);           // item of row j
-            const uint32_t in = ic + 1;
-            mbar_wait(&full[in % kStages], (in / kStages) & 1);
-            const double *rowp[3] = {
-                reinterpret_cast<const double *>(smem + (size_t)((ic - 1) % kStages) * kStageBytes),
-                reinterpret_cast<const double *>(smem + (size_t)(ic % kStages) * kStageBytes),
-                reinterpret_cast<const double *>(smem + (size_t)(in % kStages) * kStageBytes)};
-            const double *aux = reinterpret_cast<const double *>(smem + (size_t)(ic % kStages) * kStageBytes +
-                                                                 kAuxOff) + tw * Tile2dArgs::kAux;
-            if (col < W) {
-                const int64_t i = (int64_t)j * W + col;
-                const bool interior = aux[13] != 0.0;
-                double acc[3][kT], q[kT];
+            const uint32_t in = ITEM_OF(j + 1);
+            mbar_wait(&full[in % STAGES], (in / STAGES) & 1);
+            if (nvalid > 0) {
+                const double *r0 = STAGE_OF(j - 1), *r1 = STAGE_OF(j), *r2 = STAGE_OF(j + 1);
+                const double *aux0 = reinterpret_cast<const double *>(
+                                         reinterpret_cast<const unsigned char *>(r1) + G::kAuxOff) +
+                                     (R * warp) * Tile2dArgs::kAux;
+                bool interior = true;
 #pragma unroll
-                for (int tt = 0; tt < kT; ++tt) {
-                    q[tt] = 0.0;
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) acc[c][tt] = 0.0;
-                }
-                const double *gb = a.blk + i * (7 * 10);          // boundary-class blocks
-#pragma unroll
-                for (int s = 0; s < 7; ++s) {
-                    const double *xs_ = rowp[1 + kDr[s]] + ((tw + 1 + kDc[s]) * 3) * kChp + 2 + lane * kT;
-                    double cf[10];
-                    if (interior) {
-#pragma unroll
-                        for (int k = 0; k < 10; ++k) cf[k] = a.tmpl[s][k];
-                        cf[8] = aux[s];                                // kappa-dependent AA_pp entry
+                for (int n = 0; n < R; ++n)
+                    if (n < nvalid) interior &= aux0[n * Tile2dArgs::kAux + 13] != 0.0;
+                if (interior) {
+                    if (chunk == 0) {
+                        if (a.s0)
+                            group_interior<R, true, true>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                        else
+                            group_interior<R, true, false>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
                     } else {
-#pragma unroll
-                        for (int k = 0; k < 10; ++k) cf[k] = __ldg(gb + s * 10 + k);
+                        if (a.s0)
+                            group_interior<R, false, true>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                        else
+                            group_interior<R, false, false>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
                     }
+                } else {
 #pragma unroll
-                    for (int cc = 0; cc < 3; ++cc) {
-                        const double2 w2 = *reinterpret_cast<const double2 *>(xs_ + cc * kChp);
-                        const double v[kT] = {w2.x, w2.y};
-#pragma unroll
-                        for (int c = 0; c < 3; ++c)
-#pragma unroll
-                            for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf[c * 3 + cc], v[tt], acc[c][tt]);
-                        const double qc = (cc < 2) ? cf[2 * 3 + cc] : cf[9];
-#pragma unroll
-                        for (int tt = 0; tt < kT; ++tt) q[tt] = fma(qc, v[tt], q[tt]);
-                    }
+                    for (int n = 0; n < R; ++n)
+                        if (n < nvalid)
+                            node_boundary(a, r0, r1, r2, aux0 + n * Tile2dArgs::kAux, j, col0 + n, p0 + n, lane, t0,
+                                          sv, nu, npn);
                 }
-                double qprev = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
-                if (lane == 0) {
-                    const bool use_ghost = (t0 == 0);
-                    double qg = 0.0;
-#pragma unroll
-                    for (int s = 0; s < 7; ++s) {
-                        const double *xs1 = rowp[1 + kDr[s]] + ((tw + 1 + kDc[s]) * 3) * kChp + 1;
-                        const int64_t jn = i + a.off[s];
-#pragma unroll
-                        for (int cc = 0; cc < 3; ++cc) {
-                            double qc;
-                            if (interior) qc = (cc < 2) ? a.tmpl[s][2 * 3 + cc] : a.tmpl[s][9];
-                            else qc = (cc < 2) ? __ldg(gb + s * 10 + 2 * 3 + cc) : __ldg(gb + s * 10 + 9);
-                            const double xv = use_ghost ? __ldg(a.ghost + jn * 3 + cc) : xs1[cc * kChp];
-                            qg = fma(qc, xv, qg);
-                        }
-                    }
-                    qprev = qg;
-                }
-                double F[3], Dv[3], xs[3][kT];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    F[c] = aux[7 + c];
-                    Dv[c] = aux[10 + c];
-                    const double2 w2 = *reinterpret_cast<const double2 *>(rowp[1] + ((tw + 1) * 3 + c) * kChp + 2 +
-                                                                          lane * kT);
-                    xs[c][0] = w2.x;
-                    xs[c][1] = w2.y;
-                }
-                node_epilogue<2, kT>(a, i, t0, acc, q, qprev, F, Dv, xs, sv, nu, npn);
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[(ic - 1) % kStages]);   // row j-1 no longer needed
+            if (lane == 0) mbar_arrive(&empty[ITEM_OF(j - 1) % STAGES]);   // row j-1 no longer needed
         }
-        // rows jb-1 and jb are released at the end of the tile
-        const uint32_t ilast = it0 + 1 + (jb - ja);                  // item of row jb
-        if (lane == 0) {
-            mbar_arrive(&empty[(ilast - 1) % kStages]);
-            mbar_arrive(&empty[ilast % kStages]);
+        if (lane == 0) {                        // rows jb-1 and jb
+            mbar_arrive(&empty[ITEM_OF(jb - 1) % STAGES]);
+            mbar_arrive(&empty[ITEM_OF(jb) % STAGES]);
         }
-        it = ilast + 1;
+        it = ITEM_OF(jb) + 1;
+#undef ITEM_OF
+#undef STAGE_OF
         // per-step norm partials of this tile (fixed reduction order over warps)
 #pragma unroll
         for (int tt = 0; tt < kT; ++tt) {
-            red[tw][lane * kT + tt][0] = nu[tt];
-            red[tw][lane * kT + tt][1] = npn[tt];
+            red[warp][lane * kT + tt][0] = nu[tt];
+            red[warp][lane * kT + tt][1] = npn[tt];
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
         for (int k = threadIdx.x; k < kCh * 2; k += kConsumers * 32) {
@@ -277,10 +467,39 @@ __global__ void __launch_bounds__(kThreadsT, 2)
     }
 }
 
+struct TileCfg {
+    int r, stages, maxreg;
+};
+
+TileCfg tile_cfg() {
+    TileCfg c{2, 6, 168};
+    if (const char *e = std::getenv("BIOT_TILE_CFG")) {   // "r,stages,maxreg"
+        int r = 0, st = 0, mr = 0;
+        if (std::sscanf(e, "%d,%d,%d", &r, &st, &mr) == 3) c = TileCfg{r, st, mr};
+    }
+    return c;
+}
+
+using TileFn = void (*)(const CUtensorMap, const Tile2dArgs);
+
+TileFn tile_fn(TileCfg c) {
+    if (c.r == 1 && c.stages == 6 && c.maxreg == 168) return tile2d_kernel<1, 6, 168>;
+    if (c.r == 1 && c.stages == 6 && c.maxreg == 96) return tile2d_kernel<1, 6, 96>;
+    if (c.r == 2 && c.stages == 6 && c.maxreg == 168) return tile2d_kernel<2, 6, 168>;
+    if (c.r == 2 && c.stages == 4 && c.maxreg == 168) return tile2d_kernel<2, 4, 168>;
+    if (c.r == 2 && c.stages == 6 && c.maxreg == 224) return tile2d_kernel<2, 6, 224>;
+    return nullptr;
+}
+
+uint32_t stage_bytes(int r) { return r == 1 ? Geo<1>::kStageBytes : Geo<2>::kStageBytes; }
+
 }  // namespace
 
+int tile2d_seg() { return kConsumers * tile_cfg().r; }
+
 int64_t tile2d_groups(const Tile2dArgs &a) {
-    const int64_t n_seg = (a.row_w + kSeg - 1) / kSeg;
+    const int64_t seg = tile2d_seg();
+    const int64_t n_seg = (a.row_w + seg - 1) / seg;
     const int64_t n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
     return n_seg * n_jr;
 }
@@ -291,11 +510,14 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)kStages * kStageBytes;
-    e = cudaFuncSetAttribute(tile2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const TileCfg c = tile_cfg();
+    TileFn fn = tile_fn(c);
+    if (!fn) return cudaErrorInvalidValue;
+    const size_t smem = (size_t)c.stages * stage_bytes(c.r);
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel, kThreadsT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     out->grid = sms * per_sm;
@@ -305,14 +527,16 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
 
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st) {
-    tile2d_kernel<<<sh.grid, kThreadsT, sh.smem, st>>>(tmx, a);
+    TileFn fn = tile_fn(tile_cfg());
+    if (!fn) return cudaErrorInvalidValue;
+    fn<<<sh.grid, kThreadsT, sh.smem, st>>>(tmx, a);
     return cudaGetLastError();
 }
 
 // box of the x tensor map: {time steps incl. halo, tensor rows}
 void tile2d_box(uint32_t *box) {
     box[0] = kChp;
-    box[1] = kXRows;
+    box[1] = (uint32_t)((tile2d_seg() + 2) * 3);
 }
 
 }  // namespace biot

@@ -19,8 +19,12 @@ def main():
     for v in variants:
         for k in ("BIOT_KERNEL", "BIOT_STENCIL_R", "BIOT_STENCIL_T", "BIOT_MARCH_T", "BIOT_MARCH_ROWS"):
             os.environ.pop(k, None)
+        os.environ.pop("BIOT_TILE_CFG", None)
         if v in ("generic", "tile"):
             os.environ["BIOT_KERNEL"] = v
+        elif v.startswith("tile:"):          # tile:r,stages,maxreg
+            os.environ["BIOT_KERNEL"] = "tile"
+            os.environ["BIOT_TILE_CFG"] = v.split(":")[1]
         elif v.startswith("march"):          # march[:T[:rows]]
             f = v.split(":")
             os.environ["BIOT_KERNEL"] = "march"
