@@ -141,6 +141,7 @@ struct biot_ctx {
     CUtensorMap tmap[2];
     int64_t n_interior = 0;
     int s0 = 0;                       // tile2d zero-storage structural-zero variant
+    int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
     int sR = 4, sT = 2;
     int64_t gbase[8] = {0};
     int32_t slot[8][3] = {{0}};
@@ -323,6 +324,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
         a.aux = c->aux;
         a.pad_nodes = c->pad;
         a.s0 = c->s0;
+        a.dry = c->tile_dry;
         return biot::launch_tile2d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     biot::SweepArgs a = sweep_args(c, mode, xin, xout);
@@ -662,6 +664,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const bool z0 = base_ok && ctx->tmpl[1][9] == 0.0 && ctx->tmpl[6][9] == 0.0 &&
                         ctx->tmpl[1][8] == 0.0 && ctx->tmpl[6][8] == 0.0;
         ctx->s0 = z0 ? 1 : 0;
+        if (const char *e = std::getenv("BIOT_TILE_DRY")) ctx->tile_dry = std::atoi(e) != 0;
         std::vector<double> aux((size_t)ctx->n_alloc * KA, 0.0);
         int64_t n_int = 0;
         for (int64_t i = 0; i < ctx->N; ++i) {

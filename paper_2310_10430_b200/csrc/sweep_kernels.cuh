@@ -72,6 +72,7 @@ struct Tile2dArgs : SweepArgs {
     const double *aux;                // [n_alloc][kAux]
     int64_t pad_nodes;                // panel rows start at node -pad_nodes
     int32_t s0;                       // zero-storage variant: extra structural zeros (see tile2d)
+    int32_t dry;                      // dev/measurement only: stream the ring without computing
 };
 
 struct LaunchShape {

@@ -42,12 +42,9 @@ using namespace dev;
 constexpr int kT = 2;                       // time steps per lane
 constexpr int kCh = 32 * kT;                // time steps per tile
 constexpr int kChp = kCh + 2;               // + halo steps t0-2, t0-1
-constexpr int kConsumers = 8;
-constexpr int kThreadsT = (kConsumers + 1) * 32;
-
-template <int R>
+template <int R, int NC>
 struct Geo {
-    static constexpr int kSeg = kConsumers * R;                       // row nodes per tile
+    static constexpr int kSeg = NC * R;                               // row nodes per tile
     static constexpr int kStrip = kSeg + 2;                           // + halo columns
     static constexpr int kXRows = kStrip * 3;                         // tensor rows per stage
     static constexpr uint32_t kXBytes = kXRows * kChp * 8;
@@ -122,6 +119,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
             : "memory");
     }
 }
+// producer-side wait: back off between polls so the spinning thread does not
+// take issue slots from the consumer warps sharing its scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (true) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) break;
+        __nanosleep(200);
+    }
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
@@ -137,11 +148,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
         : "memory");
 }
 
-template <int R>
+template <int SEG>
 struct TileGeom {
     int64_t n_seg, n_jr, n_chunks, n_tiles;
     __device__ explicit TileGeom(const Tile2dArgs &a) {
-        n_seg = (a.row_w + Geo<R>::kSeg - 1) / Geo<R>::kSeg;
+        n_seg = (a.row_w + SEG - 1) / SEG;
         n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
         n_chunks = (a.n_tl + kCh - 1) / kCh;
         n_tiles = n_seg * n_jr * n_chunks;
@@ -188,7 +199,7 @@ __device__ __forceinline__ void fma_interior(double (&acc)[3][kT], double (&q)[k
 // R interior nodes of one row (warp group): walk the union columns once.
 template <int R, bool GHOST, bool S0>
 __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double *r0, const double *r1,
-                                               const double *r2, const double *aux0, int nvalid, int j,
+                                               const double *r2, const double *aux0, int j,
                                                int64_t col0, int p0, int lane, int t0, const double (&sv)[kT],
                                                double (&nu)[kT], double (&npn)[kT]) {
     using Wk = Walk<R>;
@@ -205,17 +216,12 @@ __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double
         }
 #pragma unroll
     for (int k = 0; k < Wk::N; ++k) {
-        // a column serving only node B (n >= 1) is skipped when B is absent
-        bool used = false;
-#pragma unroll
-        for (int n = 0; n < R; ++n) used |= (Wk::slot(k, n) >= 0 && n < nvalid);
-        if (!used) continue;
         double v[3][kT];
         load_col(v, rows[1 + Wk::dr(k)] + ((p0 + Wk::dc(k)) * 3) * kChp + 2 + lane * kT);
 #pragma unroll
         for (int n = 0; n < R; ++n) {
             const int s = Wk::slot(k, n);
-            if (s < 0 || n >= nvalid) continue;
+            if (s < 0) continue;
             fma_interior<S0>(acc[n], q[n], a, s, aux0[n * Tile2dArgs::kAux + s], v);
         }
     }
@@ -228,10 +234,6 @@ __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double
         for (int n = 0; n < R; ++n) g[n] = 0.0;
 #pragma unroll
         for (int k = 0; k < Wk::N; ++k) {
-            bool used = false;
-#pragma unroll
-            for (int n = 0; n < R; ++n) used |= (Wk::slot(k, n) >= 0 && n < nvalid);
-            if (!used) continue;
             double xv[3];
             if constexpr (GHOST) {
                 const int64_t jn = (int64_t)(j + Wk::dr(k)) * W + col0 + Wk::dc(k);
@@ -245,7 +247,7 @@ __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double
 #pragma unroll
             for (int n = 0; n < R; ++n) {
                 const int s = Wk::slot(k, n);
-                if (s < 0 || n >= nvalid) continue;
+                if (s < 0) continue;
 #pragma unroll
                 for (int cc = 0; cc < 3; ++cc) {
                     const int eq = (cc < 2) ? 6 + cc : 9;
@@ -258,7 +260,6 @@ __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double
     }
 #pragma unroll
     for (int n = 0; n < R; ++n) {
-        if (n >= nvalid) continue;
         const double *aux = aux0 + n * Tile2dArgs::kAux;
         double F[3], Dv[3], xs[3][kT];
 #pragma unroll
@@ -330,16 +331,17 @@ __device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double 
     node_epilogue<2, kT>(a, i, t0, acc, q, qp, F, Dv, xs, sv, nu, npn);
 }
 
-template <int R, int STAGES, int MAXREG>
-__global__ void __launch_bounds__(kThreadsT) __maxnreg__(MAXREG)
+template <int R, int NC, int STAGES, int MAXREG>
+__global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
-    using G = Geo<R>;
+    using G = Geo<R, NC>;
+    constexpr int kConsumers = NC;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[STAGES], empty[STAGES];
     __shared__ double red[kConsumers][kCh][2];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileGeom<R> g(a);
+    const TileGeom<G::kSeg> g(a);
     const int64_t W = a.row_w;
 
     if (threadIdx.x == 0) {
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(kThreadsT) __maxnreg__(MAXREG)
                 const int64_t i0 = seg * G::kSeg;
                 for (int r = ja - 1; r <= jb; ++r, ++it) {
                     const int st = it % STAGES;
-                    if (it >= (uint32_t)STAGES) mbar_wait(&empty[st], ((it / STAGES) - 1) & 1);
+                    if (it >= (uint32_t)STAGES) mbar_wait_sleep(&empty[st], ((it / STAGES) - 1) & 1);
                     unsigned char *base = smem + (size_t)st * G::kStageBytes;
                     const bool real = (r >= 0 && r < a.n_rows);
                     mbar_expect_tx(&full[st], G::kXBytes + (real ? G::kAuxBytes : 0u));
@@ -407,26 +409,25 @@ __global__ void __launch_bounds__(kThreadsT) __maxnreg__(MAXREG)
         for (int j = ja; j < jb; ++j) {
             const uint32_t in = ITEM_OF(j + 1);
             mbar_wait(&full[in % STAGES], (in / STAGES) & 1);
-            if (nvalid > 0) {
+            if (nvalid > 0 && !a.dry) {
                 const double *r0 = STAGE_OF(j - 1), *r1 = STAGE_OF(j), *r2 = STAGE_OF(j + 1);
                 const double *aux0 = reinterpret_cast<const double *>(
                                          reinterpret_cast<const unsigned char *>(r1) + G::kAuxOff) +
                                      (R * warp) * Tile2dArgs::kAux;
-                bool interior = true;
+                bool interior = (nvalid == R);   // partial groups (last segment) take the generic path
 #pragma unroll
-                for (int n = 0; n < R; ++n)
-                    if (n < nvalid) interior &= aux0[n * Tile2dArgs::kAux + 13] != 0.0;
+                for (int n = 0; n < R; ++n) interior &= aux0[n * Tile2dArgs::kAux + 13] != 0.0;
                 if (interior) {
                     if (chunk == 0) {
                         if (a.s0)
-                            group_interior<R, true, true>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                            group_interior<R, true, true>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
                         else
-                            group_interior<R, true, false>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                            group_interior<R, true, false>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
                     } else {
                         if (a.s0)
-                            group_interior<R, false, true>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                            group_interior<R, false, true>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
                         else
-                            group_interior<R, false, false>(a, r0, r1, r2, aux0, nvalid, j, col0, p0, lane, t0, sv, nu, npn);
+                            group_interior<R, false, false>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
                     }
                 } else {
 #pragma unroll
@@ -468,14 +469,14 @@ __global__ void __launch_bounds__(kThreadsT) __maxnreg__(MAXREG)
 }
 
 struct TileCfg {
-    int r, stages, maxreg;
+    int r, nc, stages, maxreg;
 };
 
 TileCfg tile_cfg() {
-    TileCfg c{2, 6, 168};
-    if (const char *e = std::getenv("BIOT_TILE_CFG")) {   // "r,stages,maxreg"
-        int r = 0, st = 0, mr = 0;
-        if (std::sscanf(e, "%d,%d,%d", &r, &st, &mr) == 3) c = TileCfg{r, st, mr};
+    TileCfg c{1, 15, 6, 128};
+    if (const char *e = std::getenv("BIOT_TILE_CFG")) {   // "r,consumers,stages,maxreg"
+        int r = 0, nc = 0, st = 0, mr = 0;
+        if (std::sscanf(e, "%d,%d,%d,%d", &r, &nc, &st, &mr) == 4) c = TileCfg{r, nc, st, mr};
     }
     return c;
 }
@@ -483,19 +484,29 @@ TileCfg tile_cfg() {
 using TileFn = void (*)(const CUtensorMap, const Tile2dArgs);
 
 TileFn tile_fn(TileCfg c) {
-    if (c.r == 1 && c.stages == 6 && c.maxreg == 168) return tile2d_kernel<1, 6, 168>;
-    if (c.r == 1 && c.stages == 6 && c.maxreg == 96) return tile2d_kernel<1, 6, 96>;
-    if (c.r == 2 && c.stages == 6 && c.maxreg == 168) return tile2d_kernel<2, 6, 168>;
-    if (c.r == 2 && c.stages == 4 && c.maxreg == 168) return tile2d_kernel<2, 4, 168>;
-    if (c.r == 2 && c.stages == 6 && c.maxreg == 224) return tile2d_kernel<2, 6, 224>;
+#define BIOT_TCFG(R_, NC_, ST_, MR_) \
+    if (c.r == R_ && c.nc == NC_ && c.stages == ST_ && c.maxreg == MR_) return tile2d_kernel<R_, NC_, ST_, MR_>;
+    BIOT_TCFG(2, 8, 6, 168)
+    BIOT_TCFG(1, 8, 6, 168)
+    BIOT_TCFG(1, 12, 6, 128)
+    BIOT_TCFG(1, 15, 6, 128)
+    BIOT_TCFG(1, 11, 6, 168)
+    BIOT_TCFG(2, 7, 6, 168)
+    BIOT_TCFG(2, 11, 5, 128)
+#undef BIOT_TCFG
     return nullptr;
 }
 
-uint32_t stage_bytes(int r) { return r == 1 ? Geo<1>::kStageBytes : Geo<2>::kStageBytes; }
+uint32_t stage_bytes(TileCfg c) {
+    const uint32_t seg = c.r * c.nc;
+    const uint32_t xb = (seg + 2) * 3 * kChp * 8;
+    const uint32_t off = (xb + 127) / 128 * 128;
+    return (off + seg * Tile2dArgs::kAux * 8 + 127) / 128 * 128;
+}
 
 }  // namespace
 
-int tile2d_seg() { return kConsumers * tile_cfg().r; }
+int tile2d_seg() { return tile_cfg().nc * tile_cfg().r; }
 
 int64_t tile2d_groups(const Tile2dArgs &a) {
     const int64_t seg = tile2d_seg();
@@ -513,11 +524,11 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     const TileCfg c = tile_cfg();
     TileFn fn = tile_fn(c);
     if (!fn) return cudaErrorInvalidValue;
-    const size_t smem = (size_t)c.stages * stage_bytes(c.r);
+    const size_t smem = (size_t)c.stages * stage_bytes(c);
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreadsT, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (c.nc + 1) * 32, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     out->grid = sms * per_sm;
@@ -527,9 +538,10 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
 
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st) {
-    TileFn fn = tile_fn(tile_cfg());
+    const TileCfg c = tile_cfg();
+    TileFn fn = tile_fn(c);
     if (!fn) return cudaErrorInvalidValue;
-    fn<<<sh.grid, kThreadsT, sh.smem, st>>>(tmx, a);
+    fn<<<sh.grid, (c.nc + 1) * 32, sh.smem, st>>>(tmx, a);
     return cudaGetLastError();
 }
 

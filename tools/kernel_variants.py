@@ -20,6 +20,10 @@ def main():
         for k in ("BIOT_KERNEL", "BIOT_STENCIL_R", "BIOT_STENCIL_T", "BIOT_MARCH_T", "BIOT_MARCH_ROWS"):
             os.environ.pop(k, None)
         os.environ.pop("BIOT_TILE_CFG", None)
+        os.environ.pop("BIOT_TILE_DRY", None)
+        if v.endswith(":dry"):
+            os.environ["BIOT_TILE_DRY"] = "1"
+            v = v[:-4]
         if v in ("generic", "tile"):
             os.environ["BIOT_KERNEL"] = v
         elif v.startswith("tile:"):          # tile:r,stages,maxreg
@@ -37,6 +41,8 @@ def main():
             os.environ["BIOT_KERNEL"] = "stencil"
             os.environ["BIOT_STENCIL_R"], os.environ["BIOT_STENCIL_T"] = r, t
         for pc in (2, 1):
+            if os.environ.get("BIOT_TILE_DRY") and pc == 1:
+                continue
             try:
                 g = BiotSolver(prob, precond=pc, omega=0.5)
             except Exception as e:  # unsupported combination
