@@ -200,6 +200,15 @@ void free_all(biot_ctx *c) {
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
 
+// Every transfer of a context goes on its own stream: the stream may be
+// non-blocking, so mixing it with legacy-default-stream copies would race (a
+// zero-fill enqueued earlier could land after an upload).
+cudaError_t h2d(biot_ctx *c, void *dst, const void *src, size_t bytes) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamSynchronize(c->stream);
+}
+
 biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xout) {
     biot::SweepArgs a{};
     a.x = xin;
@@ -586,33 +595,32 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         std::vector<double> x0(bc->x_initial, bc->x_initial + (size_t)ctx->N * nc);
         for (size_t q = 0; q < x0.size(); ++q)
             if (op->fixed[q]) x0[q] = 0.0;
-        CU(cudaMemcpy(ctx->ghost, x0.data(), vec_bytes, cudaMemcpyHostToDevice));
+        CU(h2d(ctx, ctx->ghost, x0.data(), vec_bytes));
     }
     // operator arrays padded to n_alloc nodes with zeros (dummy rows of the blocked kernel)
     const size_t blk_bytes = (size_t)ctx->n_alloc * ctx->S * W * sizeof(double);
     ALLOC(ctx->blk, blk_bytes);
     CU(cudaMemsetAsync(ctx->blk, 0, blk_bytes, ctx->stream));
-    CU(cudaMemcpy(ctx->blk, op->blk.data(), op->blk.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(h2d(ctx, ctx->blk, op->blk.data(), op->blk.size() * sizeof(double)));
     if (ctx->path == biot::PATH_ELL) {
         ALLOC(ctx->cols, op->cols.size() * sizeof(int32_t));
-        CU(cudaMemcpy(ctx->cols, op->cols.data(), op->cols.size() * sizeof(int32_t),
-                      cudaMemcpyHostToDevice));
+        CU(h2d(ctx, ctx->cols, op->cols.data(), op->cols.size() * sizeof(int32_t)));
     }
     const size_t vec_alloc = (size_t)ctx->n_alloc * nc * sizeof(double);
     ALLOC(ctx->load, vec_alloc);
     CU(cudaMemsetAsync(ctx->load, 0, vec_alloc, ctx->stream));
-    CU(cudaMemcpy(ctx->load, op->load.data(), vec_bytes, cudaMemcpyHostToDevice));
+    CU(h2d(ctx, ctx->load, op->load.data(), vec_bytes));
     ALLOC(ctx->dinv, vec_alloc);
     CU(cudaMemsetAsync(ctx->dinv, 0, vec_alloc, ctx->stream));
-    CU(cudaMemcpy(ctx->dinv, op->dinv.data(), vec_bytes, cudaMemcpyHostToDevice));
+    CU(h2d(ctx, ctx->dinv, op->dinv.data(), vec_bytes));
     ALLOC(ctx->fixed, (size_t)ctx->N * nc);
-    CU(cudaMemcpy(ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc, cudaMemcpyHostToDevice));
+    CU(h2d(ctx, ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc));
     {
         std::vector<double> sl(ctx->pitch, 0.0);
         for (int32_t t = 0; t < ctx->n_tl; ++t)
             sl[t] = bc->load_scale ? bc->load_scale[ctx->first_step - 1 + t] : 1.0;
         ALLOC(ctx->s, sl.size() * sizeof(double));
-        CU(cudaMemcpy(ctx->s, sl.data(), sl.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CU(h2d(ctx, ctx->s, sl.data(), sl.size() * sizeof(double)));
     }
     ALLOC(ctx->sendbuf, vec_bytes);
     CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
@@ -665,7 +673,10 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                         ctx->tmpl[1][8] == 0.0 && ctx->tmpl[6][8] == 0.0;
         ctx->s0 = z0 ? 1 : 0;
         if (const char *e = std::getenv("BIOT_TILE_DRY")) ctx->tile_dry = std::atoi(e) != 0;
-        std::vector<double> aux((size_t)ctx->n_alloc * KA, 0.0);
+        // records for every node a tile's bulk copy can touch: the last row's segment may
+        // extend up to one segment past node N-1
+        const int64_t aux_nodes = ctx->N + 2 * biot::tile2d_seg() + 8;
+        std::vector<double> aux((size_t)aux_nodes * KA, 0.0);
         int64_t n_int = 0;
         for (int64_t i = 0; i < ctx->N; ++i) {
             const double *b = op->blk.data() + (size_t)i * S * WB;
@@ -688,7 +699,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         }
         ctx->n_interior = n_int;
         ALLOC(ctx->aux, aux.size() * sizeof(double));
-        CU(cudaMemcpy(ctx->aux, aux.data(), aux.size() * sizeof(double), cudaMemcpyHostToDevice));
+        CU(h2d(ctx, ctx->aux, aux.data(), aux.size() * sizeof(double)));
         // TMA tensor maps of the two panels: {time (pitch), panel rows}
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult qres;
@@ -803,7 +814,8 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
     ctx->last_ms_iter = tot / K;
     ctx->last_ms_sweep = sweep_ms / K;
     int nf = 0;
-    CU(cudaMemcpy(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     if (nf) return fail(ctx, BIOT_E_NONFINITE, "a residual norm became non-finite");
     return BIOT_OK;
 }

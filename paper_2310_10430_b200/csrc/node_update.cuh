@@ -30,8 +30,8 @@ __device__ __forceinline__ double cload(const double *p) {
 // Epilogue of one node over the lane's T steps (shared by every sweep kernel so the
 // arithmetic is identical): r = s_t f + q(t-1) - acc, norms, z = P^-1 r (P~2, or the
 // displacement half of P~1), x^{k+1} = x^k + omega z, stores.
-template <int D, int T>
-__device__ __forceinline__ void node_epilogue(const SweepArgs &a, int64_t i, int t0,
+template <int D, int T, class A>
+__device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
                                               const double (&acc)[D + 1][T], const double (&q)[T],
                                               double qprev, const double (&F)[D + 1],
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],

@@ -272,13 +272,31 @@ __device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double
     }
 }
 
+// Everything the boundary path reads from the kernel parameters (so the
+// out-of-line function does not force the whole parameter block into local
+// memory); also what node_epilogue needs.
+struct BArgs {
+    double *xn, *zbuf, *sendbuf;
+    const double *blk, *ghost;
+    int64_t pitch, row_w;
+    int64_t off[7];
+    int32_t n_tl, mode;
+    double omega;
+};
+
+struct Norms2 {
+    double nu[kT], npn[kT];
+};
+
 // Boundary-class node at strip position p of row j: full blocks from global
-// memory, slot order.
-__device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double *r0, const double *r1,
-                                              const double *r2, const double *aux, int j, int64_t col, int p,
-                                              int lane, int t0, const double (&sv)[kT], double (&nu)[kT],
-                                              double (&npn)[kT]) {
+// memory, slot order.  Rare (domain edges, Dirichlet neighbourhoods): kept out of
+// line so its register footprint does not burden the interior path.
+__device__ __noinline__ Norms2 node_boundary(const BArgs &a, const double *r0, const double *r1,
+                                             const double *r2, const double *aux, int j, int64_t col, int p,
+                                             int lane, int t0, double sv0, double sv1) {
     const double *rows[3] = {r0, r1, r2};
+    const double sv[kT] = {sv0, sv1};
+    double nu[kT] = {0.0, 0.0}, npn[kT] = {0.0, 0.0};
     const int64_t i = (int64_t)j * a.row_w + col;
     const double *gb = a.blk + i * (7 * 10);
     double acc[3][kT], q[kT];
@@ -288,7 +306,7 @@ __device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double 
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c][tt] = 0.0;
     }
-#pragma unroll
+#pragma unroll 1
     for (int s = 0; s < 7; ++s) {
         double v[3][kT];
         load_col(v, rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 2 + lane * kT);
@@ -308,7 +326,6 @@ __device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double 
     double qp = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
     if (lane == 0) {
         double g = 0.0;
-#pragma unroll
         for (int s = 0; s < 7; ++s) {
             const int64_t jn = i + a.off[s];
             const double *colp = rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 1;
@@ -329,6 +346,13 @@ __device__ __forceinline__ void node_boundary(const Tile2dArgs &a, const double 
     }
     load_col(xs, rows[1] + (p * 3) * kChp + 2 + lane * kT);
     node_epilogue<2, kT>(a, i, t0, acc, q, qp, F, Dv, xs, sv, nu, npn);
+    Norms2 o;
+#pragma unroll
+    for (int tt = 0; tt < kT; ++tt) {
+        o.nu[tt] = nu[tt];
+        o.npn[tt] = npn[tt];
+    }
+    return o;
 }
 
 template <int R, int NC, int STAGES, int MAXREG>
@@ -401,16 +425,22 @@ __global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
             npn[tt] = 0.0;
             sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
         }
-        const uint32_t it0 = it;               // item of row ja-1
-#define ITEM_OF(r) (it0 + 1u + (uint32_t)((r) - ja))
-#define STAGE_OF(r) reinterpret_cast<const double *>(smem + (size_t)(ITEM_OF(r) % STAGES) * G::kStageBytes)
-        mbar_wait(&full[it0 % STAGES], (it0 / STAGES) & 1);
-        mbar_wait(&full[(it0 + 1) % STAGES], ((it0 + 1) / STAGES) & 1);
+        // ring positions (stage index, phase parity) of rows j-1, j, j+1, advanced
+        // incrementally (no division by the stage count in the row loop)
+        int s0i = it % STAGES;
+        uint32_t ph0 = (it / STAGES) & 1;
+        int s1i = s0i + 1 == STAGES ? 0 : s0i + 1;
+        uint32_t ph1 = s1i == 0 ? ph0 ^ 1u : ph0;
+        mbar_wait(&full[s0i], ph0);
+        mbar_wait(&full[s1i], ph1);
         for (int j = ja; j < jb; ++j) {
-            const uint32_t in = ITEM_OF(j + 1);
-            mbar_wait(&full[in % STAGES], (in / STAGES) & 1);
+            const int s2i = s1i + 1 == STAGES ? 0 : s1i + 1;
+            const uint32_t ph2 = s2i == 0 ? ph1 ^ 1u : ph1;
+            mbar_wait(&full[s2i], ph2);
             if (nvalid > 0 && !a.dry) {
-                const double *r0 = STAGE_OF(j - 1), *r1 = STAGE_OF(j), *r2 = STAGE_OF(j + 1);
+                const double *r0 = reinterpret_cast<const double *>(smem + (size_t)s0i * G::kStageBytes);
+                const double *r1 = reinterpret_cast<const double *>(smem + (size_t)s1i * G::kStageBytes);
+                const double *r2 = reinterpret_cast<const double *>(smem + (size_t)s2i * G::kStageBytes);
                 const double *aux0 = reinterpret_cast<const double *>(
                                          reinterpret_cast<const unsigned char *>(r1) + G::kAuxOff) +
                                      (R * warp) * Tile2dArgs::kAux;
@@ -430,23 +460,34 @@ __global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
                             group_interior<R, false, false>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
                     }
                 } else {
+                    BArgs b;
+                    b.xn = a.xn; b.zbuf = a.zbuf; b.sendbuf = a.sendbuf; b.blk = a.blk; b.ghost = a.ghost;
+                    b.pitch = a.pitch; b.row_w = a.row_w; b.n_tl = a.n_tl; b.mode = a.mode; b.omega = a.omega;
 #pragma unroll
-                    for (int n = 0; n < R; ++n)
-                        if (n < nvalid)
-                            node_boundary(a, r0, r1, r2, aux0 + n * Tile2dArgs::kAux, j, col0 + n, p0 + n, lane, t0,
-                                          sv, nu, npn);
+                    for (int q = 0; q < 7; ++q) b.off[q] = a.off[q];
+                    for (int n = 0; n < nvalid; ++n) {
+                        const Norms2 o = node_boundary(b, r0, r1, r2, aux0 + n * Tile2dArgs::kAux, j, col0 + n,
+                                                       p0 + n, lane, t0, sv[0], sv[1]);
+#pragma unroll
+                        for (int tt = 0; tt < kT; ++tt) {
+                            nu[tt] += o.nu[tt];
+                            npn[tt] += o.npn[tt];
+                        }
+                    }
                 }
             }
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[ITEM_OF(j - 1) % STAGES]);   // row j-1 no longer needed
+            if (lane == 0) mbar_arrive(&empty[s0i]);   // row j-1 no longer needed
+            s0i = s1i;
+            ph0 = ph1;
+            s1i = s2i;
+            ph1 = ph2;
         }
         if (lane == 0) {                        // rows jb-1 and jb
-            mbar_arrive(&empty[ITEM_OF(jb - 1) % STAGES]);
-            mbar_arrive(&empty[ITEM_OF(jb) % STAGES]);
+            mbar_arrive(&empty[s0i]);
+            mbar_arrive(&empty[s1i]);
         }
-        it = ITEM_OF(jb) + 1;
-#undef ITEM_OF
-#undef STAGE_OF
+        it += (uint32_t)(jb - ja + 2);
         // per-step norm partials of this tile (fixed reduction order over warps)
 #pragma unroll
         for (int tt = 0; tt < kT; ++tt) {
@@ -490,6 +531,9 @@ TileFn tile_fn(TileCfg c) {
     BIOT_TCFG(1, 8, 6, 168)
     BIOT_TCFG(1, 12, 6, 128)
     BIOT_TCFG(1, 15, 6, 128)
+    BIOT_TCFG(1, 15, 7, 128)
+    BIOT_TCFG(1, 15, 6, 120)
+    BIOT_TCFG(1, 19, 5, 96)
     BIOT_TCFG(1, 11, 6, 168)
     BIOT_TCFG(2, 7, 6, 168)
     BIOT_TCFG(2, 11, 5, 128)

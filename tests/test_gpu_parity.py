@@ -84,11 +84,14 @@ def test_parity_config3_windows(precond):
     K, omega = 6, 0.5 if precond == 2 else 0.3
     wins = _windows(prob.n_t, K)
     g, s = _gpu_windowed(prob, K, precond, omega, wins)
-    S = oracle.OracleSystem(prob)
-    for (a, b) in wins:
-        xo = oracle_window(S, lambda st: _x0(prob, st), s, a, b, K, precond, omega)
-        xg = g.solution(a, b - a + 1)
-        assert field_errors(xg, xo, 2).max() < TOL, (a, b)
+    try:
+        S = oracle.OracleSystem(prob)
+        for (a, b) in wins:
+            xo = oracle_window(S, lambda st: _x0(prob, st), s, a, b, K, precond, omega)
+            xg = g.solution(a, b - a + 1)
+            assert field_errors(xg, xo, 2).max() < TOL, (a, b)
+    finally:
+        g.close()
 
 
 def _box_check(prob, g, s, K, precond, omega, lo, hi, wins, x0cache):
@@ -133,10 +136,12 @@ def test_parity_3d_spacetime_windows(cid):
     boxes = [((n - m, n - m, n - m), (n, n, n)),
              ((n // 2 - m // 2,) * 3, (n // 2 + m // 2,) * 3),
              ((0, 0, 0), (m, m, m))]
-    x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
-    for lo, hi in boxes:
-        _box_check(prob, g, s, K, precond, omega, np.array(lo), np.array(hi), wins, x0cache)
-    g.close()
+    try:
+        x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
+        for lo, hi in boxes:
+            _box_check(prob, g, s, K, precond, omega, np.array(lo), np.array(hi), wins, x0cache)
+    finally:
+        g.close()          # config 5 holds ~150 GB: release it even when an assertion fails
 
 
 def test_parity_config4_p1_box():
@@ -145,10 +150,12 @@ def test_parity_config4_p1_box():
     wins = _windows(prob.n_t, K, w=6)[:3]
     g, s = _gpu_windowed(prob, K, precond, omega, wins)
     n, m = prob.n, 14
-    x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
-    _box_check(prob, g, s, K, precond, omega, np.array((n - m,) * 3), np.array((n,) * 3), wins,
-               x0cache)
-    g.close()
+    try:
+        x0cache = {(a, b): _x0(prob, np.arange(max(1, a - K), b + 1)) for (a, b) in wins}
+        _box_check(prob, g, s, K, precond, omega, np.array((n - m,) * 3), np.array((n,) * 3), wins,
+                   x0cache)
+    finally:
+        g.close()
 
 
 def test_parity_ell_path_renumbered_mesh():
