@@ -199,11 +199,8 @@ def main():
     prob = config_problem(args.config)
     nccl_id = None
     if world > 1:
-        buf = torch.zeros(128, dtype=torch.uint8)
-        if rank == 0:
-            buf.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(buf, 0)
-        nccl_id = bytes(buf.numpy().tobytes())
+        from paper_2310_10430_b200.dist import broadcast_nccl_id
+        nccl_id = broadcast_nccl_id(nccl_unique_id)
     stream = torch.cuda.current_stream()
     g = BiotSolver(prob, precond=args.precond, omega=args.omega, device=local, rank=rank, world=world,
                    nccl_id=nccl_id, stream=stream.cuda_stream, history=max(1024, args.steps + args.warmup + 8))
