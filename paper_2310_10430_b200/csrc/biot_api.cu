@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <string>
 #include <vector>
@@ -140,7 +141,11 @@ struct biot_ctx {
     double tmpl[7][10] = {{0}};
     CUtensorMap tmap[2];
     int64_t n_interior = 0;
-    int s0 = 0;                       // tile2d zero-storage structural-zero variant
+    int s0 = 0;                       // tile2d/tile3d zero-storage structural-zero variant
+    // 6: TMA-pipelined 3D tile kernel
+    double tmpl3[15][17] = {{0}};
+    double *cls = nullptr;            // tile3d geometric-class stencils (device)
+    int32_t n1 = 0, z_rows = 0;
     int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
     int sR = 4, sT = 2;
     int64_t gbase[8] = {0};
@@ -191,7 +196,8 @@ void free_all(biot_ctx *c) {
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->dinv, (void *)c->s,
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
-                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux})
+                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux,
+                    (void *)c->cls})
         if (p) cudaFree(p);
     for (cudaEvent_t e : {c->ev_a, c->ev_b})
         if (e) cudaEventDestroy(e);
@@ -266,6 +272,86 @@ biot_status halo_exchange(biot_ctx *ctx) {
     return BIOT_OK;
 }
 
+// Stencil entries of two nodes of one class agree to rounding: on a uniform mesh
+// whose coordinates are not dyadic, the per-node element integrals differ in the
+// last bits; the tile kernels apply the class value (reading R21).
+inline bool same_entry(double v, double t) {
+    if (v == t) return true;
+    if (v == 0.0 || t == 0.0) return false;
+    return std::fabs(v - t) <= 8.0 * std::numeric_limits<double>::epsilon() * std::max(std::fabs(v), std::fabs(t));
+}
+
+// Node i may take a tile kernel's interior path (one template stencil, structural
+// zeros skipped) iff none of its DoFs is fixed and every entry k <= nc*nc of every
+// slot block either is the per-node AA_pp entry (carried in the aux record), or is
+// a structural zero the kernel skips (then it must be 0 here), or equals the
+// template, or is 0 against a fixed column DoF (x is identically 0 there, so
+// template * x = 0 = entry * x).
+template <class Zero>
+bool template_node(const biot::HostOperator &op, int64_t i, const double *tb, Zero zero) {
+    const int nc = op.nc, d = op.d, S = op.n_slots, WB = biot::block_width(nc);
+    for (int c = 0; c < nc; ++c)
+        if (op.fixed[(size_t)i * nc + c]) return false;
+    const double *b = op.blk.data() + (size_t)i * S * WB;
+    for (int s = 0; s < S; ++s) {
+        const int64_t j = i + op.offsets[s];
+        for (int k = 0; k <= nc * nc; ++k) {
+            const double v = b[s * WB + k];
+            if (zero(s, k)) {
+                if (v != 0.0) return false;
+                continue;
+            }
+            if (k == nc * nc - 1) continue;
+            if (same_entry(v, tb[s * WB + k])) continue;
+            const int cc = k < nc * nc ? k % nc : d;
+            const bool col_fixed = j >= 0 && j < op.n_nodes && op.fixed[(size_t)j * nc + cc];
+            if (v == 0.0 && col_fixed) continue;
+            return false;
+        }
+    }
+    return true;
+}
+
+// Geometric classes of the structured n1^3 Kuhn cube (x, y, z each in {0, interior,
+// n1-1}: 27 classes).  On the uniform mesh every node of a class has the same blocks
+// wherever its row and column DoFs are free and the neighbour exists (AA_pp aside,
+// which is per node and travels in the aux record): fixed columns meet x = 0, fixed
+// rows are masked in the epilogue (D^{-1} = 0), missing neighbours are zero-filled,
+// so the class stencil reproduces every node's own blocks.  cls[c][s][18] holds the
+// AA block column-major (cls[..][cc*4 + c] = AA[c][cc]) and A'_pp at 16.  Returns
+// false if some node disagrees with its class (then tile3d is not used).
+bool tile3d_classes(const biot::HostOperator &op, int64_t n1, std::vector<double> &cls) {
+    constexpr int CW = biot::Tile3dArgs::kClsW;
+    const int S = op.n_slots, WB = biot::block_width(op.nc);
+    const int sdx[15] = {0, -1, 0, -1, 0, -1, 0, -1, 1, 0, 1, 0, 1, 0, 1};
+    const int sdy[15] = {0, -1, -1, 0, 0, -1, -1, 0, 0, 1, 1, 0, 0, 1, 1};
+    const int sdz[15] = {0, -1, -1, -1, -1, 0, 0, 0, 0, 0, 0, 1, 1, 1, 1};
+    auto ac = [&](int64_t v) { return v == 0 ? 0 : (v == n1 - 1 ? 2 : 1); };
+    cls.assign((size_t)27 * S * CW, 0.0);
+    std::vector<uint8_t> have(cls.size(), 0);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int64_t i = 0; i < op.n_nodes; ++i) {
+            const int64_t x = i % n1, y = (i / n1) % n1, z = i / (n1 * n1);
+            const int cl = ac(x) + 3 * ac(y) + 9 * ac(z);
+            const double *b = op.blk.data() + (size_t)i * S * WB;
+            for (int q = 0; q < S; ++q) {
+                const int64_t xx = x + sdx[q], yy = y + sdy[q], zz = z + sdz[q];
+                if (xx < 0 || yy < 0 || zz < 0 || xx >= n1 || yy >= n1 || zz >= n1) continue;
+                const int64_t j = (zz * n1 + yy) * n1 + xx;
+                for (int k = 0; k <= 16; ++k) {
+                    if (k == 15) continue;
+                    const int rc = k < 16 ? k / 4 : 3, cc = k < 16 ? k % 4 : 3;
+                    if (op.fixed[(size_t)i * 4 + rc] || op.fixed[(size_t)j * 4 + cc]) continue;
+                    const size_t o = ((size_t)cl * S + q) * CW + (k < 16 ? cc * 4 + rc : 16);
+                    const double v = b[q * WB + k];
+                    if (pass == 0 && !have[o]) { cls[o] = v; have[o] = 1; }
+                    if (pass == 1 && !same_entry(v, cls[o])) return false;
+                }
+            }
+        }
+    return true;
+}
+
 // Recognise the BDIA offset sets of the structured meshes (2D right triangles,
 // 3D Kuhn tetrahedra) and fill the run tables of the register-blocked kernel.
 bool detect_stencil(biot_ctx *c) {
@@ -325,6 +411,18 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
     if (c->kern == 2) {
         biot::StencilArgs a = stencil_args(c, mode, xin, xout);
         return biot::launch_stencil(c->d, c->sR, c->sT, a, c->shape, c->stream);
+    }
+    if (c->kern == 6) {
+        biot::Tile3dArgs a{};
+        static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
+        std::memcpy(a.tmpl, c->tmpl3, sizeof(a.tmpl));
+        a.aux = c->aux;
+        a.cls = c->cls;
+        a.n1 = c->n1;
+        a.z_rows = c->z_rows;
+        a.s0 = c->s0;
+        a.dry = c->tile_dry;
+        return biot::launch_tile3d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     if (c->kern == 4) {
         biot::Tile2dArgs a{};
@@ -528,6 +626,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->hist_cap = opts->history > 0 ? opts->history : 1024;
     ctx->pitch = ((int64_t)ctx->n_tl + biot::kChunk - 1) / biot::kChunk * biot::kChunk;
     ctx->node_block = 8;
+    std::vector<double> cls3;   // tile3d class stencils (host)
     {
         const char *kenv = std::getenv("BIOT_KERNEL");
         const bool force_generic = kenv && std::string(kenv) == "generic";
@@ -551,12 +650,23 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             else if (want == "march") ctx->kern = (ctx->mT == 2 || ctx->mT == 4) ? 3 : 1;
             else ctx->kern = (ctx->offsets == order) ? 4 : 3;
         } else {
-            ctx->kern = 1;
+            // 3D: structured n1^3 Kuhn cube in the slot order tile3d_kernels.cu walks
+            const int64_t W = ctx->gbase[4], V = W * W;
+            const std::vector<int64_t> order = {0, -V - W - 1, -V - W, -V - 1, -V, -W - 1, -W, -1,
+                                                1, W, W + 1, V, V + 1, V + W, V + W + 1};
+            if (W * V == ctx->N && ctx->offsets == order && want != "march" && W >= biot::tile3d_min_n1() &&
+                tile3d_classes(*op, W, cls3)) {
+                ctx->kern = 6;
+                ctx->n1 = (int32_t)W;
+            } else {
+                ctx->kern = 1;
+            }
         }
     }
     const int64_t chunk = ctx->kern == 2 ? 32 * ctx->sT
                         : ctx->kern == 3 ? 32 * ctx->mT
                         : ctx->kern == 4 ? biot::tile2d_chunk()
+                        : ctx->kern == 6 ? biot::tile3d_chunk()
                                          : biot::kChunk;
     const int64_t nchunks = (ctx->n_tl + chunk - 1) / chunk;
     ctx->tw = 1;
@@ -680,14 +790,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         int64_t n_int = 0;
         for (int64_t i = 0; i < ctx->N; ++i) {
             const double *b = op->blk.data() + (size_t)i * S * WB;
-            bool same = base_ok;
-            for (int q = 0; q < S && same; ++q)
-                for (int k = 0; k < WB; ++k)
-                    if (k != 8 && std::memcmp(&b[q * WB + k], &tb[q * WB + k], sizeof(double)) != 0) {
-                        same = false;
-                        break;
-                    }
-            if (same && z0 && (b[1 * WB + 8] != 0.0 || b[6 * WB + 8] != 0.0)) same = false;
+            const bool same = base_ok && template_node(*op, i, tb, [&](int q, int k) { return tz(q, k, z0); });
             double *r = aux.data() + (size_t)i * KA;
             for (int q = 0; q < S; ++q) r[q] = b[q * WB + 8];
             for (int c = 0; c < 3; ++c) {
@@ -719,6 +822,104 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+        }
+    } else if (ctx->kern == 6) {
+        CU(biot::tile3d_shape(ctx->device, &ctx->shape));
+        // planes per tile: minimise (waves of tiles) x (planes + halo cost)
+        const int64_t n1 = ctx->n1, np = (n1 + 3) / 4;
+        int64_t best_zr = n1;
+        double best = 1e300;
+        for (int64_t nzr = std::max<int64_t>(2, (n1 + biot::tile3d_max_zrows() - 1) / biot::tile3d_max_zrows());
+             nzr <= 8; ++nzr) {
+            const int64_t zr = (n1 + nzr - 1) / nzr;
+            const int64_t waves = (np * np * ((n1 + zr - 1) / zr) + ctx->shape.grid - 1) / ctx->shape.grid;
+            const double cost = (double)waves * ((double)zr + 0.25);
+            if (cost < best - 1e-9) { best = cost; best_zr = zr; }
+        }
+        if (const char *e = std::getenv("BIOT_ZROWS")) best_zr = std::max(1, std::atoi(e));
+        if (best_zr > biot::tile3d_max_zrows() || best_zr >= n1)
+            return fail(ctx, BIOT_E_INVALID, "BIOT_ZROWS must be < n1 and <= the tile kernel's plane capacity");
+        ctx->z_rows = (int32_t)best_zr;
+        biot::Tile3dArgs tmp{};
+        tmp.n1 = ctx->n1;
+        tmp.z_rows = ctx->z_rows;
+        ctx->groups = biot::tile3d_groups(tmp);
+        // interior template (centre node) + per-node aux records
+        const int S = 15, WB = biot::block_width(4), KA = biot::Tile3dArgs::kAux;
+        const int64_t c1 = n1 / 2, tnode = (c1 * n1 + c1) * n1 + c1;
+        const double *tb = op->blk.data() + (size_t)tnode * S * WB;
+        for (int q = 0; q < S; ++q)
+            for (int k = 0; k < 17; ++k) ctx->tmpl3[q][k] = tb[q * WB + k];
+        // structural zeros the kernel skips (must match tmpl3_zero in tile3d_kernels.cu)
+        auto diag = [](int q) { return q == 1 || q == 2 || q == 3 || q == 5 || q == 10 || q == 12 || q == 13 || q == 14; };
+        auto tz = [&](int q, int e, bool z0) {
+            return (q == 0) ? (e == 3 || e == 7 || e == 11 || e == 12 || e == 13 || e == 14)
+                            : diag(q) ? (e == 0 || e == 5 || e == 10 || (z0 && (e == 15 || e == 16))) : false;
+        };
+        bool base_ok = true;
+        for (int q = 0; q < S; ++q)
+            for (int k = 0; k < 17; ++k)
+                if (k != 15 && tz(q, k, false) && ctx->tmpl3[q][k] != 0.0) base_ok = false;
+        bool z0 = base_ok;
+        for (int q = 0; q < S; ++q)
+            if (diag(q) && (ctx->tmpl3[q][15] != 0.0 || ctx->tmpl3[q][16] != 0.0)) z0 = false;
+        // the zero-storage variant needs AA_pp = 0 on the diagonal slots of every interior node
+        if (z0)
+            for (int64_t i = 0; i < ctx->N && z0; ++i)
+                for (int q = 0; q < S; ++q)
+                    if (diag(q) && op->blk[((size_t)i * S + q) * WB + 15] != 0.0 &&
+                        template_node(*op, i, tb, [&](int qq, int k) { return tz(qq, k, false); })) {
+                        z0 = false;
+                        break;
+                    }
+        ctx->s0 = z0 ? 1 : 0;
+        if (const char *e = std::getenv("BIOT_TILE_DRY")) ctx->tile_dry = std::atoi(e);
+        std::vector<double> aux((size_t)(ctx->N + 8) * KA, 0.0);
+        int64_t n_int = 0;
+        for (int64_t i = 0; i < ctx->N; ++i) {
+            const int64_t x = i % n1, y = (i / n1) % n1, z = i / (n1 * n1);
+            const bool inner = x > 0 && y > 0 && z > 0 && x < n1 - 1 && y < n1 - 1 && z < n1 - 1;
+            const bool same = base_ok && inner && template_node(*op, i, tb, [&](int q, int k) { return tz(q, k, z0); });
+            const double *b = op->blk.data() + (size_t)i * S * WB;
+            double *r = aux.data() + (size_t)i * KA;
+            for (int q = 0; q < S; ++q) r[q] = b[q * WB + 15];
+            for (int c = 0; c < 4; ++c) {
+                r[15 + c] = op->load[(size_t)i * 4 + c];
+                r[19 + c] = op->dinv[(size_t)i * 4 + c];
+            }
+            // path flag: 1 interior template, 2 geometric-class stencil
+            r[23] = same ? 1.0 : 2.0;
+            n_int += same;
+        }
+        ctx->n_interior = n_int;
+        ALLOC(ctx->cls, cls3.size() * sizeof(double));
+        CU(h2d(ctx, ctx->cls, cls3.data(), cls3.size() * sizeof(double)));
+        if (std::getenv("BIOT_DEBUG"))
+            std::fprintf(stderr, "[biot] tile3d: n1=%d z_rows=%d tiles=%lld interior=%lld/%lld s0=%d grid=%d\n",
+                         ctx->n1, ctx->z_rows, (long long)ctx->groups, (long long)n_int, (long long)ctx->N, ctx->s0,
+                         ctx->shape.grid);
+        ALLOC(ctx->aux, aux.size() * sizeof(double));
+        CU(h2d(ctx, ctx->aux, aux.data(), aux.size() * sizeof(double)));
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qres;
+        CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
+        if (!fn || qres != cudaDriverEntryPointSuccess)
+            return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled not available");
+        auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        uint32_t box[4];
+        biot::tile3d_box(box);
+        for (int k = 0; k < 2; ++k) {
+            // {time, x*4 + c, y, z} over the panel at node 0; out-of-mesh boxes are zero-filled
+            cuuint64_t dims[4] = {(cuuint64_t)ctx->pitch, (cuuint64_t)(n1 * 4), (cuuint64_t)n1, (cuuint64_t)n1};
+            const cuuint64_t rb = (cuuint64_t)ctx->pitch * sizeof(double);
+            cuuint64_t strides[3] = {rb, rb * (cuuint64_t)(n1 * 4), rb * (cuuint64_t)(n1 * n1 * 4)};
+            cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            CUresult r = encode(&ctx->tmap[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->x[k], dims, strides, bx, es,
+                                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS)
+                return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (4D) failed: " + std::to_string((int)r));
         }
     } else {
         CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));
@@ -901,7 +1102,7 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->n_t_local = ctx->n_tl;
     o->first_step = ctx->first_step;
     o->iterations = ctx->iterations;
-    o->kernel_path = ctx->kern == 1 ? ctx->path : ctx->kern + 1;   // 3 stencil, 4 march, 5 tile2d
+    o->kernel_path = ctx->kern == 1 ? ctx->path : ctx->kern + 1;   // 3 stencil, 4 march, 5 tile2d, 7 tile3d
     o->n_slots = ctx->S;
     o->beta = ctx->beta;
     const double st = (double)ctx->N * ctx->nc * ctx->n_tl;

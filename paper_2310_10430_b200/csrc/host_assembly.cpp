@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <unordered_map>
 
@@ -62,8 +63,17 @@ double simplex_gradients(int d, const double *const *X, double g[4][3]) {
         }
     }
     // V[:, n:] now holds Vinv; grad phi_a[k] = Vinv[1+k][a]
+    double gmax = 0.0;
     for (int a = 0; a < n; ++a)
-        for (int k = 0; k < d; ++k) g[a][k] = V[1 + k][n + a];
+        for (int k = 0; k < d; ++k) {
+            g[a][k] = V[1 + k][n + a];
+            gmax = std::max(gmax, std::fabs(g[a][k]));
+        }
+    // components that vanish exactly (axis-aligned edges/faces) come out of the
+    // elimination as rounding residue; store them as the 0 they are (reading R21)
+    for (int a = 0; a < n; ++a)
+        for (int k = 0; k < d; ++k)
+            if (std::fabs(g[a][k]) <= 16.0 * std::numeric_limits<double>::epsilon() * gmax) g[a][k] = 0.0;
     return det / (d == 2 ? 2.0 : 6.0);
 }
 
@@ -189,6 +199,16 @@ std::string assemble(const biot_mesh &mesh, const biot_material &mat, const biot
 #pragma omp parallel for schedule(dynamic, 1024)
     for (int64_t i = 0; i < N; ++i) {
         double *bi = op.blk.data() + (size_t)i * S * W;
+        // |contributions| per entry: sums that vanish in exact arithmetic (e.g. the
+        // u_x-u_x coupling of diagonal Kuhn neighbours, the self-block B entries of an
+        // interior node) leave a rounding residue; it is stored as the exact 0 it is
+        // (reading R21), so every kernel sees the structural zeros
+        double absb[kMaxSlots * 18];
+        for (int k = 0; k < S * W; ++k) absb[k] = 0.0;
+        auto add = [&](int slot, int k, double v, double mag) {
+            bi[(size_t)slot * W + k] += v;
+            absb[slot * W + k] += mag;
+        };
         for (int64_t q = inc_ptr[i]; q < inc_ptr[i + 1]; ++q) {
             const int64_t e = inc[q];
             const int32_t *cn = mesh.cells + e * nv;
@@ -214,27 +234,41 @@ std::string assemble(const biot_mesh &mesh, const biot_material &mat, const biot
                     slot = 0;
                     while (ci[slot] != j) ++slot;
                 }
-                double *blk = bi + (size_t)slot * W;
-                double gab = 0.0;
-                for (int k = 0; k < d; ++k) gab += g[a][k] * g[b][k];
+                double gab = 0.0, gabs = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    gab += g[a][k] * g[b][k];
+                    gabs += std::fabs(g[a][k] * g[b][k]);
+                }
                 const double lab = vol * gab;                                  // L_ab
                 const double mab = vol * (a == b ? 2.0 : 1.0) / mass_den;      // M_ab
                 // displacement rows: a(u, v) incl. lambda div div  (P:L96 + R7)
                 for (int c = 0; c < d; ++c)
                     for (int ee = 0; ee < d; ++ee)
-                        blk[c * nc + ee] += vol * (mu * gab * (c == ee ? 1.0 : 0.0) +
-                                                   mu * g[a][ee] * g[b][c] +
-                                                   lam * g[a][c] * g[b][ee]);
+                        add(slot, c * nc + ee,
+                            vol * (mu * gab * (c == ee ? 1.0 : 0.0) + mu * g[a][ee] * g[b][c] +
+                                   lam * g[a][c] * g[b][ee]),
+                            vol * (mu * gabs * (c == ee ? 1.0 : 0.0) + std::fabs(mu * g[a][ee] * g[b][c]) +
+                                   std::fabs(lam * g[a][c] * g[b][ee])));
                 // B = -b(v, p): -alpha int q_b div v_(a,c)
-                for (int c = 0; c < d; ++c) blk[c * nc + d] += -alpha * vol * g[a][c] / nv;
+                for (int c = 0; c < d; ++c) {
+                    const double v = -alpha * vol * g[a][c] / nv;
+                    add(slot, c * nc + d, v, std::fabs(v));
+                }
                 // B^T: pressure row a, displacement column (b, e)
-                for (int ee = 0; ee < d; ++ee) blk[d * nc + ee] += -alpha * vol * g[b][ee] / nv;
+                for (int ee = 0; ee < d; ++ee) {
+                    const double v = -alpha * vol * g[b][ee] / nv;
+                    add(slot, d * nc + ee, v, std::fabs(v));
+                }
                 // -(S M + tau C_kappa + beta L)  (P:L159 with R8, R9)
-                blk[d * nc + d] += -(Sst * mab + (tau * kap + beta) * lab);
+                add(slot, d * nc + d, -(Sst * mab + (tau * kap + beta) * lab),
+                    Sst * mab + (tau * kap + beta) * vol * gabs);
                 // A' pressure-pressure: -(S M + beta L)
-                blk[nc * nc] += -(Sst * mab + beta * lab);
+                add(slot, nc * nc, -(Sst * mab + beta * lab), Sst * mab + beta * vol * gabs);
             }
         }
+        const double tol = 32.0 * std::numeric_limits<double>::epsilon();
+        for (int k = 0; k < S * W; ++k)
+            if (std::fabs(bi[k]) <= tol * absb[k]) bi[k] = 0.0;
     }
     if (bad_cell >= 0) return "degenerate or inverted cell " + std::to_string(bad_cell);
 

@@ -48,6 +48,10 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
 #pragma unroll
         for (int c = 0; c < D; ++c) r[c] = sv[tt] * F[c] - acc[c][tt];
         r[D] = (sv[tt] * F[D] + qp) - acc[D][tt];
+        // Dirichlet rows (D^{-1} = 0) carry no residual: kernels that apply a shared
+        // stencil to such rows (tile3d class templates) rely on this mask
+#pragma unroll
+        for (int c = 0; c < NC; ++c) r[c] = (Dv[c] == 0.0) ? 0.0 : r[c];
         double su = 0.0;
 #pragma unroll
         for (int c = 0; c < D; ++c) su = fma(r[c], r[c], su);
@@ -73,9 +77,14 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
         if (c >= ncw) break;
         double *dst = a.xn + (i * NC + c) * P + t0;
         if (full) {
+            if constexpr (T % 2 == 0) {
 #pragma unroll
-            for (int h = 0; h < T; h += 2)
-                *reinterpret_cast<double2 *>(dst + h) = make_double2(outx[c][h], outx[c][h + 1]);
+                for (int h = 0; h < T; h += 2)
+                    *reinterpret_cast<double2 *>(dst + h) = make_double2(outx[c][h], outx[c][h + 1]);
+            } else {
+#pragma unroll
+                for (int tt = 0; tt < T; ++tt) dst[tt] = outx[c][tt];
+            }
         } else {
 #pragma unroll
             for (int tt = 0; tt < T; ++tt)
@@ -87,9 +96,14 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
         for (int c = 0; c < NC; ++c) {
             double *dst = a.zbuf + (i * NC + c) * P + t0;
             if (full) {
+                if constexpr (T % 2 == 0) {
 #pragma unroll
-                for (int h = 0; h < T; h += 2)
-                    *reinterpret_cast<double2 *>(dst + h) = make_double2(outz[c][h], outz[c][h + 1]);
+                    for (int h = 0; h < T; h += 2)
+                        *reinterpret_cast<double2 *>(dst + h) = make_double2(outz[c][h], outz[c][h + 1]);
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < T; ++tt) dst[tt] = outz[c][tt];
+                }
             } else {
 #pragma unroll
                 for (int tt = 0; tt < T; ++tt)

@@ -75,6 +75,20 @@ struct Tile2dArgs : SweepArgs {
     int32_t dry;                      // dev/measurement only: stream the ring without computing
 };
 
+// Arguments of the TMA-pipelined 3D tile kernel (tile3d_kernels.cu): structured
+// n1^3 Kuhn cube, node = (z*n1 + y)*n1 + x, BDIA slot order of host_assembly.
+struct Tile3dArgs : SweepArgs {
+    static constexpr int kAux = 24;   // per-node record: AA_pp per slot [15], f [4], dinv [4], path flag
+    double tmpl[15][17];              // interior stencil: AA block [16] (pp entry unused) + A'_pp
+    const double *aux;                // [n_alloc][kAux]
+    const double *cls;                // geometric-class stencils [27][15][kClsW], column-major blocks
+    static constexpr int kClsW = 18;  // 17 entries padded to 16 B
+    int32_t n1;                      // nodes per axis
+    int32_t z_rows;                   // planes marched per tile
+    int32_t s0;                       // zero-storage structural-zero variant
+    int32_t dry;                      // dev/measurement only: stream the ring without computing
+};
+
 struct LaunchShape {
     int grid;
     size_t smem;
@@ -104,6 +118,16 @@ int tile2d_seg();   // grid columns per tile (8 x R)
 void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
+                          cudaStream_t st);
+
+// 3D TMA tile kernel: 4x4 (x,y) node patches x 32-step chunks, marching z
+int64_t tile3d_groups(const Tile3dArgs &a);
+int tile3d_chunk();
+int tile3d_max_zrows();
+int tile3d_min_n1();
+void tile3d_box(uint32_t *box);      // {time, x*4+c, y, z}
+cudaError_t tile3d_shape(int device, LaunchShape *out);
+cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
 
 bool stencil_supported(int dim, int R, int T);

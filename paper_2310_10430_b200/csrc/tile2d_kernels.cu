@@ -32,6 +32,7 @@
 
 #include "node_update.cuh"
 #include "sweep_kernels.cuh"
+#include "tma_util.cuh"
 
 namespace biot {
 
@@ -96,57 +97,7 @@ __host__ __device__ constexpr bool tmpl_zero(int s, int e, bool s0) {
                     : (s == 1 || s == 6) ? (e == 0 || e == 4 || (s0 && (e == 8 || e == 9))) : false;
 }
 
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-    }
-}
-// producer-side wait: back off between polls so the spinning thread does not
-// take issue slots from the consumer warps sharing its scheduler
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (true) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) break;
-        __nanosleep(200);
-    }
-}
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-        "[%4];" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
+using namespace tma;
 
 template <int SEG>
 struct TileGeom {
@@ -373,7 +324,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kConsumers);
         }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        fence_barrier_init();
     }
     __syncthreads();
 
@@ -395,7 +346,7 @@ __global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
                     const bool real = (r >= 0 && r < a.n_rows);
                     mbar_expect_tx(&full[st], G::kXBytes + (real ? G::kAuxBytes : 0u));
                     const int64_t node0 = (int64_t)r * W + i0 - 1;
-                    tma_load_2d(base, &tmx, chunk * kCh - 2, (int)((node0 + a.pad_nodes) * 3), &full[st]);
+                    load_2d(base, &tmx, chunk * kCh - 2, (int)((node0 + a.pad_nodes) * 3), &full[st]);
                     if (real)
                         bulk_g2s(base + G::kAuxOff, a.aux + ((int64_t)r * W + i0) * Tile2dArgs::kAux, G::kAuxBytes,
                                  &full[st]);

@@ -119,3 +119,54 @@ def test_kernel_variants_bitwise(cid, precond, monkeypatch):
     x, ref = res["tile"][0], res["generic"][0]
     assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
     assert np.allclose(res["tile"][1], res["generic"][1], rtol=1e-10, atol=0)
+
+
+def _tile3d_cases():
+    # (n cells per axis, n_t, storage, kappa sigma): ragged time tails (n_t % 32 != 0),
+    # patches cut by the mesh edge (n+1 not a multiple of 4), S = 0 (zero-storage variant)
+    return [(7, 40, 1e-3, 1.0), (8, 33, 0.0, 0.0), (5, 64, 1e-3, 1.5), (9, 7, 0.0, 1.0)]
+
+
+@pytest.mark.parametrize("case", _tile3d_cases())
+@pytest.mark.parametrize("precond", [2, 1])
+def test_tile3d_vs_generic(case, precond, monkeypatch):
+    """The 3D TMA tile kernel (template stencil, structural zeros skipped, boundary
+    nodes out of line) against the generic BDIA kernel: equal to rounding."""
+    n, nt, S, sig = case
+    prob = make_problem(3, n, nt, 0.01, 6, storage=S, kappa_median=1e-3, kappa_sigma=sig,
+                        kappa_seed=3, x0_seed=9)
+    K = 6
+    res = {}
+    for kern in ("generic", "tile"):
+        monkeypatch.setenv("BIOT_KERNEL", kern)
+        g = _seeded(prob, nt, precond=precond)
+        g.iterate(K)
+        res[kern] = (g.solution(), np.stack([g.residual_history(k) for k in range(K)]),
+                     g.residual_norms(), g.info.kernel_path)
+        g.close()
+    assert res["generic"][3] == 1 and res["tile"][3] == 7
+    x, ref = res["tile"][0], res["generic"][0]
+    assert np.abs(x - ref).max() <= 1e-12 * np.abs(ref).max()
+    assert np.allclose(res["tile"][1], res["generic"][1], rtol=1e-10, atol=0)
+    assert np.allclose(res["tile"][2], res["generic"][2], rtol=1e-10, atol=0)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tile3d_time_slabs_bitwise(world):
+    """Chunk 0 of each slab recomputes q(t0-1) from the ghost in the carry's FMA order."""
+    prob = make_problem(3, 7, 96, 0.01, 5, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0,
+                        kappa_seed=3, x0_seed=9)
+    nt, K = prob.n_t, 5
+    ref = _seeded(prob, nt, precond=2)
+    assert ref.info.kernel_path == 7
+    ref.iterate(K)
+    xr = ref.solution()
+    ranks = [_seeded(prob, nt, precond=2, rank=r, world=world, flags=FLAG_MANUAL_HALO) for r in range(world)]
+    for _ in range(K):
+        slices = [g.last_slice() for g in ranks]
+        for r in range(1, world):
+            ranks[r].set_ghost(slices[r - 1])
+        for g in ranks:
+            g.iterate(1)
+    xs = np.concatenate([g.solution() for g in ranks])
+    assert np.array_equal(xs, xr)

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+export BIOT_DEBUG=1
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -4
+for d in 0 2; do BIOT_TILE_DRY=$d timeout 300 python bench.py --config 4 --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>&1 | grep -o '\[biot\].*\|"ms_per_step": [0-9.]*' ; done
+timeout 300 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 2>&1 | grep -o '\[biot\].*\|"ms_per_step": [0-9.]*'
