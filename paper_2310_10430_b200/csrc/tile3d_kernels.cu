@@ -46,8 +46,12 @@ using namespace tma;
 constexpr int kB = 4;                      // patch edge (nodes)
 constexpr int kSE = kB + 2;                // staged edge incl. halo
 constexpr int kTc = 32;                    // time steps per chunk (one per lane)
-constexpr int kConsumers = kB * kB / 2;    // warps; two x-adjacent nodes each
-constexpr int kStages = 5;
+// R = x-adjacent nodes per consumer warp (1 or 2); consumers = 16 / R.  R = 1 (16
+// warps, 4 per scheduler) measured faster than R = 2 (8 warps, more operand reuse):
+// config 4 5.23 vs 5.29 ms; R = 4 (4 warps) 8.5 ms, a 6x4 patch with R = 2 (12 warps,
+// 3 stages) 5.93 ms.  The kernel is latency-bound at IPC ~2.5.
+template <int R> constexpr int kConsumersOf = kB * kB / R;
+template <int R> constexpr int kStagesOf = R == 2 ? 5 : 4;
 constexpr int kMaxZ = 72;                  // planes per tile (q carry capacity)
 constexpr int kCW = Tile3dArgs::kClsW;     // doubles per class-stencil slot
 constexpr int kClsD = 272;                 // doubles per class stencil in shared memory (15*18 padded)
@@ -57,9 +61,9 @@ constexpr uint32_t kXBytes = kSE * kRowD * 8;                                  /
 constexpr uint32_t kAuxRec = Tile3dArgs::kAux;                                 // doubles per record
 constexpr uint32_t kAuxBytes = kB * kB * kAuxRec * 8;                          // 3072
 constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;      // 39936
-constexpr uint32_t kClsOff = kStages * kStageBytes;
-constexpr uint32_t kCarryOff = kClsOff + kClsLocal * kClsD * 8;
-constexpr uint32_t kSmemBytes = kCarryOff + kMaxZ * kB * kB * 8;
+template <int R> constexpr uint32_t kClsOffOf = kStagesOf<R> * kStageBytes;
+template <int R> constexpr uint32_t kCarryOffOf = kClsOffOf<R> + kClsLocal * kClsD * 8;
+template <int R> constexpr uint32_t kSmemBytesOf = kCarryOffOf<R> + kMaxZ * kB * kB * 8;
 
 // (dx, dy, dz) of the 15 BDIA slots in storage order (offsets sorted ascending,
 // self first): 0, -V-W-1, -V-W, -V-1, -V, -W-1, -W, -1, 1, W, W+1, V, V+1, V+W, V+W+1
@@ -273,22 +277,43 @@ struct Geo3 {
 
 __device__ __forceinline__ int axis_class(int v, int n1) { return v == 0 ? 0 : (v == n1 - 1 ? 2 : 1); }
 
-// Node kinds of a warp's pair in one plane: 0 nothing, 1 interior template pair,
-// 2 class pair (NN = 2), 3 single class node (NN = 1: B outside the mesh)
-__device__ __forceinline__ int pair_kind(bool vA, bool vB, const double *aux) {
+// Kind of a warp's nodes in one plane: 0 nothing, 1 interior template, 2 class stencils
+__device__ __forceinline__ int group_kind(bool vA, bool vB, const double *aux) {
     if (!vA) return 0;
-    if (!vB) return 3;
-    return (aux[23] == 1.0 && aux[kAuxRec + 23] == 1.0) ? 1 : 2;
+    return (aux[23] == 1.0 && (!vB || aux[kAuxRec + 23] == 1.0)) ? 1 : 2;
 }
 
-template <bool S0>
-__global__ void __maxnreg__(168)
+template <int NN, bool S0>
+__device__ __forceinline__ void finish_any(int kind, const Tile3dArgs &a, const double *po, const double *pu,
+                                           const double *aux, int64_t iA, int sx, int sy, int lane, int t,
+                                           bool ghost, double *carry, double sv, const double *TA,
+                                           const double *TB, double (&acc)[2][4], double (&q)[2], double &nu,
+                                           double &npn) {
+    if (kind == 1)
+        finish<NN, false, S0>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
+    else if (a.dry != 2)
+        finish<NN, true, S0>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
+}
+
+template <int NN, bool S0>
+__device__ __forceinline__ void start_any(int kind, const Tile3dArgs &a, const double *pd, const double *pm,
+                                          const double *aux, int sx, int sy, int lane, const double *TA,
+                                          const double *TB, double (&acc)[2][4], double (&q)[2]) {
+    if (kind == 1)
+        start<NN, false, S0>(a, pd, pm, aux, sx, sy, lane, TA, TB, acc, q);
+    else if (a.dry != 2)
+        start<NN, true, S0>(a, pd, pm, aux, sx, sy, lane, TA, TB, acc, q);
+}
+
+template <bool S0, int R>
+__global__ void __maxnreg__(R == 2 ? 168 : 96)
     tile3d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile3dArgs a) {
+    constexpr int kConsumers = kConsumersOf<R>, kStages = kStagesOf<R>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     __shared__ double red[kConsumers][kTc][2];
-    double *cls_sm = reinterpret_cast<double *>(smem + kClsOff);      // [kClsLocal][kClsD]
-    double *qcarry = reinterpret_cast<double *>(smem + kCarryOff);    // [kMaxZ][16]
+    double *cls_sm = reinterpret_cast<double *>(smem + kClsOffOf<R>);      // [kClsLocal][kClsD]
+    double *qcarry = reinterpret_cast<double *>(smem + kCarryOffOf<R>);    // [kMaxZ][16]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Geo3 g(a);
@@ -330,7 +355,7 @@ __global__ void __maxnreg__(168)
     }
 
     // ------------------------------- consumers ------------------------------
-    const int px = (warp & 1) * 2, py = warp >> 1;
+    const int px = (warp % (kB / R)) * R, py = warp / (kB / R);
     const int sx = px + 1, sy = py + 1;
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
@@ -346,7 +371,7 @@ __global__ void __maxnreg__(168)
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
         const int xA = x0 + px, y = y0 + py;
-        const bool vA = xA < g.n1 && y < g.n1, vB = xA + 1 < g.n1 && y < g.n1;
+        const bool vA = xA < g.n1 && y < g.n1, vB = R == 2 && xA + 1 < g.n1 && y < g.n1;
         const int ccxA = axis_class(xA, g.n1), ccxB = axis_class(xA + 1, g.n1), ccy = axis_class(y, g.n1);
         for (int chunk = 0; chunk < g.nchunks; ++chunk) {
             const int t = chunk * kTc + lane;
@@ -372,35 +397,30 @@ __global__ void __maxnreg__(168)
                                             (py * kB + px) * kAuxRec;
                         const int64_t iA = ((int64_t)(m - 1) * g.n1 + y) * g.n1 + xA;
                         double *carry = qcarry + (m - 1 - za) * (kB * kB) + py * kB + px;
-                        if (kindP == 1) {
-                            finish<2, false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp, TBp,
-                                                 acc, q, nu, npn);
-                        } else if (a.dry != 2) {
-                            if (kindP == 2)
-                                finish<2, true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
-                                                    TBp, acc, q, nu, npn);
-                            else
-                                finish<1, true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
-                                                    TBp, acc, q, nu, npn);
-                        }
+                        if (vB)
+                            finish_any<2, S0>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
+                                              TBp, acc, q, nu, npn);
+                        else
+                            finish_any<1, S0>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
+                                              TBp, acc, q, nu, npn);
                     }
                     kindP = 0;
                     if (m < zb) {                // start plane m
                         const double *aux = reinterpret_cast<const double *>(
                                                 reinterpret_cast<const unsigned char *>(pm) + kXBytes) +
                                             (py * kB + px) * kAuxRec;
-                        kindP = pair_kind(vA, vB, aux);
-                        if (kindP >= 2) {
+                        kindP = group_kind(vA, vB, aux);
+                        if (kindP == 2) {
                             const int base = (axis_class(m, g.n1) != 1) * 4 + (ccy - cyl) * 2;
                             TAp = cls_sm + (base + ccxA - cxl) * kClsD;
                             TBp = cls_sm + (base + (vB ? ccxB : ccxA) - cxl) * kClsD;
                         }
-                        if (kindP == 1)
-                            start<2, false, S0>(a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
-                        else if (kindP == 2 && a.dry != 2)
-                            start<2, true, S0>(a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
-                        else if (kindP == 3 && a.dry != 2)
-                            start<1, true, S0>(a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
+                        if (kindP != 0) {
+                            if (vB)
+                                start_any<2, S0>(kindP, a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
+                            else
+                                start_any<1, S0>(kindP, a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
+                        }
                     }
                 }
                 __syncwarp();
@@ -448,22 +468,35 @@ void tile3d_box(uint32_t *box) {
     box[3] = 1;
 }
 
+int tile3d_r() {
+    static const int r = [] {
+        const char *e = std::getenv("BIOT_TILE3D_R");   // dev knob: nodes per consumer warp
+        return (e && std::atoi(e) == 2) ? 2 : 1;
+    }();
+    return r;
+}
+
+template <int R>
+cudaError_t shape_r(int sms, LaunchShape *out) {
+    for (auto fn : {tile3d_kernel<false, R>, tile3d_kernel<true, R>}) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesOf<R>);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile3d_kernel<false, R>,
+                                                                  (kConsumersOf<R> + 1) * 32, kSmemBytesOf<R>);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    out->grid = sms * per_sm;
+    out->smem = kSmemBytesOf<R>;
+    return cudaSuccess;
+}
+
 cudaError_t tile3d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    for (auto fn : {tile3d_kernel<false>, tile3d_kernel<true>}) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile3d_kernel<false>, (kConsumers + 1) * 32,
-                                                      kSmemBytes);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    out->grid = sms * per_sm;
-    out->smem = kSmemBytes;
-    return cudaSuccess;
+    return tile3d_r() == 1 ? shape_r<1>(sms, out) : shape_r<2>(sms, out);
 }
 
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
@@ -471,10 +504,15 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
     if (a.z_rows < 1 || a.z_rows > kMaxZ || a.z_rows >= a.n1 || a.n1 < kB + 1) return cudaErrorInvalidValue;
     const int64_t tiles = tile3d_groups(a);
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
-    if (a.s0)
-        tile3d_kernel<true><<<grid, (kConsumers + 1) * 32, sh.smem, st>>>(tmx, a);
-    else
-        tile3d_kernel<false><<<grid, (kConsumers + 1) * 32, sh.smem, st>>>(tmx, a);
+    const int R = tile3d_r();
+    const int threads = (kB * kB / R + 1) * 32;
+    if (R == 1) {
+        if (a.s0) tile3d_kernel<true, 1><<<grid, threads, sh.smem, st>>>(tmx, a);
+        else tile3d_kernel<false, 1><<<grid, threads, sh.smem, st>>>(tmx, a);
+    } else {
+        if (a.s0) tile3d_kernel<true, 2><<<grid, threads, sh.smem, st>>>(tmx, a);
+        else tile3d_kernel<false, 2><<<grid, threads, sh.smem, st>>>(tmx, a);
+    }
     return cudaGetLastError();
 }
 
