@@ -119,6 +119,7 @@ struct biot_ctx {
     uint8_t *fixed = nullptr;
     double *sendbuf = nullptr;
     double *partial = nullptr;
+    double *fin_scratch = nullptr;    // two-stage norm reduction
     double *hist = nullptr, *norms = nullptr;
     int *nonfinite = nullptr;
     double *staging = nullptr;
@@ -197,7 +198,7 @@ void free_all(biot_ctx *c) {
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->dinv, (void *)c->s,
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux,
-                    (void *)c->cls})
+                    (void *)c->cls, (void *)c->fin_scratch})
         if (p) cudaFree(p);
     for (cudaEvent_t e : {c->ev_a, c->ev_b})
         if (e) cudaEventDestroy(e);
@@ -352,6 +353,40 @@ bool tile3d_classes(const biot::HostOperator &op, int64_t n1, std::vector<double
     return true;
 }
 
+// Geometric classes of the structured 2D grid (column and row each in {0, interior,
+// last}: 9 classes), as tile3d_classes: cls[c][s][10] holds the AA block
+// column-major (cls[..][cc*3 + c] = AA[c][cc]) and A'_pp at 9.
+bool tile2d_classes(const biot::HostOperator &op, int64_t W, int64_t nrows, std::vector<double> &cls) {
+    constexpr int CW = biot::Tile2dArgs::kClsW;
+    const int S = op.n_slots, WB = biot::block_width(op.nc);
+    const int sdc[7] = {0, -1, 0, -1, 1, 0, 1};
+    const int sdr[7] = {0, -1, -1, 0, 0, 1, 1};
+    auto ac = [](int64_t v, int64_t n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); };
+    cls.assign((size_t)9 * S * CW, 0.0);
+    std::vector<uint8_t> have(cls.size(), 0);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int64_t i = 0; i < op.n_nodes; ++i) {
+            const int64_t x = i % W, y = i / W;
+            const int cl = ac(x, W) + 3 * ac(y, nrows);
+            const double *b = op.blk.data() + (size_t)i * S * WB;
+            for (int q = 0; q < S; ++q) {
+                const int64_t xx = x + sdc[q], yy = y + sdr[q];
+                if (xx < 0 || yy < 0 || xx >= W || yy >= nrows) continue;
+                const int64_t j = yy * W + xx;
+                for (int k = 0; k <= 9; ++k) {
+                    if (k == 8) continue;
+                    const int rc = k < 9 ? k / 3 : 2, cc = k < 9 ? k % 3 : 2;
+                    if (op.fixed[(size_t)i * 3 + rc] || op.fixed[(size_t)j * 3 + cc]) continue;
+                    const size_t o = ((size_t)cl * S + q) * CW + (k < 9 ? cc * 3 + rc : 9);
+                    const double v = b[q * WB + k];
+                    if (pass == 0 && !have[o]) { cls[o] = v; have[o] = 1; }
+                    if (pass == 1 && !same_entry(v, cls[o])) return false;
+                }
+            }
+        }
+    return true;
+}
+
 // Recognise the BDIA offset sets of the structured meshes (2D right triangles,
 // 3D Kuhn tetrahedra) and fill the run tables of the register-blocked kernel.
 bool detect_stencil(biot_ctx *c) {
@@ -429,6 +464,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
         static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
         std::memcpy(a.tmpl, c->tmpl, sizeof(a.tmpl));
         a.aux = c->aux;
+        a.cls = c->cls;
         a.pad_nodes = c->pad;
         a.s0 = c->s0;
         a.dry = c->tile_dry;
@@ -470,7 +506,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     }
     double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
     CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
-                             ctx->stream));
+                             ctx->fin_scratch, ctx->stream));
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
     return BIOT_OK;
@@ -626,7 +662,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->hist_cap = opts->history > 0 ? opts->history : 1024;
     ctx->pitch = ((int64_t)ctx->n_tl + biot::kChunk - 1) / biot::kChunk * biot::kChunk;
     ctx->node_block = 8;
-    std::vector<double> cls3;   // tile3d class stencils (host)
+    std::vector<double> cls3, cls2;   // tile3d / tile2d class stencils (host)
     {
         const char *kenv = std::getenv("BIOT_KERNEL");
         const bool force_generic = kenv && std::string(kenv) == "generic";
@@ -648,7 +684,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             const bool grid_ok = ctx->row_w * ctx->n_rows == ctx->N;
             if (!grid_ok) ctx->kern = 1;
             else if (want == "march") ctx->kern = (ctx->mT == 2 || ctx->mT == 4) ? 3 : 1;
-            else ctx->kern = (ctx->offsets == order) ? 4 : 3;
+            else ctx->kern = (ctx->offsets == order && tile2d_classes(*op, ctx->row_w, ctx->n_rows, cls2)) ? 4 : 3;
         } else {
             // 3D: structured n1^3 Kuhn cube in the slot order tile3d_kernels.cu walks
             const int64_t W = ctx->gbase[4], V = W * W;
@@ -753,11 +789,18 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ctx->groups = biot::march_groups(tmp);
     } else if (ctx->kern == 4) {
         CU(biot::tile2d_shape(ctx->device, &ctx->shape));
+        // rows per tile: minimise (waves of tiles) x (rows + halo cost)
         const int64_t n_seg = (ctx->row_w + biot::tile2d_seg() - 1) / biot::tile2d_seg();
-        int64_t rpt = ctx->n_rows;
-        while (rpt > 16 && n_seg * ((ctx->n_rows + rpt - 1) / rpt) * nchunks < 8 * (int64_t)ctx->shape.grid)
-            rpt = (rpt + 1) / 2;
+        int64_t rpt = 1;
+        double best = 1e300;
+        for (int64_t rr = 1; rr <= biot::tile2d_max_rows(); ++rr) {
+            const int64_t waves = (n_seg * ((ctx->n_rows + rr - 1) / rr) + ctx->shape.grid - 1) / ctx->shape.grid;
+            const double cost = (double)waves * ((double)std::min<int64_t>(rr, ctx->n_rows) + 0.25);
+            if (cost < best - 1e-9) { best = cost; rpt = rr; }
+        }
         if (const char *e = std::getenv("BIOT_MARCH_ROWS")) rpt = std::max(1, std::atoi(e));
+        if (rpt > biot::tile2d_max_rows())
+            return fail(ctx, BIOT_E_INVALID, "BIOT_MARCH_ROWS exceeds the tile kernel's row capacity");
         ctx->rows_per_tile = (int32_t)rpt;
         biot::Tile2dArgs tmp{};
         tmp.row_w = ctx->row_w;
@@ -782,7 +825,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const bool z0 = base_ok && ctx->tmpl[1][9] == 0.0 && ctx->tmpl[6][9] == 0.0 &&
                         ctx->tmpl[1][8] == 0.0 && ctx->tmpl[6][8] == 0.0;
         ctx->s0 = z0 ? 1 : 0;
-        if (const char *e = std::getenv("BIOT_TILE_DRY")) ctx->tile_dry = std::atoi(e) != 0;
+        if (const char *e = std::getenv("BIOT_TILE_DRY")) ctx->tile_dry = std::atoi(e);
+        ALLOC(ctx->cls, cls2.size() * sizeof(double));
+        CU(h2d(ctx, ctx->cls, cls2.data(), cls2.size() * sizeof(double)));
         // records for every node a tile's bulk copy can touch: the last row's segment may
         // extend up to one segment past node N-1
         const int64_t aux_nodes = ctx->N + 2 * biot::tile2d_seg() + 8;
@@ -797,10 +842,14 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                 r[7 + c] = op->load[(size_t)i * 3 + c];
                 r[10 + c] = op->dinv[(size_t)i * 3 + c];
             }
-            r[13] = same ? 1.0 : 0.0;
+            r[13] = same ? 1.0 : 2.0;   // path flag: 1 interior template, 2 geometric-class stencil
             n_int += same;
         }
         ctx->n_interior = n_int;
+        if (std::getenv("BIOT_DEBUG"))
+            std::fprintf(stderr, "[biot] tile2d: W=%lld rows/tile=%d groups=%lld interior=%lld/%lld s0=%d\n",
+                         (long long)ctx->row_w, ctx->rows_per_tile, (long long)ctx->groups, (long long)n_int,
+                         (long long)ctx->N, ctx->s0);
         ALLOC(ctx->aux, aux.size() * sizeof(double));
         CU(h2d(ctx, ctx->aux, aux.data(), aux.size() * sizeof(double)));
         // TMA tensor maps of the two panels: {time (pitch), panel rows}
@@ -932,6 +981,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ctx->pass2_grid = p2.grid;
     }
     ALLOC(ctx->partial, (size_t)ctx->groups * ctx->n_tl * 2 * sizeof(double));
+    ALLOC(ctx->fin_scratch, (size_t)std::max<int64_t>(1, biot::finalize_scratch_doubles((int)ctx->groups, ctx->n_tl)) *
+                                sizeof(double));
     ALLOC(ctx->hist, (size_t)ctx->hist_cap * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->nonfinite, sizeof(int));
@@ -1029,7 +1080,7 @@ biot_status biot_residual_norms(biot_ctx *ctx, double *out) {
     if (st != BIOT_OK) return st;
     CU(launch_main(ctx, biot::MODE_RESIDUAL, ctx->x[ctx->cur], nullptr));
     CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, ctx->norms, ctx->nonfinite,
-                             ctx->stream));
+                             ctx->fin_scratch, ctx->stream));
     CU(cudaMemcpyAsync(out, ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

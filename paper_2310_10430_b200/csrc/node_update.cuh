@@ -30,7 +30,8 @@ __device__ __forceinline__ double cload(const double *p) {
 // Epilogue of one node over the lane's T steps (shared by every sweep kernel so the
 // arithmetic is identical): r = s_t f + q(t-1) - acc, norms, z = P^-1 r (P~2, or the
 // displacement half of P~1), x^{k+1} = x^k + omega z, stores.
-template <int D, int T, class A>
+// MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
+template <int D, int T, class A, bool MASK = true>
 __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
                                               const double (&acc)[D + 1][T], const double (&q)[T],
                                               double qprev, const double (&F)[D + 1],
@@ -50,8 +51,10 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
         r[D] = (sv[tt] * F[D] + qp) - acc[D][tt];
         // Dirichlet rows (D^{-1} = 0) carry no residual: kernels that apply a shared
         // stencil to such rows (tile3d class templates) rely on this mask
+        if constexpr (MASK) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) r[c] = (Dv[c] == 0.0) ? 0.0 : r[c];
+            for (int c = 0; c < NC; ++c) r[c] = (Dv[c] == 0.0) ? 0.0 : r[c];
+        }
         double su = 0.0;
 #pragma unroll
         for (int c = 0; c < D; ++c) su = fma(r[c], r[c], su);

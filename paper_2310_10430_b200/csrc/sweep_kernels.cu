@@ -156,6 +156,36 @@ __global__ void finalize_kernel(const double *__restrict__ partial, int groups, 
     }
 }
 
+// First stage for many groups: block column by sums groups [by*kGch, (by+1)*kGch)
+// (fixed split over 8 y-lanes, then a fixed-order sum of the lane totals).
+constexpr int kGch = 128;
+__global__ void finalize_stage1_kernel(const double *__restrict__ partial, int groups, int n_tl,
+                                       double *__restrict__ out) {
+    __shared__ double sm[8][32][2];
+    const int t = blockIdx.x * 32 + threadIdx.x;
+    const int y = threadIdx.y;
+    const int g0 = blockIdx.y * kGch, g1 = min(groups, g0 + kGch);
+    double su = 0.0, sp = 0.0;
+    if (t < n_tl) {
+        for (int g = g0 + y; g < g1; g += 8) {
+            su += partial[((int64_t)g * n_tl + t) * 2 + 0];
+            sp += partial[((int64_t)g * n_tl + t) * 2 + 1];
+        }
+    }
+    sm[y][threadIdx.x][0] = su;
+    sm[y][threadIdx.x][1] = sp;
+    __syncthreads();
+    if (y == 0 && t < n_tl) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            a += sm[k][threadIdx.x][0];
+            b += sm[k][threadIdx.x][1];
+        }
+        out[((int64_t)blockIdx.y * n_tl + t) * 2 + 0] = a;
+        out[((int64_t)blockIdx.y * n_tl + t) * 2 + 1] = b;
+    }
+}
+
 using SweepFn = void (*)(const SweepArgs);
 using Pass2Fn = void (*)(const Pass2Args);
 
@@ -218,11 +248,20 @@ cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int
     return cudaGetLastError();
 }
 
+int64_t finalize_scratch_doubles(int groups, int n_tl) {
+    return groups > 2 * kGch ? (int64_t)((groups + kGch - 1) / kGch) * n_tl * 2 : 0;
+}
+
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
-                            int *nonfinite, cudaStream_t st) {
+                            int *nonfinite, double *scratch, cudaStream_t st) {
     dim3 block(32, 8);
-    dim3 grid((n_tl + 31) / 32);
-    finalize_kernel<<<grid, block, 0, st>>>(partial, groups, n_tl, norms, nonfinite);
+    if (groups > 2 * kGch) {   // two fixed-order stages: many groups would serialise one pass
+        const int g1 = (groups + kGch - 1) / kGch;
+        finalize_stage1_kernel<<<dim3((n_tl + 31) / 32, g1), block, 0, st>>>(partial, groups, n_tl, scratch);
+        partial = scratch;
+        groups = g1;
+    }
+    finalize_kernel<<<dim3((n_tl + 31) / 32), block, 0, st>>>(partial, groups, n_tl, norms, nonfinite);
     return cudaGetLastError();
 }
 

@@ -67,9 +67,11 @@ struct StencilArgs : SweepArgs {
 
 // Arguments of the TMA-pipelined 2D tile kernel (tile2d_kernels.cu).
 struct Tile2dArgs : SweepArgs {
-    static constexpr int kAux = 16;   // per-node record: AA_pp per slot [7], f [3], dinv [3], interior flag
+    static constexpr int kAux = 16;   // per-node record: AA_pp per slot [7], f [3], dinv [3], path flag
     double tmpl[7][10];               // interior stencil blocks (slot order), pp entry unused
     const double *aux;                // [n_alloc][kAux]
+    const double *cls;                // geometric-class stencils [9][7][kClsW], column-major blocks
+    static constexpr int kClsW = 10;  // 9 AA entries + A'_pp
     int64_t pad_nodes;                // panel rows start at node -pad_nodes
     int32_t s0;                       // zero-storage variant: extra structural zeros (see tile2d)
     int32_t dry;                      // dev/measurement only: stream the ring without computing
@@ -112,9 +114,10 @@ inline int64_t march_groups(const SweepArgs &a) {
 }
 
 // 2D TMA tile kernel: x boxes {time, rows} of the panel tensor map
-int64_t tile2d_groups(const Tile2dArgs &a);
+int64_t tile2d_groups(const Tile2dArgs &a);   // norm-partial groups: tiles x columns
 int tile2d_chunk();
-int tile2d_seg();   // grid columns per tile (8 x R)
+int tile2d_seg();         // grid columns per tile
+int tile2d_max_rows();    // rows per tile (q carry capacity)
 void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
@@ -134,7 +137,10 @@ bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);
 cudaError_t launch_stencil(int dim, int R, int T, const StencilArgs &a, const LaunchShape &sh,
                            cudaStream_t st);
+// scratch: finalize_scratch_doubles(groups, n_tl) doubles (two-stage reduction when
+// there are many groups; both stages in a fixed order, so the result is deterministic)
+int64_t finalize_scratch_doubles(int groups, int n_tl);
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
-                            int *nonfinite, cudaStream_t st);
+                            int *nonfinite, double *scratch, cudaStream_t st);
 
 }  // namespace biot

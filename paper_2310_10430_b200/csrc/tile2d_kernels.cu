@@ -1,30 +1,33 @@
-// TMA-pipelined 2D sweep kernel (structured right-triangle meshes, BDIA slot
-// order [0, -W-1, -W, -1, +1, +W, +W+1]).  One outer iteration of the
-// Jacobi-in-time inverted scheme with the block
-// preconditioner (L238-262), the damped update and the per-step norms fused.
+// TMA-pipelined 2D sweep kernel (structured n1 x n1 grid of right triangles,
+// P1-P1, BDIA slot order [0, -W-1, -W, -1, +1, +W, +W+1]).  One outer
+// iteration of the Jacobi-in-time inverted scheme (Alg. 2 as
+// BASELINE.json reads it) with the block preconditioner (L238-262), the damped
+// update and the per-step residual norms fused.
 //
-// Work tile = SEG = 8R consecutive grid columns x 64 time steps x a range of
-// grid rows, marched upward.  A producer warp streams, for every grid row r of
-// the tile (plus the two halo rows), one TMA tensor box -- the (SEG+2)-node strip
-// x 3 components x 66 time steps (t0-2 .. t0+63) of the space-time panel -- and
-// one bulk copy of the SEG row nodes' aux records (kappa-dependent pressure
-// entries, load, preconditioner diagonals) into a shared-memory ring
-// (full/empty mbarriers).  Consumer warp w computes R horizontally adjacent
-// nodes (r, i0 + R w + k) from shared memory only; for R = 2 their 14
-// (node, neighbour) products need 10 distinct columns of rows r-1, r, r+1,
-// walked once in a fixed order.  Every x value is read from HBM/L2 once per
-// tile (+2/SEG halo from L2); compute warps issue no global loads except for
-// boundary-class nodes.
+// The 2D path is HBM-bound (~88 FMAs per node and step against 48 bytes of x
+// traffic), so the kernel is built to stream the space-time panel once with as
+// few instructions per byte as possible:
+//  * work tile = SEG = 15 consecutive grid columns x a range of grid rows, for
+//    every 128-step time chunk in turn (4 steps per lane: steps 2l, 2l+1 and
+//    64+2l, 64+2l+1, so each 16-B shared-memory load of the warp is one contiguous
+//    512-B run -- conflict-free; every coefficient and every loop/barrier
+//    instruction serves 4 steps);
+//  * a producer warp streams each grid row's strip (17 nodes x 3 comps x 128
+//    steps, one TMA tensor box, no time halo) and the 15 nodes' aux records
+//    (kappa-dependent AA_pp per slot, load, preconditioner diagonals, path flag)
+//    into a 4-stage ring;
+//  * 15 consumer warps (one column each) march the rows holding only two rows:
+//    at step m (rows m-1, m resident) a warp finishes its node of row m-1 (the
+//    +W slots, then the epilogue) and starts its node of row m (-W and 0 slots);
+//  * interior nodes share one stencil (kernel parameters, uniform-register
+//    operands, structural zeros skipped); edge/corner nodes use the stencil of
+//    their geometric class (9 classes, shared memory).
 //
-// Interior nodes share one stencil (uniform lambda, mu, alpha, S and mesh):
-// their blocks are kernel parameters (constant-bank operands); only the
-// kappa-dependent pressure-pressure entry of AA varies per node (aux record).
-// Structural zeros of that stencil are skipped at compile time (host-verified;
-// fma(0, x, acc) == acc).  Nodes whose blocks differ from the template
-// (boundary rows/columns, Dirichlet masking) read full blocks from global
-// memory.  The epilogue is dev::node_epilogue, shared with every kernel; the
-// neighbour order is the fixed column order below (deterministic, independent
-// of the time-slab split; equal to the generic kernel to rounding).
+// Previous-step coupling (A' x_{n-1})_p: lane l uses q(t-1) of lane l-1 (one
+// shuffle); lane 0 takes q(t0-1) from a shared-memory carry written by lane 31
+// in the previous chunk, and in chunk 0 recomputes it from the ghost vector
+// x_{first-1} in the same FMA order (iterates are bitwise independent of the
+// time-slab split).  Per node the slots run in (row, column) order.
 #include <cuda.h>
 #include <cstdint>
 #include <cstdio>
@@ -39,511 +42,391 @@ namespace biot {
 namespace {
 
 using namespace dev;
+using namespace tma;
 
-constexpr int kT = 2;                       // time steps per lane
-constexpr int kCh = 32 * kT;                // time steps per tile
-constexpr int kChp = kCh + 2;               // + halo steps t0-2, t0-1
-template <int R, int NC>
-struct Geo {
-    static constexpr int kSeg = NC * R;                               // row nodes per tile
-    static constexpr int kStrip = kSeg + 2;                           // + halo columns
-    static constexpr int kXRows = kStrip * 3;                         // tensor rows per stage
-    static constexpr uint32_t kXBytes = kXRows * kChp * 8;
-    static constexpr uint32_t kAuxOff = (kXBytes + 127) / 128 * 128;
-    static constexpr uint32_t kAuxBytes = kSeg * Tile2dArgs::kAux * 8;
-    static constexpr uint32_t kStageBytes = (kAuxOff + kAuxBytes + 127) / 128 * 128;
-};
+constexpr int kSeg = 15;                    // grid columns per tile = consumer warps
+constexpr int kStrip = kSeg + 2;            // + halo columns
+constexpr int kT2 = 4;                      // time steps per lane
+constexpr int kCT = 32 * kT2;               // time steps per chunk
+constexpr int kStages = 4;
+constexpr int kMaxRR = 48;                  // rows per tile (q carry capacity)
+constexpr int kAuxRec = Tile2dArgs::kAux;   // doubles per aux record
+constexpr int kCW = Tile2dArgs::kClsW;      // doubles per class-stencil slot
+constexpr uint32_t kXBytes = kStrip * 3 * kCT * 8;                                 // 52224
+constexpr uint32_t kAuxBytes = kSeg * kAuxRec * 8;                                 // 1920
+constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;          // 54144
+constexpr uint32_t kClsOff = kStages * kStageBytes;
+constexpr uint32_t kCarryOff = kClsOff + 9 * 7 * kCW * 8;
+constexpr uint32_t kSmemBytes = kCarryOff + kMaxRR * kSeg * 8;
 
 // (row delta, column delta) of the 7 BDIA slots in storage order
-__device__ constexpr int kDr[7] = {0, -1, -1, 0, 0, 1, 1};
-__device__ constexpr int kDc[7] = {0, -1, 0, -1, 1, 0, 1};
-
-// Column walk of an R-node horizontal group A = (r, c), B = (r, c+1):
-// row delta, column delta (from A), slot of A served, slot of B served (-1: none).
-template <int R>
-struct Walk;
-template <>
-struct Walk<1> {
-    static constexpr int N = 7;
-    __host__ __device__ static constexpr int dr(int k) { return k == 0 ? 0 : k <= 2 ? -1 : k <= 4 ? 0 : 1; }
-    __host__ __device__ static constexpr int dc(int k) {
-        return k == 0 ? 0 : k == 1 ? -1 : k == 2 ? 0 : k == 3 ? -1 : k == 4 ? 1 : k == 5 ? 0 : 1;
-    }
-    __host__ __device__ static constexpr int slot(int k, int node) { return node == 0 ? k : -1; }
-};
-template <>
-struct Walk<2> {
-    static constexpr int N = 10;
-    __host__ __device__ static constexpr int dr(int k) { return k <= 2 ? -1 : k <= 6 ? 0 : 1; }
-    __host__ __device__ static constexpr int dc(int k) {
-        return k == 0 ? -1 : k == 1 ? 0 : k == 2 ? 1 : k == 3 ? -1 : k == 4 ? 0 : k == 5 ? 1 : k == 6 ? 2
-               : k == 7 ? 0 : k == 8 ? 1 : 2;
-    }
-    __host__ __device__ static constexpr int slot(int k, int node) {
-        // A: k -> 1 2 - 3 0 4 - 5 6 - ;  B: k -> - 1 2 - 3 0 4 - 5 6
-        return node == 0 ? (k == 0 ? 1 : k == 1 ? 2 : k == 2 ? -1 : k == 3 ? 3 : k == 4 ? 0 : k == 5 ? 4
-                            : k == 6 ? -1 : k == 7 ? 5 : k == 8 ? 6 : -1)
-                         : (k == 0 ? -1 : k == 1 ? 1 : k == 2 ? 2 : k == 3 ? -1 : k == 4 ? 3 : k == 5 ? 0
-                            : k == 6 ? 4 : k == 7 ? -1 : k == 8 ? 5 : 6);
-    }
-};
+__host__ __device__ constexpr int sdr(int s) { return (s == 1 || s == 2) ? -1 : (s >= 5) ? 1 : 0; }
+__host__ __device__ constexpr int sdc(int s) { return (s == 1 || s == 3) ? -1 : (s == 4 || s == 6) ? 1 : 0; }
+__host__ __device__ constexpr int slot2(int dr, int dc) {
+    int r = -1;
+    for (int s = 0; s < 7; ++s)
+        if (sdr(s) == dr && sdc(s) == dc) r = s;
+    return r;
+}
 
 // Structural zeros of the interior right-triangle stencil, entry e = c*3+cc of the
 // AA block (e < 9) or 9 = A'_pp: the self block has no displacement-pressure
 // coupling, the diagonal (SW/NE) neighbours have no u_x-u_x / u_y-u_y coupling,
-// and with S = 0 no pressure-pressure coupling either (L is the 5-point stencil).
+// and with S = 0 and uniform kappa no pressure-pressure coupling either (L is the
+// 5-point stencil).  Host-verified.
 __host__ __device__ constexpr bool tmpl_zero(int s, int e, bool s0) {
     return (s == 0) ? (e == 2 || e == 5 || e == 6 || e == 7)
                     : (s == 1 || s == 6) ? (e == 0 || e == 4 || (s0 && (e == 8 || e == 9))) : false;
 }
 
-using namespace tma;
+// lane l holds steps t0 + {2l, 2l+1, 64+2l, 64+2l+1}: index tt -> (tt>>1)*64 + 2l + (tt&1)
+__device__ __forceinline__ const double *col2(const double *row, int p, int c, int lane) {
+    return row + (p * 3 + c) * kCT + lane * 2;
+}
 
-template <int SEG>
-struct TileGeom {
-    int64_t n_seg, n_jr, n_chunks, n_tiles;
-    __device__ explicit TileGeom(const Tile2dArgs &a) {
-        n_seg = (a.row_w + SEG - 1) / SEG;
-        n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
-        n_chunks = (a.n_tl + kCh - 1) / kCh;
-        n_tiles = n_seg * n_jr * n_chunks;
-    }
-};
-
-// x of one column (3 components x kT steps) from a ring stage
-__device__ __forceinline__ void load_col(double (&v)[3][kT], const double *colp) {
+__device__ __forceinline__ void load_v(double (&v)[3][kT2], const double *row, int p, int lane) {
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
-        const double2 w2 = *reinterpret_cast<const double2 *>(colp + cc * kChp);
-        v[cc][0] = w2.x;
-        v[cc][1] = w2.y;
+        const double *src = col2(row, p, cc, lane);
+#pragma unroll
+        for (int h = 0; h < kT2; h += 2) {
+            const double2 w = *reinterpret_cast<const double2 *>(src + (h >> 1) * (kCT / 2));
+            v[cc][h] = w.x;
+            v[cc][h + 1] = w.y;
+        }
     }
 }
 
-// interior block coefficient (template, with the per-node pp entry)
-__device__ __forceinline__ double tcoef(const Tile2dArgs &a, int s, int e, double pp) {
-    return (e == 8) ? pp : a.tmpl[s][e];
-}
-
-// acc/q update of one interior node by gathered column v through slot s
+// acc/q of one interior node through slot s by the gathered column v
 template <bool S0>
-__device__ __forceinline__ void fma_interior(double (&acc)[3][kT], double (&q)[kT], const Tile2dArgs &a, int s,
-                                             double pp, const double (&v)[3][kT]) {
+__device__ __forceinline__ void fma_tmpl(double (&acc)[3][kT2], double (&q)[kT2], const Tile2dArgs &a, int s,
+                                         double pp, const double (&v)[3][kT2]) {
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const int e = c * 3 + cc;
             if (tmpl_zero(s, e, S0)) continue;
-            const double cf = tcoef(a, s, e, pp);
+            const double cf = (e == 8) ? pp : a.tmpl[s][e];
 #pragma unroll
-            for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
+            for (int tt = 0; tt < kT2; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
         }
-        const int eq = (cc < 2) ? 6 + cc : 9;
+        const int eq = cc < 2 ? 6 + cc : 9;
         if (!tmpl_zero(s, eq, S0)) {
 #pragma unroll
-            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(a.tmpl[s][eq], v[cc][tt], q[tt]);
+            for (int tt = 0; tt < kT2; ++tt) q[tt] = fma(a.tmpl[s][eq], v[cc][tt], q[tt]);
         }
     }
 }
 
-// R interior nodes of one row (warp group): walk the union columns once.
-template <int R, bool GHOST, bool S0>
-__device__ __forceinline__ void group_interior(const Tile2dArgs &a, const double *r0, const double *r1,
-                                               const double *r2, const double *aux0, int j,
-                                               int64_t col0, int p0, int lane, int t0, const double (&sv)[kT],
-                                               double (&nu)[kT], double (&npn)[kT]) {
-    using Wk = Walk<R>;
-    const double *rows[3] = {r0, r1, r2};
-    const int64_t W = a.row_w;
-    double acc[R][3][kT], q[R][kT];
+// same through a class stencil in shared memory (column-major per slot:
+// T[cc*3 + c] = AA[c][cc], T[9] = A'_pp)
+__device__ __forceinline__ void fma_cls(double (&acc)[3][kT2], double (&q)[kT2], const double *T, double pp,
+                                        const double (&v)[3][kT2]) {
 #pragma unroll
-    for (int n = 0; n < R; ++n)
+    for (int cc = 0; cc < 3; ++cc) {
+        const double c0 = T[cc * 3], c1 = T[cc * 3 + 1], c2 = cc == 2 ? pp : T[cc * 3 + 2];
+        const double cq = cc < 2 ? T[cc * 3 + 2] : T[9];
 #pragma unroll
-        for (int tt = 0; tt < kT; ++tt) {
-            q[n][tt] = 0.0;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) acc[n][c][tt] = 0.0;
-        }
-#pragma unroll
-    for (int k = 0; k < Wk::N; ++k) {
-        double v[3][kT];
-        load_col(v, rows[1 + Wk::dr(k)] + ((p0 + Wk::dc(k)) * 3) * kChp + 2 + lane * kT);
-#pragma unroll
-        for (int n = 0; n < R; ++n) {
-            const int s = Wk::slot(k, n);
-            if (s < 0) continue;
-            fma_interior<S0>(acc[n], q[n], a, s, aux0[n * Tile2dArgs::kAux + s], v);
+        for (int tt = 0; tt < kT2; ++tt) {
+            acc[0][tt] = fma(c0, v[cc][tt], acc[0][tt]);
+            acc[1][tt] = fma(c1, v[cc][tt], acc[1][tt]);
+            acc[2][tt] = fma(c2, v[cc][tt], acc[2][tt]);
+            q[tt] = fma(cq, v[cc][tt], q[tt]);
         }
     }
-    double qp[R];
+}
+
+// slots of row delta DR for the warp's node (strip position p), in column order
+template <int DR, bool CLS, bool S0>
+__device__ __forceinline__ void accum_row(const Tile2dArgs &a, const double *row, int p, int lane,
+                                          const double *aux, const double *T, double (&acc)[3][kT2],
+                                          double (&q)[kT2]) {
 #pragma unroll
-    for (int n = 0; n < R; ++n) qp[n] = __shfl_up_sync(0xffffffffu, q[n][kT - 1], 1);
-    if (lane == 0) {                 // q(t0-1): same order, x at t0-1 (ring) or the ghost
-        double g[R];
+    for (int dc = -1; dc <= 1; ++dc) {
+        const int s = slot2(DR, dc);
+        if (s < 0) continue;
+        double v[3][kT2];
+        load_v(v, row, p + dc, lane);
+        if constexpr (CLS) fma_cls(acc, q, T + s * kCW, aux[s], v);
+        else fma_tmpl<S0>(acc, q, a, s, aux[s], v);
+    }
+}
+
+// q(t0-1) from the ghost x_{first-1} in the accumulation order (lane 0, chunk 0)
+template <bool CLS, bool S0>
+__device__ __forceinline__ double ghost_q(const Tile2dArgs &a, int64_t i, const double *T) {
+    double g = 0.0;
 #pragma unroll
-        for (int n = 0; n < R; ++n) g[n] = 0.0;
+    for (int dr = -1; dr <= 1; ++dr)
 #pragma unroll
-        for (int k = 0; k < Wk::N; ++k) {
-            double xv[3];
-            if constexpr (GHOST) {
-                const int64_t jn = (int64_t)(j + Wk::dr(k)) * W + col0 + Wk::dc(k);
+        for (int dc = -1; dc <= 1; ++dc) {
+            const int s = slot2(dr, dc);
+            if (s < 0) continue;
+            const int64_t j = i + a.off[s];
 #pragma unroll
-                for (int cc = 0; cc < 3; ++cc) xv[cc] = __ldg(a.ghost + jn * 3 + cc);
-            } else {
-                const double *colp = rows[1 + Wk::dr(k)] + ((p0 + Wk::dc(k)) * 3) * kChp + 1;
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc) xv[cc] = colp[cc * kChp];
-            }
-#pragma unroll
-            for (int n = 0; n < R; ++n) {
-                const int s = Wk::slot(k, n);
-                if (s < 0) continue;
-#pragma unroll
-                for (int cc = 0; cc < 3; ++cc) {
-                    const int eq = (cc < 2) ? 6 + cc : 9;
-                    if (!tmpl_zero(s, eq, S0)) g[n] = fma(a.tmpl[s][eq], xv[cc], g[n]);
+            for (int cc = 0; cc < 3; ++cc) {
+                const double xv = __ldg(a.ghost + j * 3 + cc);
+                if constexpr (CLS) {
+                    g = fma(cc < 2 ? T[s * kCW + cc * 3 + 2] : T[s * kCW + 9], xv, g);
+                } else {
+                    const int eq = cc < 2 ? 6 + cc : 9;
+                    if (!tmpl_zero(s, eq, S0)) g = fma(a.tmpl[s][eq], xv, g);
                 }
             }
         }
-#pragma unroll
-        for (int n = 0; n < R; ++n) qp[n] = g[n];
-    }
-#pragma unroll
-    for (int n = 0; n < R; ++n) {
-        const double *aux = aux0 + n * Tile2dArgs::kAux;
-        double F[3], Dv[3], xs[3][kT];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            F[c] = aux[7 + c];
-            Dv[c] = aux[10 + c];
-        }
-        load_col(xs, rows[1] + ((p0 + n) * 3) * kChp + 2 + lane * kT);
-        node_epilogue<2, kT>(a, (int64_t)j * W + col0 + n, t0, acc[n], q[n], qp[n], F, Dv, xs, sv, nu, npn);
-    }
+    return g;
 }
 
-// Everything the boundary path reads from the kernel parameters (so the
-// out-of-line function does not force the whole parameter block into local
-// memory); also what node_epilogue needs.
-struct BArgs {
-    double *xn, *zbuf, *sendbuf;
-    const double *blk, *ghost;
-    int64_t pitch, row_w;
-    int64_t off[7];
-    int32_t n_tl, mode;
-    double omega;
-};
-
-struct Norms2 {
-    double nu[kT], npn[kT];
-};
-
-// Boundary-class node at strip position p of row j: full blocks from global
-// memory, slot order.  Rare (domain edges, Dirichlet neighbourhoods): kept out of
-// line so its register footprint does not burden the interior path.
-__device__ __noinline__ Norms2 node_boundary(const BArgs &a, const double *r0, const double *r1,
-                                             const double *r2, const double *aux, int j, int64_t col, int p,
-                                             int lane, int t0, double sv0, double sv1) {
-    const double *rows[3] = {r0, r1, r2};
-    const double sv[kT] = {sv0, sv1};
-    double nu[kT] = {0.0, 0.0}, npn[kT] = {0.0, 0.0};
-    const int64_t i = (int64_t)j * a.row_w + col;
-    const double *gb = a.blk + i * (7 * 10);
-    double acc[3][kT], q[kT];
+template <bool CLS, bool S0>
+__device__ __forceinline__ void start(const Tile2dArgs &a, const double *pd, const double *pm, int p, int lane,
+                                      const double *aux, const double *T, double (&acc)[3][kT2],
+                                      double (&q)[kT2]) {
 #pragma unroll
-    for (int tt = 0; tt < kT; ++tt) {
+    for (int tt = 0; tt < kT2; ++tt) {
         q[tt] = 0.0;
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c][tt] = 0.0;
     }
-#pragma unroll 1
-    for (int s = 0; s < 7; ++s) {
-        double v[3][kT];
-        load_col(v, rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 2 + lane * kT);
-#pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                const double cf = __ldg(gb + s * 10 + c * 3 + cc);
-#pragma unroll
-                for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
-            }
-            const double qc = __ldg(gb + s * 10 + ((cc < 2) ? 6 + cc : 9));
-#pragma unroll
-            for (int tt = 0; tt < kT; ++tt) q[tt] = fma(qc, v[cc][tt], q[tt]);
-        }
-    }
-    double qp = __shfl_up_sync(0xffffffffu, q[kT - 1], 1);
-    if (lane == 0) {
-        double g = 0.0;
-        for (int s = 0; s < 7; ++s) {
-            const int64_t jn = i + a.off[s];
-            const double *colp = rows[1 + kDr[s]] + ((p + kDc[s]) * 3) * kChp + 1;
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                const double qc = __ldg(gb + s * 10 + ((cc < 2) ? 6 + cc : 9));
-                const double xv = (t0 == 0) ? __ldg(a.ghost + jn * 3 + cc) : colp[cc * kChp];
-                g = fma(qc, xv, g);
-            }
-        }
-        qp = g;
-    }
-    double F[3], Dv[3], xs[3][kT];
+    accum_row<-1, CLS, S0>(a, pd, p, lane, aux, T, acc, q);
+    accum_row<0, CLS, S0>(a, pm, p, lane, aux, T, acc, q);
+}
+
+// The epilogue runs on each half (2 consecutive steps) of the lane's steps.
+template <bool CLS, bool S0>
+__device__ __forceinline__ void finish(const Tile2dArgs &a, const double *po, const double *pu, int p, int lane,
+                                       const double *aux, const double *T, int64_t i, int t0, bool ghost,
+                                       double *carry, const double (&sv)[kT2], double (&acc)[3][kT2],
+                                       double (&q)[kT2], double (&nu)[kT2], double (&npn)[kT2]) {
+    accum_row<1, CLS, S0>(a, pu, p, lane, aux, T, acc, q);
+    // q(t-1) of each half's first step: lane l-1's matching step; lane 0 of the second
+    // half takes lane 31's first-half step 63, lane 0 of the first half the carry
+    double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
+    double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
+    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0>(a, i, T) : *carry;
+    __syncwarp();
+    if (lane == 31) *carry = q[3];
+    double F[3], Dv[3], xs[3][kT2];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
         F[c] = aux[7 + c];
         Dv[c] = aux[10 + c];
     }
-    load_col(xs, rows[1] + (p * 3) * kChp + 2 + lane * kT);
-    node_epilogue<2, kT>(a, i, t0, acc, q, qp, F, Dv, xs, sv, nu, npn);
-    Norms2 o;
+    load_v(xs, po, p, lane);
 #pragma unroll
-    for (int tt = 0; tt < kT; ++tt) {
-        o.nu[tt] = nu[tt];
-        o.npn[tt] = npn[tt];
+    for (int h = 0; h < 2; ++h) {
+        double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2];
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            q2[tt] = q[2 * h + tt];
+            sv2[tt] = sv[2 * h + tt];
+            nu2[tt] = nu[2 * h + tt];
+            np2[tt] = npn[2 * h + tt];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                acc2[c][tt] = acc[c][2 * h + tt];
+                xs2[c][tt] = xs[c][2 * h + tt];
+            }
+        }
+        node_epilogue<2, 2, Tile2dArgs, CLS>(a, i, t0 + h * (kCT / 2), acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2,
+                                             sv2, nu2, np2);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            nu[2 * h + tt] = nu2[tt];
+            npn[2 * h + tt] = np2[tt];
+        }
     }
-    return o;
 }
 
-template <int R, int NC, int STAGES, int MAXREG>
-__global__ void __launch_bounds__((NC + 1) * 32) __maxnreg__(MAXREG)
+struct Geo2 {
+    int W, nrows, nseg, nrr, ntiles, nchunks, rr;
+    __device__ explicit Geo2(const Tile2dArgs &a) {
+        W = (int)a.row_w;
+        nrows = a.n_rows;
+        rr = a.rows_per_tile;
+        nseg = (W + kSeg - 1) / kSeg;
+        nrr = (nrows + rr - 1) / rr;
+        ntiles = nseg * nrr;
+        nchunks = (a.n_tl + kCT - 1) / kCT;
+    }
+    __device__ void decode(int tile, int &i0, int &ja, int &jb) const {
+        const int seg = tile % nseg, r = tile / nseg;
+        i0 = seg * kSeg;
+        ja = r * rr;
+        jb = min(nrows, ja + rr);
+    }
+};
+
+__device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); }
+
+template <bool S0>
+__global__ void __launch_bounds__((kSeg + 1) * 32, 1)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
-    using G = Geo<R, NC>;
-    constexpr int kConsumers = NC;
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ uint64_t full[STAGES], empty[STAGES];
-    __shared__ double red[kConsumers][kCh][2];
+    __shared__ uint64_t full[kStages], empty[kStages];
+    double *cls_sm = reinterpret_cast<double *>(smem + kClsOff);     // [9][7][kCW]
+    double *qcarry = reinterpret_cast<double *>(smem + kCarryOff);   // [kMaxRR][kSeg]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileGeom<G::kSeg> g(a);
-    const int64_t W = a.row_w;
+    const Geo2 g(a);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumers);
+            mbar_init(&empty[s], kSeg);
         }
         fence_barrier_init();
     }
+    for (int k = threadIdx.x; k < 9 * 7 * kCW; k += blockDim.x) cls_sm[k] = a.cls[k];
     __syncthreads();
 
-    if (warp == kConsumers) {
+    if (warp == kSeg) {
         // ------------------------------- producer -------------------------------
         if (lane == 0) {
             uint32_t it = 0;
-            for (int64_t tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
-                const int chunk = (int)(tile % g.n_chunks);
-                const int64_t grp = tile / g.n_chunks;
-                const int64_t seg = grp % g.n_seg, jr = grp / g.n_seg;
-                const int ja = (int)(jr * a.rows_per_tile);
-                const int jb = min(a.n_rows, ja + a.rows_per_tile);
-                const int64_t i0 = seg * G::kSeg;
-                for (int r = ja - 1; r <= jb; ++r, ++it) {
-                    const int st = it % STAGES;
-                    if (it >= (uint32_t)STAGES) mbar_wait_sleep(&empty[st], ((it / STAGES) - 1) & 1);
-                    unsigned char *base = smem + (size_t)st * G::kStageBytes;
-                    const bool real = (r >= 0 && r < a.n_rows);
-                    mbar_expect_tx(&full[st], G::kXBytes + (real ? G::kAuxBytes : 0u));
-                    const int64_t node0 = (int64_t)r * W + i0 - 1;
-                    load_2d(base, &tmx, chunk * kCh - 2, (int)((node0 + a.pad_nodes) * 3), &full[st]);
-                    if (real)
-                        bulk_g2s(base + G::kAuxOff, a.aux + ((int64_t)r * W + i0) * Tile2dArgs::kAux, G::kAuxBytes,
-                                 &full[st]);
-                }
+            for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+                int i0, ja, jb;
+                g.decode(tile, i0, ja, jb);
+                for (int chunk = 0; chunk < g.nchunks; ++chunk)
+                    for (int r = ja - 1; r <= jb; ++r, ++it) {
+                        const int st = it % kStages;
+                        if (it >= (uint32_t)kStages) mbar_wait_suspend(&empty[st], ((it / kStages) - 1) & 1);
+                        unsigned char *base = smem + (size_t)st * kStageBytes;
+                        const bool real = (r >= 0 && r < g.nrows);
+                        mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
+                        const int64_t node0 = (int64_t)r * g.W + i0 - 1;
+                        load_2d(base, &tmx, chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
+                        if (real)
+                            bulk_g2s(base + kXBytes, a.aux + ((int64_t)r * g.W + i0) * kAuxRec, kAuxBytes,
+                                     &full[st]);
+                    }
             }
         }
         return;
     }
 
     // ------------------------------- consumers ------------------------------
+    const int p = warp + 1;                   // strip position of the warp's column
     uint32_t it = 0;
-    const int p0 = 1 + R * warp;              // strip position of the warp's first node
-    for (int64_t tile = blockIdx.x; tile < g.n_tiles; tile += gridDim.x) {
-        const int chunk = (int)(tile % g.n_chunks);
-        const int64_t grp = tile / g.n_chunks;
-        const int64_t seg = grp % g.n_seg, jr = grp / g.n_seg;
-        const int ja = (int)(jr * a.rows_per_tile);
-        const int jb = min(a.n_rows, ja + a.rows_per_tile);
-        const int64_t col0 = seg * G::kSeg + R * warp;
-        const int64_t rem = W - col0;
-        const int nvalid = rem <= 0 ? 0 : (rem >= R ? R : (int)rem);
-        const int t0 = chunk * kCh + lane * kT;
-        double nu[kT], npn[kT], sv[kT];
+    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
+        int i0, ja, jb;
+        g.decode(tile, i0, ja, jb);
+        const int col = i0 + warp;
+        const bool valid = col < g.W;
+        const int ccx = axis_class(min(col, g.W - 1), g.W);
+        for (int chunk = 0; chunk < g.nchunks; ++chunk) {
+            const int t0 = chunk * kCT + lane * 2;   // the lane's first half; second half at t0 + 64
+            const bool ghost = chunk == 0;
+            double nu[kT2], npn[kT2], sv[kT2];
 #pragma unroll
-        for (int tt = 0; tt < kT; ++tt) {
-            nu[tt] = 0.0;
-            npn[tt] = 0.0;
-            sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
-        }
-        // ring positions (stage index, phase parity) of rows j-1, j, j+1, advanced
-        // incrementally (no division by the stage count in the row loop)
-        int s0i = it % STAGES;
-        uint32_t ph0 = (it / STAGES) & 1;
-        int s1i = s0i + 1 == STAGES ? 0 : s0i + 1;
-        uint32_t ph1 = s1i == 0 ? ph0 ^ 1u : ph0;
-        mbar_wait(&full[s0i], ph0);
-        mbar_wait(&full[s1i], ph1);
-        for (int j = ja; j < jb; ++j) {
-            const int s2i = s1i + 1 == STAGES ? 0 : s1i + 1;
-            const uint32_t ph2 = s2i == 0 ? ph1 ^ 1u : ph1;
-            mbar_wait(&full[s2i], ph2);
-            if (nvalid > 0 && !a.dry) {
-                const double *r0 = reinterpret_cast<const double *>(smem + (size_t)s0i * G::kStageBytes);
-                const double *r1 = reinterpret_cast<const double *>(smem + (size_t)s1i * G::kStageBytes);
-                const double *r2 = reinterpret_cast<const double *>(smem + (size_t)s2i * G::kStageBytes);
-                const double *aux0 = reinterpret_cast<const double *>(
-                                         reinterpret_cast<const unsigned char *>(r1) + G::kAuxOff) +
-                                     (R * warp) * Tile2dArgs::kAux;
-                bool interior = (nvalid == R);   // partial groups (last segment) take the generic path
-#pragma unroll
-                for (int n = 0; n < R; ++n) interior &= aux0[n * Tile2dArgs::kAux + 13] != 0.0;
-                if (interior) {
-                    if (chunk == 0) {
-                        if (a.s0)
-                            group_interior<R, true, true>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
+            for (int tt = 0; tt < kT2; ++tt) {
+                nu[tt] = 0.0;
+                npn[tt] = 0.0;
+                const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
+                sv[tt] = (t < a.n_tl) ? a.s[t] : 0.0;
+            }
+            double acc[3][kT2], q[kT2];
+            int kindP = 0;                       // pending node (row m-1): 0 none, 1 interior, 2 class
+            const double *T = cls_sm;
+            int sd = it % kStages;               // stage of row m-1
+            uint32_t phd = (it / kStages) & 1;
+            mbar_wait_suspend(&full[sd], phd);
+            for (int m = ja; m <= jb; ++m) {
+                const int sm_ = sd + 1 == kStages ? 0 : sd + 1;
+                const uint32_t phm = sm_ == 0 ? phd ^ 1u : phd;
+                mbar_wait_suspend(&full[sm_], phm);
+                const double *pd = reinterpret_cast<const double *>(smem + (size_t)sd * kStageBytes);
+                const double *pm = reinterpret_cast<const double *>(smem + (size_t)sm_ * kStageBytes);
+                if (a.dry != 1) {
+                    if (kindP != 0) {            // finish row m-1
+                        const double *aux = reinterpret_cast<const double *>(
+                                                reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
+                        const int64_t i = (int64_t)(m - 1) * g.W + col;
+                        double *carry = qcarry + (m - 1 - ja) * kSeg + warp;
+                        if (kindP == 1)
+                            finish<false, S0>(a, pd, pm, p, lane, aux, T, i, t0, ghost, carry, sv, acc, q, nu, npn);
                         else
-                            group_interior<R, true, false>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
-                    } else {
-                        if (a.s0)
-                            group_interior<R, false, true>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
-                        else
-                            group_interior<R, false, false>(a, r0, r1, r2, aux0, j, col0, p0, lane, t0, sv, nu, npn);
+                            finish<true, S0>(a, pd, pm, p, lane, aux, T, i, t0, ghost, carry, sv, acc, q, nu, npn);
                     }
-                } else {
-                    BArgs b;
-                    b.xn = a.xn; b.zbuf = a.zbuf; b.sendbuf = a.sendbuf; b.blk = a.blk; b.ghost = a.ghost;
-                    b.pitch = a.pitch; b.row_w = a.row_w; b.n_tl = a.n_tl; b.mode = a.mode; b.omega = a.omega;
-#pragma unroll
-                    for (int q = 0; q < 7; ++q) b.off[q] = a.off[q];
-                    for (int n = 0; n < nvalid; ++n) {
-                        const Norms2 o = node_boundary(b, r0, r1, r2, aux0 + n * Tile2dArgs::kAux, j, col0 + n,
-                                                       p0 + n, lane, t0, sv[0], sv[1]);
-#pragma unroll
-                        for (int tt = 0; tt < kT; ++tt) {
-                            nu[tt] += o.nu[tt];
-                            npn[tt] += o.npn[tt];
+                    kindP = 0;
+                    if (m < jb && valid) {       // start row m
+                        const double *aux = reinterpret_cast<const double *>(
+                                                reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                        kindP = aux[13] == 1.0 ? 1 : 2;
+                        if (kindP == 1) {
+                            start<false, S0>(a, pd, pm, p, lane, aux, T, acc, q);
+                        } else {
+                            T = cls_sm + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
+                            start<true, S0>(a, pd, pm, p, lane, aux, T, acc, q);
                         }
                     }
                 }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sd]);   // row m-1 no longer needed
+                sd = sm_;
+                phd = phm;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s0i]);   // row j-1 no longer needed
-            s0i = s1i;
-            ph0 = ph1;
-            s1i = s2i;
-            ph1 = ph2;
-        }
-        if (lane == 0) {                        // rows jb-1 and jb
-            mbar_arrive(&empty[s0i]);
-            mbar_arrive(&empty[s1i]);
-        }
-        it += (uint32_t)(jb - ja + 2);
-        // per-step norm partials of this tile (fixed reduction order over warps)
+            if (lane == 0) mbar_arrive(&empty[sd]);       // row jb
+            it += (uint32_t)(jb - ja + 2);
+            // per-step norm partials of this (tile, column, chunk), summed over the rows
 #pragma unroll
-        for (int tt = 0; tt < kT; ++tt) {
-            red[warp][lane * kT + tt][0] = nu[tt];
-            red[warp][lane * kT + tt][1] = npn[tt];
-        }
-        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
-        for (int k = threadIdx.x; k < kCh * 2; k += kConsumers * 32) {
-            const int tl = k >> 1, part = k & 1;
-            const int t = chunk * kCh + tl;
-            if (t < a.n_tl) {
-                double sum = 0.0;
-#pragma unroll
-                for (int w = 0; w < kConsumers; ++w) sum += red[w][tl][part];
-                a.partial[(grp * a.n_tl + t) * 2 + part] = sum;
+            for (int tt = 0; tt < kT2; ++tt) {
+                const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
+                if (t < a.n_tl) {
+                    double *dst = a.partial + (((int64_t)tile * kSeg + warp) * a.n_tl + t) * 2;
+                    dst[0] = nu[tt];
+                    dst[1] = npn[tt];
+                }
             }
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
     }
-}
-
-struct TileCfg {
-    int r, nc, stages, maxreg;
-};
-
-TileCfg tile_cfg() {
-    TileCfg c{1, 15, 6, 128};
-    if (const char *e = std::getenv("BIOT_TILE_CFG")) {   // "r,consumers,stages,maxreg"
-        int r = 0, nc = 0, st = 0, mr = 0;
-        if (std::sscanf(e, "%d,%d,%d,%d", &r, &nc, &st, &mr) == 4) c = TileCfg{r, nc, st, mr};
-    }
-    return c;
-}
-
-using TileFn = void (*)(const CUtensorMap, const Tile2dArgs);
-
-TileFn tile_fn(TileCfg c) {
-#define BIOT_TCFG(R_, NC_, ST_, MR_) \
-    if (c.r == R_ && c.nc == NC_ && c.stages == ST_ && c.maxreg == MR_) return tile2d_kernel<R_, NC_, ST_, MR_>;
-    BIOT_TCFG(2, 8, 6, 168)
-    BIOT_TCFG(1, 8, 6, 168)
-    BIOT_TCFG(1, 12, 6, 128)
-    BIOT_TCFG(1, 15, 6, 128)
-    BIOT_TCFG(1, 15, 7, 128)
-    BIOT_TCFG(1, 15, 6, 120)
-    BIOT_TCFG(1, 19, 5, 96)
-    BIOT_TCFG(1, 11, 6, 168)
-    BIOT_TCFG(2, 7, 6, 168)
-    BIOT_TCFG(2, 11, 5, 128)
-#undef BIOT_TCFG
-    return nullptr;
-}
-
-uint32_t stage_bytes(TileCfg c) {
-    const uint32_t seg = c.r * c.nc;
-    const uint32_t xb = (seg + 2) * 3 * kChp * 8;
-    const uint32_t off = (xb + 127) / 128 * 128;
-    return (off + seg * Tile2dArgs::kAux * 8 + 127) / 128 * 128;
 }
 
 }  // namespace
 
-int tile2d_seg() { return tile_cfg().nc * tile_cfg().r; }
+int tile2d_seg() { return kSeg; }
+int tile2d_chunk() { return kCT; }
+int tile2d_max_rows() { return kMaxRR; }
 
 int64_t tile2d_groups(const Tile2dArgs &a) {
-    const int64_t seg = tile2d_seg();
-    const int64_t n_seg = (a.row_w + seg - 1) / seg;
-    const int64_t n_jr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
-    return n_seg * n_jr;
+    const int64_t n_seg = (a.row_w + kSeg - 1) / kSeg;
+    const int64_t n_rr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
+    return n_seg * n_rr * kSeg;
 }
-
-int tile2d_chunk() { return kCh; }
 
 cudaError_t tile2d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    const TileCfg c = tile_cfg();
-    TileFn fn = tile_fn(c);
-    if (!fn) return cudaErrorInvalidValue;
-    const size_t smem = (size_t)c.stages * stage_bytes(c);
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    for (auto fn : {tile2d_kernel<false>, tile2d_kernel<true>}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
+        if (e != cudaSuccess) return e;
+    }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (c.nc + 1) * 32, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false>, (kSeg + 1) * 32, kSmemBytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     out->grid = sms * per_sm;
-    out->smem = smem;
+    out->smem = kSmemBytes;
     return cudaSuccess;
 }
 
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st) {
-    const TileCfg c = tile_cfg();
-    TileFn fn = tile_fn(c);
-    if (!fn) return cudaErrorInvalidValue;
-    fn<<<sh.grid, (c.nc + 1) * 32, sh.smem, st>>>(tmx, a);
+    if (a.rows_per_tile < 1 || a.rows_per_tile > kMaxRR) return cudaErrorInvalidValue;
+    const int64_t tiles = tile2d_groups(a) / kSeg;
+    const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
+    if (a.s0)
+        tile2d_kernel<true><<<grid, (kSeg + 1) * 32, sh.smem, st>>>(tmx, a);
+    else
+        tile2d_kernel<false><<<grid, (kSeg + 1) * 32, sh.smem, st>>>(tmx, a);
     return cudaGetLastError();
 }
 
-// box of the x tensor map: {time steps incl. halo, tensor rows}
+// box of the x tensor map: {time steps, tensor rows}
 void tile2d_box(uint32_t *box) {
-    box[0] = kChp;
-    box[1] = (uint32_t)((tile2d_seg() + 2) * 3);
+    box[0] = kCT;
+    box[1] = (uint32_t)(kStrip * 3);
 }
 
 }  // namespace biot
