@@ -101,6 +101,21 @@ class ClockSampler:
                 "samples": len(sms)}
 
 
+KERNELS = {1: "sweep_kernel<BDIA> (generic, fused residual + P~ + update + norms)",
+           2: "sweep_kernel<ELL> (generic, fused residual + P~ + update + norms)",
+           3: "stencil_kernel", 4: "march2d_kernel",
+           5: "tile2d_kernel (TMA row march, fused residual + P~ + update + norms)",
+           7: "tile3d_kernel (TMA plane march, fused residual + P~ + update + norms)"}
+
+
+def fp64_peak(sm_mhz):
+    """FP64 FMA peak: DFMA microbenchmark (tools/ubench/dfma.cu, profiles/r01_ubench_dfma.txt):
+    58.8 FMA/clk/SM sustained at 16-32 warps/SM x 4-8 chains; nominal 64."""
+    measured = 148 * 58.8 * 2 * sm_mhz * 1e6 / 1e12
+    nominal = 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+    return measured, nominal
+
+
 def load_traffic(cid):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
@@ -259,21 +274,26 @@ def main():
         algo_bytes = info.bytes_per_iter          # per launch of the sweep kernel (this rank)
         achieved_gbs = algo_bytes / (sweep_ms / 1e3) / 1e9
         sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
-        fp64_peak_tf = 148 * 64 * 2 * sm_max * 1e6 / 1e12   # 148 SMs x 64 DFMA/clk x 2 flop
+        fp64_meas_tf, fp64_nom_tf = fp64_peak(sm_max)
         achieved_tf = info.flops_per_iter / (sweep_ms / 1e3) / 1e12
         if prob.dim == 2:
             roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                     "frac": achieved_gbs / hbm, "traffic": load_traffic(args.config),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
-                    "fp64_tflops": achieved_tf, "fp64_peak_tflops_nominal": fp64_peak_tf}
+                    "fp64_tflops": achieved_tf, "fp64_peak_tflops_measured": fp64_meas_tf}
         else:
-            roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_peak_tf, "unit": "TFLOP/s",
-                    "frac": achieved_tf / fp64_peak_tf, "traffic": load_traffic(args.config),
-                    "peak_source": "148 SMs x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
+            roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_meas_tf, "unit": "TFLOP/s",
+                    "frac": achieved_tf / fp64_meas_tf, "traffic": load_traffic(args.config),
+                    "peak_source": "DFMA microbenchmark 58.8 FMA/clk/SM x 148 SMs x 2 x sm_max_mhz "
+                                   "(profiles/r01_ubench_dfma.txt); nominal 64 FMA/clk/SM = "
+                                   f"{fp64_nom_tf:.1f} TFLOP/s",
                     "hbm_gbs": achieved_gbs, "hbm_peak": hbm}
-        roof["kernel"] = "biot sweep_kernel (fused residual + P~ + update + norms)"
+        roof["kernel"] = KERNELS.get(info.kernel_path, f"kernel path {info.kernel_path}")
         roof["kernel_ms"] = sweep_ms
-        per_step = 2 if args.precond == 2 else 3
+        roof["algorithmic"] = {"bytes_per_launch": algo_bytes, "flops_per_launch": info.flops_per_iter,
+                               "per_unit": "16 B and 2*(nnz(AA)+nnz(A'))/n_dof flop per space-time DoF "
+                                           "update + operator values once (DESIGN.md roofline)"}
+        per_step = info.launches_per_iter
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define BIOT_PIT_ABI_VERSION 1
+#define BIOT_PIT_ABI_VERSION 2
 
 typedef struct biot_ctx biot_ctx;   /* opaque; owned by the library until biot_destroy */
 
@@ -117,12 +117,15 @@ typedef struct {
     int32_t kernel_path;             /* 1 = BDIA offsets, 2 = ELL explicit columns,
                                         3 = register-blocked structured stencil,
                                         4 = 2D row-march (L1-reuse) kernel,
-                                        5 = 2D TMA-pipelined tile kernel             */
+                                        5 = 2D TMA-pipelined tile kernel,
+                                        7 = 3D TMA-pipelined tile kernel             */
     int32_t n_slots;                 /* neighbour slots per node                        */
     double beta;                     /* the beta actually used                          */
     double bytes_per_iter;           /* algorithmic bytes per outer iteration (this rank) */
     double flops_per_iter;           /* algorithmic flops per outer iteration (this rank) */
     double device_bytes;             /* device memory held by the context               */
+    int32_t launches_per_iter;       /* kernels biot_iterate launches per outer iteration */
+    int32_t interior_nodes;          /* nodes on the shared interior stencil (tile kernels; 0 otherwise) */
 } biot_info;
 
 /* Build the operators on the host, upload, allocate the space-time panels

@@ -1160,6 +1160,9 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->bytes_per_iter = 16.0 * st + 8.0 * (double)(ctx->nnz_AA + ctx->nnz_AP);
     o->flops_per_iter = 2.0 * (double)(ctx->nnz_AA + ctx->nnz_AP) * ctx->n_tl;
     o->device_bytes = (double)ctx->device_bytes;
+    o->launches_per_iter = 1 + (ctx->precond == 1 ? 1 : 0) +
+                           (biot::finalize_scratch_doubles((int)ctx->groups, ctx->n_tl) > 0 ? 2 : 1);
+    o->interior_nodes = (int32_t)ctx->n_interior;
     return BIOT_OK;
 }
 

@@ -21,6 +21,8 @@ from paper_2310_10430_b200 import _lib, assemble_host, BiotSolver, BiotError
 from workloads import make_problem, config_problem
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(ROOT, "include", "biot_pit.h")
 
 
@@ -41,7 +43,19 @@ def test_exports_every_declared_symbol():
         assert n in exported, n
         getattr(L, n)
     assert set(_lib.EXPORTS) == set(names)
-    assert L.biot_abi_version() == 1
+    hdr = open(os.path.join(ROOT, "include", "biot_pit.h")).read()
+    assert L.biot_abi_version() == int(re.search(r"#define BIOT_PIT_ABI_VERSION (\d+)", hdr).group(1))
+
+
+def test_info_struct_matches_header():
+    """The ctypes mirror of biot_info has the header's field names in order."""
+    hdr = open(os.path.join(ROOT, "include", "biot_pit.h")).read()
+    body = hdr[hdr.index("/* Read-only facts about a context. */"):hdr.index("} biot_info;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    names = []
+    for decl in re.findall(r"(?:int32_t|int64_t|double)\s+([^;]+);", body):
+        names += [v.strip() for v in decl.split(",")]
+    assert [f[0] for f in _lib.BiotInfo._fields_] == names
 
 
 def test_no_torch_in_signatures_and_no_oracle_link():

@@ -1,0 +1,13 @@
+# Round profile set (run under gpurun): bench lines, launch lists and one ncu --set full
+# capture per dominant kernel; outputs in gpurun_out/ (copied to profiles/ afterwards).
+set -u
+mkdir -p gpurun_out
+timeout 600 python bench.py > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+timeout 300 python bench.py --config 4 --steps 20 --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err
+timeout 300 python bench.py --config 2 --steps 100 --no-cpu-baseline > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.err
+timeout 600 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c3.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_c3.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_c4.csv python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_launch_c4.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:tile2d -s 3 -c 1 -o gpurun_out/r01_tile2d_c3 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_full_c3.log 2>&1
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:tile3d -s 3 -c 1 -o gpurun_out/r01_tile3d_c4 python bench.py --config 4 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/ncu_full_c4.log 2>&1
+for f in gpurun_out/bench_c*.json; do echo $f; grep -o '"ms_per_step": [0-9.]*\|"frac": [0-9.]*\|"kernel_ms": [0-9.]*' $f | tr '\n' ' '; echo; done
