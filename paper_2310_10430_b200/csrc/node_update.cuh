@@ -27,21 +27,17 @@ __device__ __forceinline__ double cload(const double *p) {
     else return __ldg(p);
 }
 
-// Epilogue of one node over the lane's T steps (shared by every sweep kernel so the
-// arithmetic is identical): r = s_t f + q(t-1) - acc, norms, z = P^-1 r (P~2, or the
-// displacement half of P~1), x^{k+1} = x^k + omega z, stores.
+// Arithmetic of the epilogue of one node over T consecutive steps (shared by every
+// sweep kernel so the results are identical): r = s_t f + q(t-1) - acc, norms,
+// z = P^-1 r (P~2, or the displacement half of P~1), x^{k+1} = x^k + omega z.
 // MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
-template <int D, int T, class A, bool MASK = true>
-__device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
-                                              const double (&acc)[D + 1][T], const double (&q)[T],
+template <int D, int T, bool MASK>
+__device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[D + 1][T], const double (&q)[T],
                                               double qprev, const double (&F)[D + 1],
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
-                                              const double (&sv)[T], double (&nu)[T], double (&npn)[T]) {
+                                              const double (&sv)[T], double (&nu)[T], double (&npn)[T],
+                                              double (&outx)[D + 1][T], double (&outz)[D + 1][T]) {
     constexpr int NC = D + 1;
-    const int64_t P = a.pitch;
-    const int mode = a.mode;
-    const double omega = a.omega;
-    double outx[NC][T], outz[NC][T];
 #pragma unroll
     for (int tt = 0; tt < T; ++tt) {
         const double qp = (tt == 0) ? qprev : q[tt - 1];
@@ -70,6 +66,21 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
             outz[c][tt] = (c < D) ? z[c] : r[D];
         }
     }
+}
+
+// Epilogue of one node over the lane's T steps: the shared arithmetic, then the
+// stores (x^{k+1}, the P~1 Z panel, the send slice) by mode.
+template <int D, int T, class A, bool MASK = true>
+__device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
+                                              const double (&acc)[D + 1][T], const double (&q)[T],
+                                              double qprev, const double (&F)[D + 1],
+                                              const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
+                                              const double (&sv)[T], double (&nu)[T], double (&npn)[T]) {
+    constexpr int NC = D + 1;
+    const int64_t P = a.pitch;
+    const int mode = a.mode;
+    double outx[NC][T], outz[NC][T];
+    epilogue_math<D, T, MASK>(a.omega, acc, q, qprev, F, Dv, xs, sv, nu, npn, outx, outz);
     if (mode == MODE_RESIDUAL) return;
 
     const int n_tl = a.n_tl;

@@ -98,8 +98,8 @@ __device__ __forceinline__ void load_v(double (&v)[3][kT2], const double *row, i
 }
 
 // acc/q of one interior node through slot s by the gathered column v
-template <bool S0>
-__device__ __forceinline__ void fma_tmpl(double (&acc)[3][kT2], double (&q)[kT2], const Tile2dArgs &a, int s,
+template <bool S0, class A>
+__device__ __forceinline__ void fma_tmpl(double (&acc)[3][kT2], double (&q)[kT2], const A &a, int s,
                                          double pp, const double (&v)[3][kT2]) {
 #pragma unroll
     for (int cc = 0; cc < 3; ++cc) {
@@ -138,8 +138,8 @@ __device__ __forceinline__ void fma_cls(double (&acc)[3][kT2], double (&q)[kT2],
 }
 
 // slots of row delta DR for the warp's node (strip position p), in column order
-template <int DR, bool CLS, bool S0>
-__device__ __forceinline__ void accum_row(const Tile2dArgs &a, const double *row, int p, int lane,
+template <int DR, bool CLS, bool S0, class A>
+__device__ __forceinline__ void accum_row(const A &a, const double *row, int p, int lane,
                                           const double *aux, const double *T, double (&acc)[3][kT2],
                                           double (&q)[kT2]) {
 #pragma unroll
@@ -149,13 +149,13 @@ __device__ __forceinline__ void accum_row(const Tile2dArgs &a, const double *row
         double v[3][kT2];
         load_v(v, row, p + dc, lane);
         if constexpr (CLS) fma_cls(acc, q, T + s * kCW, aux[s], v);
-        else fma_tmpl<S0>(acc, q, a, s, aux[s], v);
+        else fma_tmpl<S0, A>(acc, q, a, s, aux[s], v);
     }
 }
 
 // q(t0-1) from the ghost x_{first-1} in the accumulation order (lane 0, chunk 0)
-template <bool CLS, bool S0>
-__device__ __forceinline__ double ghost_q(const Tile2dArgs &a, int64_t i, const double *T) {
+template <bool CLS, bool S0, class A>
+__device__ __forceinline__ double ghost_q(const A &a, int64_t i, const double *T) {
     double g = 0.0;
 #pragma unroll
     for (int dr = -1; dr <= 1; ++dr)
@@ -178,8 +178,8 @@ __device__ __forceinline__ double ghost_q(const Tile2dArgs &a, int64_t i, const 
     return g;
 }
 
-template <bool CLS, bool S0>
-__device__ __forceinline__ void start(const Tile2dArgs &a, const double *pd, const double *pm, int p, int lane,
+template <bool CLS, bool S0, class A>
+__device__ __forceinline__ void start(const A &a, const double *pd, const double *pm, int p, int lane,
                                       const double *aux, const double *T, double (&acc)[3][kT2],
                                       double (&q)[kT2]) {
 #pragma unroll
@@ -188,22 +188,24 @@ __device__ __forceinline__ void start(const Tile2dArgs &a, const double *pd, con
 #pragma unroll
         for (int c = 0; c < 3; ++c) acc[c][tt] = 0.0;
     }
-    accum_row<-1, CLS, S0>(a, pd, p, lane, aux, T, acc, q);
-    accum_row<0, CLS, S0>(a, pm, p, lane, aux, T, acc, q);
+    accum_row<-1, CLS, S0, A>(a, pd, p, lane, aux, T, acc, q);
+    accum_row<0, CLS, S0, A>(a, pm, p, lane, aux, T, acc, q);
 }
 
-// The epilogue runs on each half (2 consecutive steps) of the lane's steps.
-template <bool CLS, bool S0>
-__device__ __forceinline__ void finish(const Tile2dArgs &a, const double *po, const double *pu, int p, int lane,
+// The epilogue runs on each half (2 consecutive steps) of the lane's steps: the shared
+// arithmetic (dev::epilogue_math), then stores through one row pointer per node (the
+// mode is a compile-time parameter; `full`: the whole chunk lies inside the slab).
+template <bool CLS, bool S0, int MODE, class A>
+__device__ __forceinline__ void finish(const A &a, const double *po, const double *pu, int p, int lane,
                                        const double *aux, const double *T, int64_t i, int t0, bool ghost,
-                                       double *carry, const double (&sv)[kT2], double (&acc)[3][kT2],
-                                       double (&q)[kT2], double (&nu)[kT2], double (&npn)[kT2]) {
-    accum_row<1, CLS, S0>(a, pu, p, lane, aux, T, acc, q);
+                                       bool full, double *carry, double (&acc)[3][kT2], double (&q)[kT2],
+                                       double (&nu)[kT2], double (&npn)[kT2]) {
+    accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
     // q(t-1) of each half's first step: lane l-1's matching step; lane 0 of the second
     // half takes lane 31's first-half step 63, lane 0 of the first half the carry
     double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
     double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
-    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0>(a, i, T) : *carry;
+    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
     double F[3], Dv[3], xs[3][kT2];
@@ -213,13 +215,18 @@ __device__ __forceinline__ void finish(const Tile2dArgs &a, const double *po, co
         Dv[c] = aux[10 + c];
     }
     load_v(xs, po, p, lane);
+    const int64_t P = a.pitch;
+    const int n_tl = a.n_tl;
+    const int64_t row = i * 3 * P + t0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2];
+        double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2], outx[3][2], outz[3][2];
+        const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + t0 + h * (kCT / 2)));
+        sv2[0] = s2.x;
+        sv2[1] = s2.y;
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             q2[tt] = q[2 * h + tt];
-            sv2[tt] = sv[2 * h + tt];
             nu2[tt] = nu[2 * h + tt];
             np2[tt] = npn[2 * h + tt];
 #pragma unroll
@@ -228,12 +235,43 @@ __device__ __forceinline__ void finish(const Tile2dArgs &a, const double *po, co
                 xs2[c][tt] = xs[c][2 * h + tt];
             }
         }
-        node_epilogue<2, 2, Tile2dArgs, CLS>(a, i, t0 + h * (kCT / 2), acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2,
-                                             sv2, nu2, np2);
+        epilogue_math<2, 2, CLS>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2, sv2, nu2, np2, outx, outz);
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             nu[2 * h + tt] = nu2[tt];
             npn[2 * h + tt] = np2[tt];
+        }
+        if constexpr (MODE != MODE_RESIDUAL) {
+            constexpr int ncw = MODE == MODE_UPDATE_P2 ? 3 : 2;   // P~1: pressure written by pass 2
+            const int th = t0 + h * (kCT / 2);
+#pragma unroll
+            for (int c = 0; c < ncw; ++c) {
+                double *dst = a.xn + row + c * P + h * (kCT / 2);
+                if (full) {
+                    *reinterpret_cast<double2 *>(dst) = make_double2(outx[c][0], outx[c][1]);
+                } else {
+                    if (th < n_tl) dst[0] = outx[c][0];
+                    if (th + 1 < n_tl) dst[1] = outx[c][1];
+                }
+            }
+            if constexpr (MODE == MODE_P1_PASS1) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    double *dst = a.zbuf + row + c * P + h * (kCT / 2);
+                    if (full) {
+                        *reinterpret_cast<double2 *>(dst) = make_double2(outz[c][0], outz[c][1]);
+                    } else {
+                        if (th < n_tl) dst[0] = outz[c][0];
+                        if (th + 1 < n_tl) dst[1] = outz[c][1];
+                    }
+                }
+            }
+            if (a.sendbuf) {
+                const int tl = n_tl - 1 - th;
+                if (tl == 0 || tl == 1)
+#pragma unroll
+                    for (int c = 0; c < ncw; ++c) a.sendbuf[i * 3 + c] = tl == 0 ? outx[c][0] : outx[c][1];
+            }
         }
     }
 }
@@ -259,7 +297,7 @@ struct Geo2 {
 
 __device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); }
 
-template <bool S0>
+template <bool S0, int MODE>
 __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -317,13 +355,12 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
         for (int chunk = 0; chunk < g.nchunks; ++chunk) {
             const int t0 = chunk * kCT + lane * 2;   // the lane's first half; second half at t0 + 64
             const bool ghost = chunk == 0;
-            double nu[kT2], npn[kT2], sv[kT2];
+            const bool whole = (chunk + 1) * kCT <= a.n_tl;   // chunk inside the slab
+            double nu[kT2], npn[kT2];
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
                 nu[tt] = 0.0;
                 npn[tt] = 0.0;
-                const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
-                sv[tt] = (t < a.n_tl) ? a.s[t] : 0.0;
             }
             double acc[3][kT2], q[kT2];
             int kindP = 0;                       // pending node (row m-1): 0 none, 1 interior, 2 class
@@ -344,9 +381,9 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
                         const int64_t i = (int64_t)(m - 1) * g.W + col;
                         double *carry = qcarry + (m - 1 - ja) * kSeg + warp;
                         if (kindP == 1)
-                            finish<false, S0>(a, pd, pm, p, lane, aux, T, i, t0, ghost, carry, sv, acc, q, nu, npn);
+                            finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole, carry, acc, q, nu, npn);
                         else
-                            finish<true, S0>(a, pd, pm, p, lane, aux, T, i, t0, ghost, carry, sv, acc, q, nu, npn);
+                            finish<true, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole, carry, acc, q, nu, npn);
                     }
                     kindP = 0;
                     if (m < jb && valid) {       // start row m
@@ -354,10 +391,10 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
                                                 reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
                         kindP = aux[13] == 1.0 ? 1 : 2;
                         if (kindP == 1) {
-                            start<false, S0>(a, pd, pm, p, lane, aux, T, acc, q);
+                            start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                         } else {
                             T = cls_sm + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
-                            start<true, S0>(a, pd, pm, p, lane, aux, T, acc, q);
+                            start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                         }
                     }
                 }
@@ -398,12 +435,15 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    for (auto fn : {tile2d_kernel<false>, tile2d_kernel<true>}) {
+    for (auto fn : {tile2d_kernel<false, MODE_UPDATE_P2>, tile2d_kernel<true, MODE_UPDATE_P2>,
+                    tile2d_kernel<false, MODE_P1_PASS1>, tile2d_kernel<true, MODE_P1_PASS1>,
+                    tile2d_kernel<false, MODE_RESIDUAL>, tile2d_kernel<true, MODE_RESIDUAL>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false>, (kSeg + 1) * 32, kSmemBytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false, MODE_UPDATE_P2>, (kSeg + 1) * 32,
+                                                      kSmemBytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     out->grid = sms * per_sm;
@@ -416,10 +456,12 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
     if (a.rows_per_tile < 1 || a.rows_per_tile > kMaxRR) return cudaErrorInvalidValue;
     const int64_t tiles = tile2d_groups(a) / kSeg;
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
-    if (a.s0)
-        tile2d_kernel<true><<<grid, (kSeg + 1) * 32, sh.smem, st>>>(tmx, a);
-    else
-        tile2d_kernel<false><<<grid, (kSeg + 1) * 32, sh.smem, st>>>(tmx, a);
+    const dim3 block((kSeg + 1) * 32);
+#define BIOT_T2(S0_, M_) tile2d_kernel<S0_, M_><<<grid, block, sh.smem, st>>>(tmx, a)
+    if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2(true, MODE_UPDATE_P2); else BIOT_T2(false, MODE_UPDATE_P2); }
+    else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2(true, MODE_P1_PASS1); else BIOT_T2(false, MODE_P1_PASS1); }
+    else { if (a.s0) BIOT_T2(true, MODE_RESIDUAL); else BIOT_T2(false, MODE_RESIDUAL); }
+#undef BIOT_T2
     return cudaGetLastError();
 }
 
