@@ -199,7 +199,7 @@ __device__ __forceinline__ void ghost_q(const double *ghost, int64_t n1, int64_t
 
 // Finish the NN nodes of plane m-1 at step m: z+1 columns from plane m (pu), the
 // previous-step coupling, the epilogue with their own x and aux (plane m-1, po).
-template <int NN, bool CLS, bool S0>
+template <int NN, bool CLS, bool S0, int MODE>
 __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, const double *pu, const double *aux,
                                        int64_t iA, int sx, int sy, int lane, int t, bool ghost, double *carry,
                                        double sv, const double *TA, const double *TB, double (&acc)[2][4],
@@ -236,9 +236,26 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
             xs[c][0] = cp[c * kTc];
             acc1[c][0] = acc[n][c];
         }
-        node_epilogue<3, 1>(a, iA + n, t, acc1, q1, qp[n], F, Dv, xs, sv1, nu1, np1);
+        double outx[4][1], outz[4][1];
+        epilogue_math<3, 1, CLS>(a.omega, acc1, q1, qp[n], F, Dv, xs, sv1, nu1, np1, outx, outz);
         nu += nu1[0];
         npn += np1[0];
+        if constexpr (MODE != MODE_RESIDUAL) {   // stores through one row pointer per node
+            constexpr int ncw = MODE == MODE_UPDATE_P2 ? 4 : 3;   // P~1: pressure written by pass 2
+            if (t < a.n_tl) {
+                const int64_t P = a.pitch, row = (iA + n) * 4 * P + t;
+#pragma unroll
+                for (int c = 0; c < ncw; ++c) a.xn[row + c * P] = outx[c][0];
+                if constexpr (MODE == MODE_P1_PASS1) {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) a.zbuf[row + c * P] = outz[c][0];
+                }
+                if (a.sendbuf && t == a.n_tl - 1) {
+#pragma unroll
+                    for (int c = 0; c < ncw; ++c) a.sendbuf[(iA + n) * 4 + c] = outx[c][0];
+                }
+            }
+        }
     }
 }
 
@@ -283,16 +300,16 @@ __device__ __forceinline__ int group_kind(bool vA, bool vB, const double *aux) {
     return (aux[23] == 1.0 && (!vB || aux[kAuxRec + 23] == 1.0)) ? 1 : 2;
 }
 
-template <int NN, bool S0>
+template <int NN, bool S0, int MODE>
 __device__ __forceinline__ void finish_any(int kind, const Tile3dArgs &a, const double *po, const double *pu,
                                            const double *aux, int64_t iA, int sx, int sy, int lane, int t,
                                            bool ghost, double *carry, double sv, const double *TA,
                                            const double *TB, double (&acc)[2][4], double (&q)[2], double &nu,
                                            double &npn) {
     if (kind == 1)
-        finish<NN, false, S0>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
+        finish<NN, false, S0, MODE>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
     else if (a.dry != 2)
-        finish<NN, true, S0>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
+        finish<NN, true, S0, MODE>(a, po, pu, aux, iA, sx, sy, lane, t, ghost, carry, sv, TA, TB, acc, q, nu, npn);
 }
 
 template <int NN, bool S0>
@@ -305,7 +322,7 @@ __device__ __forceinline__ void start_any(int kind, const Tile3dArgs &a, const d
         start<NN, true, S0>(a, pd, pm, aux, sx, sy, lane, TA, TB, acc, q);
 }
 
-template <bool S0, int R>
+template <bool S0, int R, int MODE>
 __global__ void __maxnreg__(R == 2 ? 168 : 96)
     tile3d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile3dArgs a) {
     constexpr int kConsumers = kConsumersOf<R>, kStages = kStagesOf<R>;
@@ -398,10 +415,10 @@ __global__ void __maxnreg__(R == 2 ? 168 : 96)
                         const int64_t iA = ((int64_t)(m - 1) * g.n1 + y) * g.n1 + xA;
                         double *carry = qcarry + (m - 1 - za) * (kB * kB) + py * kB + px;
                         if (vB)
-                            finish_any<2, S0>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
+                            finish_any<2, S0, MODE>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
                                               TBp, acc, q, nu, npn);
                         else
-                            finish_any<1, S0>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
+                            finish_any<1, S0, MODE>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
                                               TBp, acc, q, nu, npn);
                     }
                     kindP = 0;
@@ -468,35 +485,27 @@ void tile3d_box(uint32_t *box) {
     box[3] = 1;
 }
 
-int tile3d_r() {
-    static const int r = [] {
-        const char *e = std::getenv("BIOT_TILE3D_R");   // dev knob: nodes per consumer warp
-        return (e && std::atoi(e) == 2) ? 2 : 1;
-    }();
-    return r;
-}
-
-template <int R>
-cudaError_t shape_r(int sms, LaunchShape *out) {
-    for (auto fn : {tile3d_kernel<false, R>, tile3d_kernel<true, R>}) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesOf<R>);
-        if (e != cudaSuccess) return e;
-    }
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile3d_kernel<false, R>,
-                                                                  (kConsumersOf<R> + 1) * 32, kSmemBytesOf<R>);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    out->grid = sms * per_sm;
-    out->smem = kSmemBytesOf<R>;
-    return cudaSuccess;
-}
+// One node per consumer warp (R = 1) is the configuration in use (see kConsumersOf).
+constexpr int kR = 1;
 
 cudaError_t tile3d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    return tile3d_r() == 1 ? shape_r<1>(sms, out) : shape_r<2>(sms, out);
+    for (auto fn : {tile3d_kernel<false, kR, MODE_UPDATE_P2>, tile3d_kernel<true, kR, MODE_UPDATE_P2>,
+                    tile3d_kernel<false, kR, MODE_P1_PASS1>, tile3d_kernel<true, kR, MODE_P1_PASS1>,
+                    tile3d_kernel<false, kR, MODE_RESIDUAL>, tile3d_kernel<true, kR, MODE_RESIDUAL>}) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesOf<kR>);
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile3d_kernel<false, kR, MODE_UPDATE_P2>,
+                                                      (kConsumersOf<kR> + 1) * 32, kSmemBytesOf<kR>);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    out->grid = sms * per_sm;
+    out->smem = kSmemBytesOf<kR>;
+    return cudaSuccess;
 }
 
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
@@ -504,15 +513,12 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
     if (a.z_rows < 1 || a.z_rows > kMaxZ || a.z_rows >= a.n1 || a.n1 < kB + 1) return cudaErrorInvalidValue;
     const int64_t tiles = tile3d_groups(a);
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
-    const int R = tile3d_r();
-    const int threads = (kB * kB / R + 1) * 32;
-    if (R == 1) {
-        if (a.s0) tile3d_kernel<true, 1><<<grid, threads, sh.smem, st>>>(tmx, a);
-        else tile3d_kernel<false, 1><<<grid, threads, sh.smem, st>>>(tmx, a);
-    } else {
-        if (a.s0) tile3d_kernel<true, 2><<<grid, threads, sh.smem, st>>>(tmx, a);
-        else tile3d_kernel<false, 2><<<grid, threads, sh.smem, st>>>(tmx, a);
-    }
+    const dim3 block((kConsumersOf<kR> + 1) * 32);
+#define BIOT_T3(S0_, M_) tile3d_kernel<S0_, kR, M_><<<grid, block, sh.smem, st>>>(tmx, a)
+    if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T3(true, MODE_UPDATE_P2); else BIOT_T3(false, MODE_UPDATE_P2); }
+    else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T3(true, MODE_P1_PASS1); else BIOT_T3(false, MODE_P1_PASS1); }
+    else { if (a.s0) BIOT_T3(true, MODE_RESIDUAL); else BIOT_T3(false, MODE_RESIDUAL); }
+#undef BIOT_T3
     return cudaGetLastError();
 }
 
