@@ -322,8 +322,14 @@ __device__ __forceinline__ void start_any(int kind, const Tile3dArgs &a, const d
         start<NN, true, S0>(a, pd, pm, aux, sx, sy, lane, TA, TB, acc, q);
 }
 
+// Block = the consumer warpgroups + one producer warpgroup (only its first lane issues
+// copies): the producer group hands its registers to the consumers (setmaxnreg), which
+// run at 112 registers instead of the 96 an even split of 20 warps would leave them.
+template <int R> constexpr int kThreadsOf = (kConsumersOf<R> + 4) * 32;
+constexpr int kProducerRegs = 24, kConsumerRegs = 112;
+
 template <bool S0, int R, int MODE>
-__global__ void __maxnreg__(R == 2 ? 168 : 96)
+__global__ void __launch_bounds__(kThreadsOf<R>, 1)
     tile3d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile3dArgs a) {
     constexpr int kConsumers = kConsumersOf<R>, kStages = kStagesOf<R>;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -344,9 +350,10 @@ __global__ void __maxnreg__(R == 2 ? 168 : 96)
     }
     __syncthreads();
 
-    if (warp == kConsumers) {
+    if (warp >= kConsumers) {
         // ------------------------------- producer -------------------------------
-        if (lane == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+        if (warp == kConsumers && lane == 0) {
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
                 int x0, y0, za, zb;
@@ -372,6 +379,7 @@ __global__ void __maxnreg__(R == 2 ? 168 : 96)
     }
 
     // ------------------------------- consumers ------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
     const int px = (warp % (kB / R)) * R, py = warp / (kB / R);
     const int sx = px + 1, sy = py + 1;
     uint32_t it = 0;
@@ -500,7 +508,7 @@ cudaError_t tile3d_shape(int device, LaunchShape *out) {
     }
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile3d_kernel<false, kR, MODE_UPDATE_P2>,
-                                                      (kConsumersOf<kR> + 1) * 32, kSmemBytesOf<kR>);
+                                                      kThreadsOf<kR>, kSmemBytesOf<kR>);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     out->grid = sms * per_sm;
@@ -513,7 +521,7 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
     if (a.z_rows < 1 || a.z_rows > kMaxZ || a.z_rows >= a.n1 || a.n1 < kB + 1) return cudaErrorInvalidValue;
     const int64_t tiles = tile3d_groups(a);
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
-    const dim3 block((kConsumersOf<kR> + 1) * 32);
+    const dim3 block(kThreadsOf<kR>);
 #define BIOT_T3(S0_, M_) tile3d_kernel<S0_, kR, M_><<<grid, block, sh.smem, st>>>(tmx, a)
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T3(true, MODE_UPDATE_P2); else BIOT_T3(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T3(true, MODE_P1_PASS1); else BIOT_T3(false, MODE_P1_PASS1); }
