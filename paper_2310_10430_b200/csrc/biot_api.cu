@@ -806,7 +806,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         tmp.row_w = ctx->row_w;
         tmp.n_rows = ctx->n_rows;
         tmp.rows_per_tile = ctx->rows_per_tile;
-        ctx->groups = biot::tile2d_groups(tmp);
+        ctx->groups = biot::tile2d_groups(tmp, ctx->shape.grid);
         // interior template + per-node aux records
         const int S = 7, WB = 10, KA = biot::Tile2dArgs::kAux;
         const int64_t tnode = (int64_t)(ctx->n_rows / 2) * ctx->row_w + ctx->row_w / 2;

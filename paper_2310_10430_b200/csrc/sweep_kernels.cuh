@@ -114,7 +114,8 @@ inline int64_t march_groups(const SweepArgs &a) {
 }
 
 // 2D TMA tile kernel: x boxes {time, rows} of the panel tensor map
-int64_t tile2d_groups(const Tile2dArgs &a);   // norm-partial groups: tiles x columns
+int64_t tile2d_tiles(const Tile2dArgs &a);
+int64_t tile2d_groups(const Tile2dArgs &a, int grid);   // norm-partial groups: CTAs x columns
 int tile2d_chunk();
 int tile2d_seg();         // grid columns per tile
 int tile2d_max_rows();    // rows per tile (q carry capacity)

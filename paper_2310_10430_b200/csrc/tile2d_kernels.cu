@@ -44,12 +44,12 @@ namespace {
 using namespace dev;
 using namespace tma;
 
-constexpr int kSeg = 15;                    // grid columns per tile = consumer warps
+constexpr int kSeg = 12;                    // grid columns per tile = consumer warps (3 warpgroups)
 constexpr int kStrip = kSeg + 2;            // + halo columns
 constexpr int kT2 = 4;                      // time steps per lane
 constexpr int kCT = 32 * kT2;               // time steps per chunk
-constexpr int kStages = 4;
-constexpr int kMaxRR = 48;                  // rows per tile (q carry capacity)
+constexpr int kStages = 5;
+constexpr int kMaxRR = 32;                  // rows per tile (q carry capacity)
 constexpr int kAuxRec = Tile2dArgs::kAux;   // doubles per aux record
 constexpr int kCW = Tile2dArgs::kClsW;      // doubles per class-stencil slot
 constexpr uint32_t kXBytes = kStrip * 3 * kCT * 8;                                 // 52224
@@ -297,8 +297,13 @@ struct Geo2 {
 
 __device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); }
 
+// Block = 3 consumer warpgroups + 1 producer warpgroup (only its first lane issues
+// copies); the producer group hands its registers to the consumers (setmaxnreg).
+constexpr int kThreads2 = (kSeg + 4) * 32;
+constexpr int kProducerRegs = 24, kConsumerRegs = 160;
+
 template <bool S0, int MODE>
-__global__ void __launch_bounds__((kSeg + 1) * 32, 1)
+__global__ void __launch_bounds__(kThreads2, 1)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
@@ -318,9 +323,10 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
     for (int k = threadIdx.x; k < 9 * 7 * kCW; k += blockDim.x) cls_sm[k] = a.cls[k];
     __syncthreads();
 
-    if (warp == kSeg) {
+    if (warp >= kSeg) {
         // ------------------------------- producer -------------------------------
-        if (lane == 0) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+        if (warp == kSeg && lane == 0) {
             uint32_t it = 0;
             for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
                 int i0, ja, jb;
@@ -344,6 +350,7 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
     }
 
     // ------------------------------- consumers ------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
     const int p = warp + 1;                   // strip position of the warp's column
     uint32_t it = 0;
     for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
@@ -405,14 +412,16 @@ __global__ void __launch_bounds__((kSeg + 1) * 32, 1)
             }
             if (lane == 0) mbar_arrive(&empty[sd]);       // row jb
             it += (uint32_t)(jb - ja + 2);
-            // per-step norm partials of this (tile, column, chunk), summed over the rows
+            // per-step norm partials of this (CTA, column), summed over the rows and, in
+            // the CTA's fixed tile order, over its tiles (the lane re-reads its own sums)
+            const bool first = tile == (int)blockIdx.x;
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
                 const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
                 if (t < a.n_tl) {
-                    double *dst = a.partial + (((int64_t)tile * kSeg + warp) * a.n_tl + t) * 2;
-                    dst[0] = nu[tt];
-                    dst[1] = npn[tt];
+                    double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
+                    dst[0] = first ? nu[tt] : dst[0] + nu[tt];
+                    dst[1] = first ? npn[tt] : dst[1] + npn[tt];
                 }
             }
         }
@@ -425,10 +434,15 @@ int tile2d_seg() { return kSeg; }
 int tile2d_chunk() { return kCT; }
 int tile2d_max_rows() { return kMaxRR; }
 
-int64_t tile2d_groups(const Tile2dArgs &a) {
+int64_t tile2d_tiles(const Tile2dArgs &a) {
     const int64_t n_seg = (a.row_w + kSeg - 1) / kSeg;
     const int64_t n_rr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
-    return n_seg * n_rr * kSeg;
+    return n_seg * n_rr;
+}
+
+int64_t tile2d_groups(const Tile2dArgs &a, int grid) {
+    const int64_t tiles = tile2d_tiles(a);
+    return (tiles < grid ? tiles : grid) * kSeg;
 }
 
 cudaError_t tile2d_shape(int device, LaunchShape *out) {
@@ -442,7 +456,7 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
         if (e != cudaSuccess) return e;
     }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false, MODE_UPDATE_P2>, (kSeg + 1) * 32,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false, MODE_UPDATE_P2>, kThreads2,
                                                       kSmemBytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -454,9 +468,9 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st) {
     if (a.rows_per_tile < 1 || a.rows_per_tile > kMaxRR) return cudaErrorInvalidValue;
-    const int64_t tiles = tile2d_groups(a) / kSeg;
-    const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
-    const dim3 block((kSeg + 1) * 32);
+    const int64_t tiles = tile2d_tiles(a);
+    const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);   // = tile2d_groups / kSeg
+    const dim3 block(kThreads2);
 #define BIOT_T2(S0_, M_) tile2d_kernel<S0_, M_><<<grid, block, sh.smem, st>>>(tmx, a)
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2(true, MODE_UPDATE_P2); else BIOT_T2(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2(true, MODE_P1_PASS1); else BIOT_T2(false, MODE_P1_PASS1); }
