@@ -51,8 +51,8 @@ constexpr int kTc = 32;                    // time steps per chunk (one per lane
 // config 4 5.23 vs 5.29 ms; R = 4 (4 warps) 8.5 ms, a 6x4 patch with R = 2 (12 warps,
 // 3 stages) 5.93 ms.  The kernel is latency-bound at IPC ~2.5.
 template <int R> constexpr int kConsumersOf = kB * kB / R;
-template <int R> constexpr int kStagesOf = R == 2 ? 5 : 4;
-constexpr int kMaxZ = 72;                  // planes per tile (q carry capacity)
+template <int R> constexpr int kStagesOf = 5;
+constexpr int kMaxZ = 24;                  // planes per tile (q carry capacity)
 constexpr int kCW = Tile3dArgs::kClsW;     // doubles per class-stencil slot
 constexpr int kClsD = 272;                 // doubles per class stencil in shared memory (15*18 padded)
 constexpr int kClsLocal = 8;               // classes a tile can touch: 2 (x) x 2 (y) x 2 (z; one z face per tile)
