@@ -156,7 +156,9 @@ biot_status biot_residual_history(biot_ctx *ctx, int64_t k, double *out);
 biot_status biot_solution(biot_ctx *ctx, int32_t n, int32_t count, double *out);
 
 /* Manual halo (BIOT_FLAG_MANUAL_HALO): copy the current iterate of the last
- * owned step out (host, n_dof), and set the ghost (step first_step-1) in. */
+ * owned step out (host, n_dof) -- for world > 1 after an iteration, the send
+ * buffer the sweep wrote, i.e. exactly what the NCCL exchange would send -- and
+ * set the ghost (step first_step-1) in. */
 biot_status biot_last_slice(biot_ctx *ctx, double *out);
 biot_status biot_set_ghost(biot_ctx *ctx, const double *x);
 

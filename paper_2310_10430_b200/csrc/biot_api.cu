@@ -509,6 +509,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
                              ctx->fin_scratch, ctx->stream));
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
+    if (ctx->world > 1) ctx->send_dirty = false;   // the sweep (and pass 2) wrote the slice of x^{k+1}
     return BIOT_OK;
 }
 
@@ -1128,6 +1129,16 @@ biot_status biot_solution(biot_ctx *ctx, int32_t n, int32_t count, double *out) 
 
 biot_status biot_last_slice(biot_ctx *ctx, double *out) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (ctx->world > 1 && !ctx->send_dirty) {
+        // the slice NCCL would send: the send buffer the sweep kernels wrote (so the
+        // manual-halo tests check exactly the data path of the NCCL exchange)
+        if (!out) return fail(ctx, BIOT_E_INVALID, "out is NULL");
+        CU(cudaSetDevice(ctx->device));
+        CU(cudaMemcpyAsync(out, ctx->sendbuf, (size_t)ctx->N * ctx->nc * sizeof(double), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return BIOT_OK;
+    }
     return biot_solution(ctx, ctx->first_step + ctx->n_tl - 1, 1, out);
 }
 

@@ -60,6 +60,9 @@ def test_time_slabs_bitwise(world, precond):
             g.iterate(1)
     xs = np.concatenate([g.solution() for g in ranks])
     assert np.array_equal(xs, xr)
+    # the send buffer written by the last sweep equals the last owned step
+    for g in ranks:
+        assert np.array_equal(g.last_slice(), g.solution(g.first_step + g.n_tl - 1, 1)[0])
     # norms agree to rounding (reduction grouping depends on the slab length)
     hs = np.concatenate([g.residual_history(K - 1) for g in ranks])
     assert np.allclose(hs, ref.residual_history(K - 1), rtol=1e-12, atol=0)
@@ -152,16 +155,20 @@ def test_tile3d_vs_generic(case, precond, monkeypatch):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-def test_tile3d_time_slabs_bitwise(world):
-    """Chunk 0 of each slab recomputes q(t0-1) from the ghost in the carry's FMA order."""
+@pytest.mark.parametrize("precond", [2, 1])
+def test_tile3d_time_slabs_bitwise(world, precond):
+    """Chunk 0 of each slab recomputes q(t0-1) from the ghost in the carry's FMA order; the
+    slices moved between the contexts are the send buffers the kernels wrote (the NCCL
+    data path)."""
     prob = make_problem(3, 7, 96, 0.01, 5, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0,
                         kappa_seed=3, x0_seed=9)
     nt, K = prob.n_t, 5
-    ref = _seeded(prob, nt, precond=2)
+    ref = _seeded(prob, nt, precond=precond)
     assert ref.info.kernel_path == 7
     ref.iterate(K)
     xr = ref.solution()
-    ranks = [_seeded(prob, nt, precond=2, rank=r, world=world, flags=FLAG_MANUAL_HALO) for r in range(world)]
+    ranks = [_seeded(prob, nt, precond=precond, rank=r, world=world, flags=FLAG_MANUAL_HALO)
+             for r in range(world)]
     for _ in range(K):
         slices = [g.last_slice() for g in ranks]
         for r in range(1, world):
