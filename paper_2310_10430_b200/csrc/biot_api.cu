@@ -141,6 +141,7 @@ struct biot_ctx {
     double *aux = nullptr;
     double tmpl[7][10] = {{0}};
     CUtensorMap tmap[2];
+    CUtensorMap tmapz;                // P~1 Z panel (tile kernels' second pass)
     int64_t n_interior = 0;
     int s0 = 0;                       // tile2d/tile3d zero-storage structural-zero variant
     // 6: TMA-pipelined 3D tile kernel
@@ -468,6 +469,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
         a.pad_nodes = c->pad;
         a.s0 = c->s0;
         a.dry = c->tile_dry;
+        if (mode == biot::MODE_PASS2) return biot::launch_tile2d(c->tmapz, a, c->shape, c->stream);
         return biot::launch_tile2d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     biot::SweepArgs a = sweep_args(c, mode, xin, xout);
@@ -486,7 +488,9 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     if (timing) CU(cudaEventRecord(e0, ctx->stream));
     CU(launch_main(ctx, mode, xin, xout));
     if (timing) CU(cudaEventRecord(e1, ctx->stream));
-    if (ctx->precond == 1) {
+    if (ctx->precond == 1 && ctx->kern == 4) {
+        CU(launch_main(ctx, biot::MODE_PASS2, xin, xout));     // tile second pass on the Z panel
+    } else if (ctx->precond == 1) {
         biot::Pass2Args p{};
         p.x = xin;
         p.xn = xout;
@@ -872,6 +876,13 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+            if (k == 0 && ctx->zbase) {
+                r = encode(&ctx->tmapz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, ctx->zbase, dims, strides, bx, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS)
+                    return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (Z) failed: " + std::to_string((int)r));
+            }
         }
     } else if (ctx->kern == 6) {
         CU(biot::tile3d_shape(ctx->device, &ctx->shape));

@@ -15,6 +15,7 @@ enum SweepMode : int {
     MODE_UPDATE_P2 = 0,   // fused residual + P~2 + update + norms
     MODE_P1_PASS1 = 1,    // residual, x_u update, Z = (z_u, r_p), norms
     MODE_RESIDUAL = 2,    // residual norms only (no writes)
+    MODE_PASS2 = 3,       // P~1 second pass (tile kernels): x_p += omega DSinv (B^T z_u - r_p)
 };
 
 struct SweepArgs {

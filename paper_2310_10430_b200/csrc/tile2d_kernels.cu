@@ -276,6 +276,71 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     }
 }
 
+// ---- P~1 second pass (PAPER.md eq. p1: z_p = S~p^{-1} (B^T z_u - r_p)) on the Z panel
+// staged like x: bt = (B^T z_u) over the slots in (row, column) order, interior
+// coefficients AA[p][u_cc] from the template (zeros skipped) or the class stencil.
+template <int DR, bool CLS, bool S0, class A>
+__device__ __forceinline__ void accum_row_bt(const A &a, const double *row, int p, int lane, const double *T,
+                                             double (&bt)[kT2]) {
+#pragma unroll
+    for (int dc = -1; dc <= 1; ++dc) {
+        const int s = slot2(DR, dc);
+        if (s < 0) continue;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            if constexpr (!CLS) {
+                if (tmpl_zero(s, 6 + cc, S0)) continue;
+            }
+            const double cf = CLS ? T[s * kCW + cc * 3 + 2] : a.tmpl[s][6 + cc];
+            const double *src = col2(row, p + dc, cc, lane);
+#pragma unroll
+            for (int h = 0; h < kT2; h += 2) {
+                const double2 w = *reinterpret_cast<const double2 *>(src + (h >> 1) * (kCT / 2));
+                bt[h] = fma(cf, w.x, bt[h]);
+                bt[h + 1] = fma(cf, w.y, bt[h + 1]);
+            }
+        }
+    }
+}
+
+template <bool CLS, bool S0, class A>
+__device__ __forceinline__ void start_bt(const A &a, const double *pd, const double *pm, int p, int lane,
+                                         const double *T, double (&bt)[kT2]) {
+#pragma unroll
+    for (int tt = 0; tt < kT2; ++tt) bt[tt] = 0.0;
+    accum_row_bt<-1, CLS, S0, A>(a, pd, p, lane, T, bt);
+    accum_row_bt<0, CLS, S0, A>(a, pm, p, lane, T, bt);
+}
+
+template <bool CLS, bool S0, class A>
+__device__ __forceinline__ void finish_bt(const A &a, const double *po, const double *pu, int p, int lane,
+                                          const double *aux, const double *T, int64_t i, int t0, bool whole,
+                                          double (&bt)[kT2]) {
+    accum_row_bt<1, CLS, S0, A>(a, pu, p, lane, T, bt);
+    const double dv = aux[12];
+    const int64_t P = a.pitch, row = i * 3 * P + 2 * P + t0;
+    const double *rp = col2(po, p, 2, lane);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const double2 r2 = *reinterpret_cast<const double2 *>(rp + h * (kCT / 2));
+        const double2 x2 = __ldg(reinterpret_cast<const double2 *>(a.x + row + h * (kCT / 2)));
+        const double v0 = fma(a.omega, dv * (bt[2 * h] - r2.x), x2.x);
+        const double v1 = fma(a.omega, dv * (bt[2 * h + 1] - r2.y), x2.y);
+        double *dst = a.xn + row + h * (kCT / 2);
+        const int th = t0 + h * (kCT / 2);
+        if (whole) {
+            *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+        } else {
+            if (th < a.n_tl) dst[0] = v0;
+            if (th + 1 < a.n_tl) dst[1] = v1;
+        }
+        if (a.sendbuf) {
+            if (th == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v0;
+            if (th + 1 == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v1;
+        }
+    }
+}
+
 struct Geo2 {
     int W, nrows, nseg, nrr, ntiles, nchunks, rr;
     __device__ explicit Geo2(const Tile2dArgs &a) {
@@ -387,21 +452,30 @@ __global__ void __launch_bounds__(kThreads2, 1)
                                                 reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
                         const int64_t i = (int64_t)(m - 1) * g.W + col;
                         double *carry = qcarry + (m - 1 - ja) * kSeg + warp;
-                        if (kindP == 1)
-                            finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole, carry, acc, q, nu, npn);
-                        else
-                            finish<true, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole, carry, acc, q, nu, npn);
+                        if constexpr (MODE == MODE_PASS2) {
+                            if (kindP == 1) finish_bt<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, whole, q);
+                            else finish_bt<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, whole, q);
+                        } else {
+                            if (kindP == 1)
+                                finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                                                    carry, acc, q, nu, npn);
+                            else
+                                finish<true, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                                                   carry, acc, q, nu, npn);
+                        }
                     }
                     kindP = 0;
                     if (m < jb && valid) {       // start row m
                         const double *aux = reinterpret_cast<const double *>(
                                                 reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
                         kindP = aux[13] == 1.0 ? 1 : 2;
-                        if (kindP == 1) {
-                            start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                        if (kindP == 2) T = cls_sm + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
+                        if constexpr (MODE == MODE_PASS2) {   // bt rides in q
+                            if (kindP == 1) start_bt<false, S0, Tile2dArgs>(a, pd, pm, p, lane, T, q);
+                            else start_bt<true, S0, Tile2dArgs>(a, pd, pm, p, lane, T, q);
                         } else {
-                            T = cls_sm + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
-                            start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                            if (kindP == 1) start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                            else start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                         }
                     }
                 }
@@ -417,6 +491,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const bool first = tile == (int)blockIdx.x;
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
+                if constexpr (MODE == MODE_PASS2) break;   // the norms come from pass 1
                 const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
                 if (t < a.n_tl) {
                     double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
@@ -451,7 +526,8 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     if (e != cudaSuccess) return e;
     for (auto fn : {tile2d_kernel<false, MODE_UPDATE_P2>, tile2d_kernel<true, MODE_UPDATE_P2>,
                     tile2d_kernel<false, MODE_P1_PASS1>, tile2d_kernel<true, MODE_P1_PASS1>,
-                    tile2d_kernel<false, MODE_RESIDUAL>, tile2d_kernel<true, MODE_RESIDUAL>}) {
+                    tile2d_kernel<false, MODE_RESIDUAL>, tile2d_kernel<true, MODE_RESIDUAL>,
+                    tile2d_kernel<false, MODE_PASS2>, tile2d_kernel<true, MODE_PASS2>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
@@ -474,6 +550,7 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
 #define BIOT_T2(S0_, M_) tile2d_kernel<S0_, M_><<<grid, block, sh.smem, st>>>(tmx, a)
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2(true, MODE_UPDATE_P2); else BIOT_T2(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2(true, MODE_P1_PASS1); else BIOT_T2(false, MODE_P1_PASS1); }
+    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2(true, MODE_PASS2); else BIOT_T2(false, MODE_PASS2); }
     else { if (a.s0) BIOT_T2(true, MODE_RESIDUAL); else BIOT_T2(false, MODE_RESIDUAL); }
 #undef BIOT_T2
     return cudaGetLastError();
