@@ -93,14 +93,20 @@ def terzaghi_uy(y, t, lam, mu, alpha, S, kappa, L=1.0, sigma0=1.0, terms=400):
     return (alpha * ip - sigma0 * y) / Mc
 
 
-def gauss_seidel_in_time(sysm, X, s, K, precond=2, omega=0.5):
-    """Algorithm 2 literally: b^{n,m} uses X^{n-1,m} of the current sweep."""
+def gauss_seidel_in_time(sysm, X, s, K, precond=2, omega=0.5, history=False):
+    """Algorithm 2 literally: b^{n,m} uses X^{n-1,m} of the current sweep.
+
+    history=True also returns the norms of the residual each update uses,
+    r = A' X^{n-1,m} + f^n - AA X^{n,m-1}, split (u, p) as in R12: [K, nt, 2].
+    """
     X = np.array(X, dtype=np.float64, copy=True)
     nt = X.shape[0] - 1
     nu = sysm.nu
-    for _ in range(K):
+    hist = np.zeros((K, nt, 2))
+    for m in range(K):
         for n in range(1, nt + 1):
             r = sysm.AP @ X[n - 1] + s[n - 1] * sysm.F - sysm.AA @ X[n]
+            hist[m, n - 1] = np.linalg.norm(r[:nu]), np.linalg.norm(r[nu:])
             z = np.empty_like(r)
             z[:nu] = sysm.DAinv * r[:nu]
             if precond == 2:
@@ -108,5 +114,5 @@ def gauss_seidel_in_time(sysm, X, s, K, precond=2, omega=0.5):
             else:
                 z[nu:] = sysm.DSinv * (sysm.BT @ z[:nu] - r[nu:])
             X[n] = X[n] + omega * z
-    return X
+    return (X, hist) if history else X
 

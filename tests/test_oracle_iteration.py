@@ -144,3 +144,54 @@ def test_terzaghi_column(storage):
     assert e16 < 0.07 and e32 < 0.04 and e64 < 0.022, (e16, e32, e64)
     assert e16 / e32 > 1.5 and e32 / e64 > 1.6          # first order in (h, tau)
     assert u64 < u16 and u64 < 0.01
+
+
+# ---- Gauss-Seidel in time (Algorithm 2 read literally) ----
+
+@pytest.mark.parametrize("dim,n,nt,K", [(2, 3, 6, 4000), (3, 1, 4, 3000)])
+@pytest.mark.parametrize("precond", [1, 2])
+def test_gs_fixed_point_is_backward_euler(dim, n, nt, K, precond):
+    """GS-in-time converges to the same sequential BE solution (direct solve)."""
+    prob = make_problem(dim, n, nt, 1.0 / nt, K, storage=1e-3, kappa_median=1e-2)
+    S = oracle.OracleSystem(prob)
+    s = load_scales(nt, parity=True)
+    X = extras.gauss_seidel_in_time(S, _rand_run(prob, S, nt), s, K, precond, 0.5)
+    Xbe = extras.sequential_be(S, np.zeros(S.ndof), s, nt)
+    assert np.abs(X - Xbe).max() / np.abs(Xbe).max() < 1e-11
+
+
+def test_gs_single_step_equals_jacobi_and_step_one_is_sequential():
+    """N_t = 1: GS and Jacobi are the same iteration (bitwise); step 1 of GS never sees a
+    changing predecessor, so after m sweeps it equals m Jacobi sweeps of step 1 alone."""
+    prob = make_problem(2, 4, 1, 0.1, 7, storage=1e-3, kappa_median=1e-2)
+    S = oracle.OracleSystem(prob)
+    s = load_scales(1, parity=True)
+    X0 = _rand_run(prob, S, 1)
+    for pc in (1, 2):
+        Xg, hg = extras.gauss_seidel_in_time(S, X0, s, 7, pc, 0.5, history=True)
+        Xj, hj = S.iterate(X0.copy(), s, 7, pc, 0.5)
+        assert np.array_equal(Xg, Xj)
+        assert np.allclose(hg, hj, rtol=1e-13, atol=0)
+    prob4 = make_problem(2, 4, 5, 0.1, 6, storage=1e-3, kappa_median=1e-2)
+    S4 = oracle.OracleSystem(prob4)
+    s4 = load_scales(5, parity=True)
+    X4 = _rand_run(prob4, S4, 5)
+    Xg = extras.gauss_seidel_in_time(S4, X4, s4, 6)
+    Xj, _ = S4.iterate(X4[:2].copy(), s4[:1], 6, 2, 0.5, history=False)
+    assert np.array_equal(Xg[1], Xj[1])
+
+
+def test_gs_causality_one_sweep_reaches_every_step():
+    """With no load (s = 0) and x^0 = 0 except step 1, one GS sweep carries the
+    perturbation to every later step (b^{n,m} uses X^{n-1,m}), one Jacobi sweep
+    only to step 2 (the information fronts of the two schemes)."""
+    prob = make_problem(2, 3, 6, 0.1, 1, storage=1e-3, kappa_median=1e-2)
+    S = oracle.OracleSystem(prob)
+    s = np.zeros(6)
+    X = np.zeros((7, S.ndof))
+    X[1] = S.to_paper(initial_iterate(prob.dirichlet, np.array([1]), 3))[0]
+    Xg = extras.gauss_seidel_in_time(S, X, s, 1)
+    Xj, _ = S.iterate(X.copy(), s, 1, 2, 0.5, history=False)
+    assert all(np.abs(Xg[n]).max() > 0 for n in range(1, 7))
+    assert np.abs(Xj[2]).max() > 0 and all(np.abs(Xj[n]).max() == 0 for n in range(3, 7))
+
