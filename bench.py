@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs"],
+                    help="jacobi: all steps at once (BASELINE metric); gs: Gauss-Seidel in time "
+                         "(PAPER.md Alg. 2 literal) as a wavefront, one GPU")
     return ap.parse_args()
 
 
@@ -149,7 +152,8 @@ def cpu_baseline(prob, precond, omega, budget_s=12.0, window=64):
 def workload_config(args, prob, world):
     from workloads import DESCRIPTIONS
     ws_gb = 2 * prob.n_dof * prob.n_t * 8 / 1e9
-    return {"workload": f"config{args.config}: {DESCRIPTIONS[args.config]}",
+    return {"workload": f"config{args.config}: {DESCRIPTIONS[args.config]}"
+                        + (", Gauss-Seidel in time (wavefront)" if args.method == "gs" else ""),
             "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
             "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
             "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
@@ -226,15 +230,16 @@ def main():
         if world > 1:
             dist.barrier()
 
+    step = g.iterate_gs if args.method == "gs" else g.iterate
     # warm-up (untimed)
-    g.iterate(max(args.warmup, 3))
+    step(max(args.warmup, 3))
     barrier()
     clk = ClockSampler(local)
     clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     ev0.record(stream)
-    g.iterate(args.steps)              # K outer iterations, one library call, no host sync inside
+    step(args.steps)                   # K outer iterations, one library call, no host sync inside
     ev1.record(stream)
     barrier()
     clocks = clk.stop()
@@ -259,7 +264,7 @@ def main():
     e0.record(stream)
     for _ in range(args.e2e_steps):
         g.set_load_scale(s_np)
-        g.iterate(1)
+        step(1)
         _lib.check(g.lib.biot_residual_history(g.ctx, g.get_info().iterations - 1, _lib.ptr(out_np)), g.ctx)
     e1.record(stream)
     barrier()
@@ -294,6 +299,9 @@ def main():
                                "per_unit": "16 B and 2*(nnz(AA)+nnz(A'))/n_dof flop per space-time DoF "
                                            "update + operator values once (DESIGN.md roofline)"}
         per_step = info.launches_per_iter
+        launches = per_step * args.steps
+        if args.method == "gs":   # n_t + K - 1 waves and two checkerboard copies per call
+            launches = 2 + (info.n_t_local + args.steps - 1) * per_step
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -302,7 +310,7 @@ def main():
                         "d2h_bytes_per_step": int(16 * info.n_t_local),
                         "what": "per step: biot_set_load_scale (host s_n) + biot_iterate(1) + "
                                 "biot_residual_history readback, host sync each step"},
-                "gpu_launches": per_step * args.steps,
+                "gpu_launches": launches,
                 "clocks": clocks}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(prob, args.precond, args.omega)

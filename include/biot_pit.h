@@ -143,6 +143,13 @@ biot_status biot_set_load_scale(biot_ctx *ctx, const double *s);
 /* K outer iterations (K >= 0; K = 0 is a no-op).  Collective for world > 1. */
 biot_status biot_iterate(biot_ctx *ctx, int32_t K);
 
+/* K Gauss-Seidel-in-time sweeps (Algorithm 2 literally: the right-hand side
+ * of step n uses the CURRENT sweep's X^{n-1}), run as a pipelined wavefront of
+ * n_t_local + K - 1 windows.  Same preconditioner and omega as biot_iterate; the
+ * residual history records, for sweep k and step n, the residual that update used.
+ * Needs a structured 2D mesh (tile kernel) and world == 1, else BIOT_E_STATE. */
+biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
+
 /* Residual norms at the current iterate: out[n_t_local][2] = ||r_u||, ||r_p||
  * of the owned steps (a residual-only pass, no update). */
 biot_status biot_residual_norms(biot_ctx *ctx, double *out);

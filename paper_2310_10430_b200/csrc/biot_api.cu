@@ -90,6 +90,20 @@ __global__ void gather_steps_kernel(const double *__restrict__ panel, double *__
     }
 }
 
+// Copy the odd (parity = 1) or even (parity = 0) time columns of the first n_tl steps
+// of every panel row: the Gauss-Seidel wavefront keeps step t of sweep u in panel
+// (u + t) % 2 (see biot_iterate_gs).
+__global__ void copy_parity_columns_kernel(const double *__restrict__ src, double *__restrict__ dst,
+                                           int64_t nrows, int64_t pitch, int n_tl, int parity) {
+    const int64_t half = (n_tl - parity + 1) / 2;
+    const int64_t total = nrows * half;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < total;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = k / half, t = 2 * (k % half) + parity;
+        dst[row * pitch + t] = src[row * pitch + t];
+    }
+}
+
 }  // namespace
 
 struct biot_ctx {
@@ -443,7 +457,15 @@ biot::StencilArgs stencil_args(biot_ctx *c, int mode, const double *xin, double 
     return a;
 }
 
-cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) {
+// A time window of the panel (Gauss-Seidel waves): steps [t_off, t_off + len), the
+// predecessor of step t_off read from `ghost` with stride `stride`.
+struct Window {
+    int t_off = 0, len = 0, t_lo = 0;   // t_lo: window steps below it are not stored (alignment)
+    const double *ghost = nullptr;
+    int64_t stride = 1;
+};
+
+cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, const Window *win = nullptr) {
     if (c->kern == 2) {
         biot::StencilArgs a = stencil_args(c, mode, xin, xout);
         return biot::launch_stencil(c->d, c->sR, c->sT, a, c->shape, c->stream);
@@ -467,6 +489,16 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout) 
         a.aux = c->aux;
         a.cls = c->cls;
         a.pad_nodes = c->pad;
+        a.ghost_stride = 1;
+        a.t_off = 0;
+        a.t_lo = 0;
+        if (win) {
+            a.t_off = win->t_off;
+            a.t_lo = win->t_lo;
+            a.n_tl = win->len;
+            a.ghost = win->ghost;
+            a.ghost_stride = win->stride;
+        }
         a.s0 = c->s0;
         a.dry = c->tile_dry;
         if (mode == biot::MODE_PASS2) return biot::launch_tile2d(c->tmapz, a, c->shape, c->stream);
@@ -767,7 +799,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ALLOC(ctx->fixed, (size_t)ctx->N * nc);
     CU(h2d(ctx, ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc));
     {
-        std::vector<double> sl(ctx->pitch, 0.0);
+        std::vector<double> sl(ctx->pitch + 128, 0.0);   // zero past n_tl (window reads may overrun)
         for (int32_t t = 0; t < ctx->n_tl; ++t)
             sl[t] = bc->load_scale ? bc->load_scale[ctx->first_step - 1 + t] : 1.0;
         ALLOC(ctx->s, sl.size() * sizeof(double));
@@ -1077,6 +1109,67 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
     }
     ctx->last_ms_iter = tot / K;
     ctx->last_ms_sweep = sweep_ms / K;
+    int nf = 0;
+    CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (nf) return fail(ctx, BIOT_E_NONFINITE, "a residual norm became non-finite");
+    return BIOT_OK;
+}
+
+// Gauss-Seidel in time (Alg. 2 read literally: b^{n,m} =
+// A' X^{n-1,m} + f^n), pipelined as a wavefront: sweep u of step t runs in wave
+// w = t + u - 1 and needs only wave w-1 (X^{t,u-1} and X^{t-1,u}), so wave w updates
+// the window of steps max(0, w-K+1)..min(n_tl-1, w) at once.  Wave w reads panel
+// (cur + w) % 2 and writes the other, so step t's iterate of sweep u lives in panel
+// (cur + t + u) % 2: the odd columns are moved before and after (checkerboard).
+biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
+    if (ctx->kern != 4)
+        return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs the 2D tile kernel (structured 2D mesh)");
+    if (ctx->world != 1)
+        return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time runs on one time slab in this version");
+    if (K == 0) return BIOT_OK;
+    CU(cudaSetDevice(ctx->device));
+    const int64_t rows = ctx->N * ctx->nc;
+    const int nt = ctx->n_tl;
+    auto parity_copy = [&](const double *src, double *dst) {
+        copy_parity_columns_kernel<<<1184, 256, 0, ctx->stream>>>(src, dst, rows, ctx->pitch, nt, 1);
+        return cudaGetLastError();
+    };
+    CU(cudaEventRecord(ctx->ev_a, ctx->stream));
+    CU(parity_copy(ctx->x[ctx->cur], ctx->x[1 - ctx->cur]));
+    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+    const int64_t k0 = ctx->iterations;
+    for (int w = 0; w <= nt + K - 2; ++w) {
+        const int lo = std::max(0, w - K + 1), hi = std::min(nt - 1, w);
+        const int r = (ctx->cur + w) % 2;
+        Window win;
+        win.t_off = lo & ~1;                 // 16-B aligned columns; step lo-1 (if any) is not stored
+        win.t_lo = lo - win.t_off;
+        win.len = hi - win.t_off + 1;
+        if (win.t_off == 0) {
+            win.ghost = ctx->ghost;
+            win.stride = 1;
+        } else {
+            win.ghost = ctx->x[r] + (win.t_off - 1);
+            win.stride = ctx->pitch;
+        }
+        CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
+        if (ctx->precond == 1) CU(launch_main(ctx, biot::MODE_PASS2, ctx->x[r], ctx->x[1 - r], &win));
+        CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, k0 + w, ctx->hist_cap,
+                                      nt, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
+    }
+    ctx->cur = (ctx->cur + K) % 2;
+    CU(parity_copy(ctx->x[1 - ctx->cur], ctx->x[ctx->cur]));
+    CU(cudaEventRecord(ctx->ev_b, ctx->stream));
+    CU(cudaEventSynchronize(ctx->ev_b));
+    float tot = 0.f;
+    CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
+    ctx->last_ms_iter = tot / K;
+    ctx->last_ms_sweep = tot / K;
+    ctx->iterations += K;
+    ctx->send_dirty = true;
     int nf = 0;
     CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

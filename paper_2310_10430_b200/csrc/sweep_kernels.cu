@@ -186,6 +186,41 @@ __global__ void finalize_stage1_kernel(const double *__restrict__ partial, int g
     }
 }
 
+// Second stage for a Gauss-Seidel wave: fixed-order sum as finalize_kernel, written to
+// the history slot of each step's iteration.
+__global__ void finalize_wave_kernel(const double *__restrict__ partial, int groups, int len, int lo, int t_first,
+                                     int64_t k0, int cap, int n_tl, double *__restrict__ hist, int *nonfinite) {
+    __shared__ double sm[8][32][2];
+    const int t = blockIdx.x * 32 + threadIdx.x;
+    const int y = threadIdx.y;
+    double su = 0.0, sp = 0.0;
+    if (t < len) {
+        for (int g = y; g < groups; g += 8) {
+            su += partial[((int64_t)g * len + t) * 2 + 0];
+            sp += partial[((int64_t)g * len + t) * 2 + 1];
+        }
+    }
+    sm[y][threadIdx.x][0] = su;
+    sm[y][threadIdx.x][1] = sp;
+    __syncthreads();
+    if (y == 0 && t < len) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            a += sm[k][threadIdx.x][0];
+            b += sm[k][threadIdx.x][1];
+        }
+        a = sqrt(a);
+        b = sqrt(b);
+        const int tg = lo + t;
+        if (tg >= t_first) {   // steps below t_first were computed for alignment only
+            double *o = hist + (((k0 - tg) % cap) * (int64_t)n_tl + tg) * 2;   // [slot][t][2]
+            o[0] = a;
+            o[1] = b;
+            if (!isfinite(a) || !isfinite(b)) atomicOr(nonfinite, 1);
+        }
+    }
+}
+
 using SweepFn = void (*)(const SweepArgs);
 using Pass2Fn = void (*)(const Pass2Args);
 
@@ -245,6 +280,20 @@ cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int
     Pass2Fn pf;
     if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
     pf<<<grid, kThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int lo, int t_first, int64_t k0,
+                                 int cap, int n_tl, double *hist, int *nonfinite, double *scratch, cudaStream_t st) {
+    dim3 block(32, 8);
+    if (groups > 2 * kGch) {
+        const int g1 = (groups + kGch - 1) / kGch;
+        finalize_stage1_kernel<<<dim3((len + 31) / 32, g1), block, 0, st>>>(partial, groups, len, scratch);
+        partial = scratch;
+        groups = g1;
+    }
+    finalize_wave_kernel<<<dim3((len + 31) / 32), block, 0, st>>>(partial, groups, len, lo, t_first, k0, cap, n_tl,
+                                                                  hist, nonfinite);
     return cudaGetLastError();
 }
 

@@ -74,6 +74,9 @@ struct Tile2dArgs : SweepArgs {
     const double *cls;                // geometric-class stencils [9][7][kClsW], column-major blocks
     static constexpr int kClsW = 10;  // 9 AA entries + A'_pp
     int64_t pad_nodes;                // panel rows start at node -pad_nodes
+    int64_t ghost_stride;             // doubles between ghost entries (1: a vector; pitch: a panel column)
+    int32_t t_off;                    // first panel column of the time window (Gauss-Seidel waves; even)
+    int32_t t_lo;                     // window steps below t_lo are computed but not stored or counted
     int32_t s0;                       // zero-storage variant: extra structural zeros (see tile2d)
     int32_t dry;                      // dev/measurement only: stream the ring without computing
 };
@@ -144,5 +147,9 @@ cudaError_t launch_stencil(int dim, int R, int T, const StencilArgs &a, const La
 int64_t finalize_scratch_doubles(int groups, int n_tl);
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
                             int *nonfinite, double *scratch, cudaStream_t st);
+// Gauss-Seidel wave: the window's steps t = lo..lo+len-1 carry iteration k = k0 - t;
+// norms of t >= t_first go to hist[(k % cap) * n_tl + t] (the residual-history ring)
+cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int lo, int t_first, int64_t k0,
+                                 int cap, int n_tl, double *hist, int *nonfinite, double *scratch, cudaStream_t st);
 
 }  // namespace biot

@@ -166,7 +166,7 @@ __device__ __forceinline__ double ghost_q(const A &a, int64_t i, const double *T
             const int64_t j = i + a.off[s];
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {
-                const double xv = __ldg(a.ghost + j * 3 + cc);
+                const double xv = __ldg(a.ghost + (j * 3 + cc) * a.ghost_stride);
                 if constexpr (CLS) {
                     g = fma(cc < 2 ? T[s * kCW + cc * 3 + 2] : T[s * kCW + 9], xv, g);
                 } else {
@@ -217,11 +217,11 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     load_v(xs, po, p, lane);
     const int64_t P = a.pitch;
     const int n_tl = a.n_tl;
-    const int64_t row = i * 3 * P + t0;
+    const int64_t row = i * 3 * P + a.t_off + t0;   // t0: step within the window
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2], outx[3][2], outz[3][2];
-        const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + t0 + h * (kCT / 2)));
+        const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
         sv2[0] = s2.x;
         sv2[1] = s2.y;
 #pragma unroll
@@ -244,14 +244,15 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
         if constexpr (MODE != MODE_RESIDUAL) {
             constexpr int ncw = MODE == MODE_UPDATE_P2 ? 3 : 2;   // P~1: pressure written by pass 2
             const int th = t0 + h * (kCT / 2);
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
 #pragma unroll
             for (int c = 0; c < ncw; ++c) {
                 double *dst = a.xn + row + c * P + h * (kCT / 2);
                 if (full) {
                     *reinterpret_cast<double2 *>(dst) = make_double2(outx[c][0], outx[c][1]);
                 } else {
-                    if (th < n_tl) dst[0] = outx[c][0];
-                    if (th + 1 < n_tl) dst[1] = outx[c][1];
+                    if (st0) dst[0] = outx[c][0];
+                    if (st1) dst[1] = outx[c][1];
                 }
             }
             if constexpr (MODE == MODE_P1_PASS1) {
@@ -261,8 +262,8 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
                     if (full) {
                         *reinterpret_cast<double2 *>(dst) = make_double2(outz[c][0], outz[c][1]);
                     } else {
-                        if (th < n_tl) dst[0] = outz[c][0];
-                        if (th + 1 < n_tl) dst[1] = outz[c][1];
+                        if (st0) dst[0] = outz[c][0];
+                        if (st1) dst[1] = outz[c][1];
                     }
                 }
             }
@@ -318,7 +319,7 @@ __device__ __forceinline__ void finish_bt(const A &a, const double *po, const do
                                           double (&bt)[kT2]) {
     accum_row_bt<1, CLS, S0, A>(a, pu, p, lane, T, bt);
     const double dv = aux[12];
-    const int64_t P = a.pitch, row = i * 3 * P + 2 * P + t0;
+    const int64_t P = a.pitch, row = i * 3 * P + 2 * P + a.t_off + t0;
     const double *rp = col2(po, p, 2, lane);
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
@@ -331,7 +332,7 @@ __device__ __forceinline__ void finish_bt(const A &a, const double *po, const do
         if (whole) {
             *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
         } else {
-            if (th < a.n_tl) dst[0] = v0;
+            if (th < a.n_tl && th >= a.t_lo) dst[0] = v0;
             if (th + 1 < a.n_tl) dst[1] = v1;
         }
         if (a.sendbuf) {
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const bool real = (r >= 0 && r < g.nrows);
                         mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
                         const int64_t node0 = (int64_t)r * g.W + i0 - 1;
-                        load_2d(base, &tmx, chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
+                        load_2d(base, &tmx, a.t_off + chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
                         if (real)
                             bulk_g2s(base + kXBytes, a.aux + ((int64_t)r * g.W + i0) * kAuxRec, kAuxBytes,
                                      &full[st]);
@@ -427,7 +428,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         for (int chunk = 0; chunk < g.nchunks; ++chunk) {
             const int t0 = chunk * kCT + lane * 2;   // the lane's first half; second half at t0 + 64
             const bool ghost = chunk == 0;
-            const bool whole = (chunk + 1) * kCT <= a.n_tl;   // chunk inside the slab
+            const bool whole = (chunk + 1) * kCT <= a.n_tl && (chunk > 0 || a.t_lo == 0);   // chunk inside the window
             double nu[kT2], npn[kT2];
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
@@ -495,8 +496,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
                 if (t < a.n_tl) {
                     double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
-                    dst[0] = first ? nu[tt] : dst[0] + nu[tt];
-                    dst[1] = first ? npn[tt] : dst[1] + npn[tt];
+                    const double u = t >= a.t_lo ? nu[tt] : 0.0, v = t >= a.t_lo ? npn[tt] : 0.0;
+                    dst[0] = first ? u : dst[0] + u;
+                    dst[1] = first ? v : dst[1] + v;
                 }
             }
         }

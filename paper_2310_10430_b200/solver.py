@@ -75,6 +75,9 @@ class BiotSolver:
         assert s.shape == (self.n_t,)
         check(self.lib.biot_set_load_scale(self.ctx, ptr(s)), self.ctx)
 
+    def iterate_gs(self, K):
+        check(self.lib.biot_iterate_gs(self.ctx, K), self.ctx)
+
     def iterate(self, K):
         check(self.lib.biot_iterate(self.ctx, int(K)), self.ctx)
 

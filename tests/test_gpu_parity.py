@@ -181,3 +181,80 @@ def test_parity_ragged_and_small(dim):
         (xg, hg, rg), (xo, ho, ro) = _run_full(prob, 7, 2, 0.5)
         assert field_errors(xg, xo, dim).max() < TOL, nt
         assert norm_errors(hg, ho).max() < TOL, nt
+
+
+# ---- Gauss-Seidel in time (Alg. 2 literal) ----
+
+def _gs_pair(prob, nt, K, precond, omega):
+    from oracle import extras
+    s = load_scales(nt, parity=True)
+    x0 = _x0(prob, np.arange(1, nt + 1))
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega, load_scale=s)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate_gs(K)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(k) for k in range(K)])
+    finally:
+        g.close()
+    S = oracle.OracleSystem(prob)
+    X = np.zeros((nt + 1, S.ndof))
+    X[1:] = S.to_paper(x0)
+    Xo, ho = extras.gauss_seidel_in_time(S, X, s, K, precond, omega, history=True)
+    return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho)
+
+
+@pytest.mark.parametrize("precond,omega", [(2, 0.5), (1, 0.3)])
+@pytest.mark.parametrize("nt,K", [(32, 6), (5, 9), (40, 40)])
+def test_gs_parity_config1(precond, omega, nt, K):
+    """Wavefront GS on the GPU vs the oracle's literal Algorithm 2: x^K and the residual
+    of every (sweep, step) update; windows shorter and longer than K, N_t < K."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gs_pair(prob, nt, K, precond, omega)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_gs_parity_config2_windows_span_chunks():
+    """N_t = 256 with the lognormal-kappa 128^2 mesh: every wave runs the full tile grid."""
+    prob = config_problem(2)
+    (xg, hg), (xo, ho) = _gs_pair(prob, 256, 3, 2, 0.5)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_gs_additive_and_converges_faster():
+    """iterate_gs(a); iterate_gs(b) == iterate_gs(a + b) bitwise; after the same number of
+    sweeps GS is closer to the backward-Euler solution than Jacobi (config 1)."""
+    prob = config_problem(1)
+    nt = prob.n_t
+    s = load_scales(nt, parity=True)
+    x0 = _x0(prob, np.arange(1, nt + 1))
+    res = []
+    for split in ((3, 4), (7,)):
+        g = BiotSolver(prob, precond=2, omega=0.5, load_scale=s)
+        g.set_iterate(1, x0)
+        for k in split:
+            g.iterate_gs(k)
+        res.append((g.solution(), [g.residual_history(k) for k in range(7)]))
+        g.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][1], res[1][1]))
+    gj = BiotSolver(prob, precond=2, omega=0.5, load_scale=s)
+    gj.set_iterate(1, x0)
+    gj.iterate(7)
+    gg = BiotSolver(prob, precond=2, omega=0.5, load_scale=s)
+    gg.set_iterate(1, x0)
+    gg.iterate_gs(7)
+    assert (np.sqrt((gg.residual_norms() ** 2).sum()) < np.sqrt((gj.residual_norms() ** 2).sum()))
+    gj.close()
+    gg.close()
+
+
+def test_gs_parity_long_windows():
+    """K = 150 sweeps over N_t = 200: waves up to 150 steps wide run two 128-step chunks,
+    the second taking q(t0-1) from the carry of the first."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gs_pair(prob, 200, 150, 2, 0.5)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
