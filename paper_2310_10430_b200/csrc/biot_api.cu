@@ -480,6 +480,16 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         a.z_rows = c->z_rows;
         a.s0 = c->s0;
         a.dry = c->tile_dry;
+        a.ghost_stride = 1;
+        a.t_off = 0;
+        a.t_lo = 0;
+        if (win) {
+            a.t_off = win->t_off;
+            a.t_lo = win->t_lo;
+            a.n_tl = win->len;
+            a.ghost = win->ghost;
+            a.ghost_stride = win->stride;
+        }
         return biot::launch_tile3d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     if (c->kern == 4) {
@@ -509,6 +519,29 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
     return biot::launch_sweep(c->d, c->path, c->S, a, c->shape, c->stream);
 }
 
+// P~1 second pass: the 2D tile mode on the Z panel, else the generic kernel.
+cudaError_t launch_pass2_any(biot_ctx *ctx, const double *xin, double *xout, double *sendbuf, const Window *win) {
+    if (ctx->kern == 4) return launch_main(ctx, biot::MODE_PASS2, xin, xout, win);
+    biot::Pass2Args p{};
+    p.x = xin;
+    p.xn = xout;
+    p.zbuf = ctx->z;
+    p.blk = ctx->blk;
+    p.cols = ctx->cols;
+    p.dinv = ctx->dinv;
+    p.sendbuf = sendbuf;
+    p.n_nodes = ctx->N;
+    p.pitch = ctx->pitch;
+    p.n_tl = win ? win->len : ctx->n_tl;
+    p.t_off = win ? win->t_off : 0;
+    p.t_lo = win ? win->t_lo : 0;
+    p.tw = ctx->tw;
+    p.node_block = ctx->node_block;
+    p.omega = ctx->omega;
+    for (int s = 0; s < 32; ++s) p.off[s] = s < (int)ctx->offsets.size() ? ctx->offsets[s] : 0;
+    return biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream);
+}
+
 biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     const bool timing = e0 != nullptr;
     biot_status st = halo_exchange(ctx);
@@ -520,26 +553,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     if (timing) CU(cudaEventRecord(e0, ctx->stream));
     CU(launch_main(ctx, mode, xin, xout));
     if (timing) CU(cudaEventRecord(e1, ctx->stream));
-    if (ctx->precond == 1 && ctx->kern == 4) {
-        CU(launch_main(ctx, biot::MODE_PASS2, xin, xout));     // tile second pass on the Z panel
-    } else if (ctx->precond == 1) {
-        biot::Pass2Args p{};
-        p.x = xin;
-        p.xn = xout;
-        p.zbuf = ctx->z;
-        p.blk = ctx->blk;
-        p.cols = ctx->cols;
-        p.dinv = ctx->dinv;
-        p.sendbuf = a.sendbuf;
-        p.n_nodes = ctx->N;
-        p.pitch = ctx->pitch;
-        p.n_tl = ctx->n_tl;
-        p.tw = ctx->tw;
-        p.node_block = ctx->node_block;
-        p.omega = ctx->omega;
-        for (int s = 0; s < 32; ++s) p.off[s] = a.off[s];
-        CU(biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream));
-    }
+    if (ctx->precond == 1) CU(launch_pass2_any(ctx, xin, xout, a.sendbuf, nullptr));
     double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
     CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
                              ctx->fin_scratch, ctx->stream));
@@ -1125,8 +1139,8 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
 biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
-    if (ctx->kern != 4)
-        return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs the 2D tile kernel (structured 2D mesh)");
+    if (ctx->kern != 4 && ctx->kern != 6)
+        return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs a tile kernel (structured 2D / 3D mesh)");
     if (ctx->world != 1)
         return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time runs on one time slab in this version");
     if (K == 0) return BIOT_OK;
@@ -1156,7 +1170,7 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
             win.stride = ctx->pitch;
         }
         CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
-        if (ctx->precond == 1) CU(launch_main(ctx, biot::MODE_PASS2, ctx->x[r], ctx->x[1 - r], &win));
+        if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], nullptr, &win));
         CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, k0 + w, ctx->hist_cap,
                                       nt, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
     }

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
 #pragma unroll
                     for (int cc = 0; cc < D; ++cc) {
                         const double cf = __ldg(bp + s * W + D * NC + cc);
-                        const double *src = a.zbuf + (j * NC + cc) * P + t0;
+                        const double *src = a.zbuf + (j * NC + cc) * P + a.t_off + t0;
                         const double2 v01 = __ldg(reinterpret_cast<const double2 *>(src));
                         const double2 v23 = __ldg(reinterpret_cast<const double2 *>(src + 2));
                         bt[0] = fma(cf, v01.x, bt[0]);
@@ -108,12 +108,12 @@ __global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
                     }
                 }
                 const double dv = __ldg(a.dinv + i * NC + D);
-                const double *rp = a.zbuf + (i * NC + D) * P + t0;
-                const double *xp = a.x + (i * NC + D) * P + t0;
-                double *dst = a.xn + (i * NC + D) * P + t0;
+                const double *rp = a.zbuf + (i * NC + D) * P + a.t_off + t0;
+                const double *xp = a.x + (i * NC + D) * P + a.t_off + t0;
+                double *dst = a.xn + (i * NC + D) * P + a.t_off + t0;
 #pragma unroll
                 for (int tt = 0; tt < kT; ++tt) {
-                    if (t0 + tt < n_tl) {
+                    if (t0 + tt < n_tl && t0 + tt >= a.t_lo) {
                         const double zp = dv * (bt[tt] - rp[tt]);
                         const double v = fma(a.omega, zp, xp[tt]);
                         dst[tt] = v;

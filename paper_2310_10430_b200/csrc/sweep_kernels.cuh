@@ -45,6 +45,7 @@ struct SweepArgs {
 };
 
 struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
+    int32_t t_off, t_lo;    // time window (Gauss-Seidel waves): columns t_off.., stores from t_lo
     const double *x;
     double *xn;
     const double *zbuf;
@@ -89,6 +90,9 @@ struct Tile3dArgs : SweepArgs {
     const double *aux;                // [n_alloc][kAux]
     const double *cls;                // geometric-class stencils [27][15][kClsW], column-major blocks
     static constexpr int kClsW = 18;  // 17 entries padded to 16 B
+    int64_t ghost_stride;             // doubles between ghost entries (1: a vector; pitch: a panel column)
+    int32_t t_off;                    // first panel column of the time window (Gauss-Seidel waves)
+    int32_t t_lo;                     // window steps below t_lo are computed but not stored or counted
     int32_t n1;                      // nodes per axis
     int32_t z_rows;                   // planes marched per tile
     int32_t s0;                       // zero-storage structural-zero variant

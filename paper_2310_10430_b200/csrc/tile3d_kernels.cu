@@ -178,7 +178,7 @@ __device__ __forceinline__ void ghost_q(const double *ghost, int64_t n1, int64_t
                 const int64_t j = iA + ((int64_t)dz * n1 + dy) * n1 + dxc;
                 double xv[4];
 #pragma unroll
-                for (int cc = 0; cc < 4; ++cc) xv[cc] = __ldg(ghost + j * 4 + cc);
+                for (int cc = 0; cc < 4; ++cc) xv[cc] = __ldg(ghost + (j * 4 + cc) * a.ghost_stride);
 #pragma unroll
                 for (int n = 0; n < NN; ++n) {
                     const int s = n == 0 ? sA : sB;
@@ -242,8 +242,8 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
         npn += np1[0];
         if constexpr (MODE != MODE_RESIDUAL) {   // stores through one row pointer per node
             constexpr int ncw = MODE == MODE_UPDATE_P2 ? 4 : 3;   // P~1: pressure written by pass 2
-            if (t < a.n_tl) {
-                const int64_t P = a.pitch, row = (iA + n) * 4 * P + t;
+            if (t < a.n_tl && t >= a.t_lo) {
+                const int64_t P = a.pitch, row = (iA + n) * 4 * P + a.t_off + t;
 #pragma unroll
                 for (int c = 0; c < ncw; ++c) a.xn[row + c * P] = outx[c][0];
                 if constexpr (MODE == MODE_P1_PASS1) {
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
                         unsigned char *base = smem + (size_t)st * kStageBytes;
                         const bool real = (z >= 0 && z < g.n1);
                         mbar_expect_tx(&full[st], kXBytes + (real ? (uint32_t)ny * kB * kAuxRec * 8 : 0u));
-                        load_4d(base, &tmx, chunk * kTc, (x0 - 1) * 4, y0 - 1, z, &full[st]);
+                        load_4d(base, &tmx, a.t_off + chunk * kTc, (x0 - 1) * 4, y0 - 1, z, &full[st]);
                         if (real)
                             for (int yy = 0; yy < ny; ++yy)
                                 bulk_g2s(base + kXBytes + yy * kB * kAuxRec * 8,
@@ -400,7 +400,7 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
         const int ccxA = axis_class(xA, g.n1), ccxB = axis_class(xA + 1, g.n1), ccy = axis_class(y, g.n1);
         for (int chunk = 0; chunk < g.nchunks; ++chunk) {
             const int t = chunk * kTc + lane;
-            const double sv = t < a.n_tl ? a.s[t] : 0.0;
+            const double sv = t < a.n_tl ? a.s[a.t_off + t] : 0.0;
             const bool ghost = chunk == 0;
             double nu = 0.0, npn = 0.0;
             double acc[2][4], q[2];
@@ -456,8 +456,8 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
             if (lane == 0) mbar_arrive(&empty[sd]);       // plane zb
             it += (uint32_t)(zb - za + 2);
             // per-step norm partials of this (tile, chunk), fixed reduction order over warps
-            red[warp][lane][0] = nu;
-            red[warp][lane][1] = npn;
+            red[warp][lane][0] = t >= a.t_lo ? nu : 0.0;
+            red[warp][lane][1] = t >= a.t_lo ? npn : 0.0;
             asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
             if (threadIdx.x < kTc * 2) {
                 const int tl = threadIdx.x >> 1, part = threadIdx.x & 1;

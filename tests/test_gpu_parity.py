@@ -258,3 +258,13 @@ def test_gs_parity_long_windows():
     (xg, hg), (xo, ho) = _gs_pair(prob, 200, 150, 2, 0.5)
     assert field_errors(xg, xo, 2).max() < TOL
     assert norm_errors(hg, ho).max() < TOL
+
+
+@pytest.mark.parametrize("precond,omega", [(2, 0.5), (1, 0.3)])
+def test_gs_parity_3d(precond, omega):
+    """3D tile kernel in wavefront GS (lognormal kappa, ragged windows) vs Alg. 2 literal."""
+    prob = make_problem(3, 7, 40, 0.01, 6, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0,
+                        kappa_seed=3, x0_seed=9)
+    (xg, hg), (xo, ho) = _gs_pair(prob, 40, 7, precond, omega)
+    assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
