@@ -490,6 +490,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost = win->ghost;
             a.ghost_stride = win->stride;
         }
+        if (mode == biot::MODE_PASS2) return biot::launch_tile3d(c->tmapz, a, c->shape, c->stream);
         return biot::launch_tile3d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
     if (c->kern == 4) {
@@ -521,7 +522,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
 
 // P~1 second pass: the 2D tile mode on the Z panel, else the generic kernel.
 cudaError_t launch_pass2_any(biot_ctx *ctx, const double *xin, double *xout, double *sendbuf, const Window *win) {
-    if (ctx->kern == 4) return launch_main(ctx, biot::MODE_PASS2, xin, xout, win);
+    if (ctx->kern == 4 || ctx->kern == 6) return launch_main(ctx, biot::MODE_PASS2, xin, xout, win);
     biot::Pass2Args p{};
     p.x = xin;
     p.xn = xout;
@@ -1027,6 +1028,13 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
             if (r != CUDA_SUCCESS)
                 return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (4D) failed: " + std::to_string((int)r));
+            if (k == 0 && ctx->z) {
+                r = encode(&ctx->tmapz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->z, dims, strides, bx, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                if (r != CUDA_SUCCESS)
+                    return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (4D, Z) failed: " + std::to_string((int)r));
+            }
         }
     } else {
         CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));

@@ -274,6 +274,45 @@ __device__ __forceinline__ void start(const Tile3dArgs &a, const double *pd, con
     accum_plane<0, NN, CLS, S0>(a, pm, sx, sy, lane, aux, TA, TB, acc, q);
 }
 
+// ---- P~1 second pass (PAPER.md eq. p1: z_p = S~p^{-1} (B^T z_u - r_p)) on the Z panel
+// staged like x: bt = (B^T z_u) over the slots in (dz, dy, dx) order, one node per warp
+// (R = 1), coefficients AA[p][u_cc] from the interior template (zeros skipped) or the
+// class stencil (column-major: T[cc*4 + 3]).
+template <int DZ, bool CLS, bool S0>
+__device__ __forceinline__ void accum_plane_bt(const Tile3dArgs &a, const double *pl, int sx, int sy, int lane,
+                                               const double *T, double &bt) {
+#pragma unroll
+    for (int dy = -1; dy <= 1; ++dy)
+#pragma unroll
+        for (int dx = -1; dx <= 1; ++dx) {
+            const int s = slot_of(dx, dy, DZ);
+            if (s < 0) continue;
+            const double *cp = col_ptr(pl, sx + dx, sy + dy, lane);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                if constexpr (!CLS) {
+                    if (tmpl3_zero(s, 12 + cc, S0)) continue;
+                }
+                const double cf = CLS ? T[s * kCW + cc * 4 + 3] : a.tmpl[s][12 + cc];
+                bt = fma(cf, cp[cc * kTc], bt);
+            }
+        }
+}
+
+template <bool CLS, bool S0>
+__device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po, const double *pu,
+                                          const double *aux, int64_t i, int sx, int sy, int lane, int t,
+                                          const double *T, double bt) {
+    accum_plane_bt<1, CLS, S0>(a, pu, sx, sy, lane, T, bt);
+    if (t < a.n_tl && t >= a.t_lo) {
+        const int64_t P = a.pitch, row = i * 4 * P + 3 * P + a.t_off + t;
+        const double rp = col_ptr(po, sx, sy, lane)[3 * kTc];
+        const double v = fma(a.omega, aux[22] * (bt - rp), __ldg(a.x + row));
+        a.xn[row] = v;
+        if (a.sendbuf && t == a.n_tl - 1) a.sendbuf[i * 4 + 3] = v;
+    }
+}
+
 struct Geo3 {
     int n1, np, nzr, ntiles, nchunks;
     __device__ explicit Geo3(const Tile3dArgs &a) {
@@ -422,12 +461,16 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
                                             (py * kB + px) * kAuxRec;
                         const int64_t iA = ((int64_t)(m - 1) * g.n1 + y) * g.n1 + xA;
                         double *carry = qcarry + (m - 1 - za) * (kB * kB) + py * kB + px;
-                        if (vB)
+                        if constexpr (MODE == MODE_PASS2) {   // bt rides in q[0]
+                            if (kindP == 1) finish_bt<false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q[0]);
+                            else finish_bt<true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q[0]);
+                        } else if (vB) {
                             finish_any<2, S0, MODE>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
                                               TBp, acc, q, nu, npn);
-                        else
+                        } else {
                             finish_any<1, S0, MODE>(kindP, a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp,
                                               TBp, acc, q, nu, npn);
+                        }
                     }
                     kindP = 0;
                     if (m < zb) {                // start plane m
@@ -440,7 +483,18 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
                             TAp = cls_sm + (base + ccxA - cxl) * kClsD;
                             TBp = cls_sm + (base + (vB ? ccxB : ccxA) - cxl) * kClsD;
                         }
-                        if (kindP != 0) {
+                        if constexpr (MODE == MODE_PASS2) {
+                            if (kindP != 0) {
+                                q[0] = 0.0;
+                                if (kindP == 1) {
+                                    accum_plane_bt<-1, false, S0>(a, pd, sx, sy, lane, TAp, q[0]);
+                                    accum_plane_bt<0, false, S0>(a, pm, sx, sy, lane, TAp, q[0]);
+                                } else {
+                                    accum_plane_bt<-1, true, S0>(a, pd, sx, sy, lane, TAp, q[0]);
+                                    accum_plane_bt<0, true, S0>(a, pm, sx, sy, lane, TAp, q[0]);
+                                }
+                            }
+                        } else if (kindP != 0) {
                             if (vB)
                                 start_any<2, S0>(kindP, a, pd, pm, aux, sx, sy, lane, TAp, TBp, acc, q);
                             else
@@ -456,6 +510,7 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
             if (lane == 0) mbar_arrive(&empty[sd]);       // plane zb
             it += (uint32_t)(zb - za + 2);
             // per-step norm partials of this (tile, chunk), fixed reduction order over warps
+            if constexpr (MODE == MODE_PASS2) continue;   // the norms come from pass 1
             red[warp][lane][0] = t >= a.t_lo ? nu : 0.0;
             red[warp][lane][1] = t >= a.t_lo ? npn : 0.0;
             asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
@@ -502,7 +557,8 @@ cudaError_t tile3d_shape(int device, LaunchShape *out) {
     if (e != cudaSuccess) return e;
     for (auto fn : {tile3d_kernel<false, kR, MODE_UPDATE_P2>, tile3d_kernel<true, kR, MODE_UPDATE_P2>,
                     tile3d_kernel<false, kR, MODE_P1_PASS1>, tile3d_kernel<true, kR, MODE_P1_PASS1>,
-                    tile3d_kernel<false, kR, MODE_RESIDUAL>, tile3d_kernel<true, kR, MODE_RESIDUAL>}) {
+                    tile3d_kernel<false, kR, MODE_RESIDUAL>, tile3d_kernel<true, kR, MODE_RESIDUAL>,
+                    tile3d_kernel<false, kR, MODE_PASS2>, tile3d_kernel<true, kR, MODE_PASS2>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesOf<kR>);
         if (e != cudaSuccess) return e;
     }
@@ -525,6 +581,7 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
 #define BIOT_T3(S0_, M_) tile3d_kernel<S0_, kR, M_><<<grid, block, sh.smem, st>>>(tmx, a)
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T3(true, MODE_UPDATE_P2); else BIOT_T3(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T3(true, MODE_P1_PASS1); else BIOT_T3(false, MODE_P1_PASS1); }
+    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T3(true, MODE_PASS2); else BIOT_T3(false, MODE_PASS2); }
     else { if (a.s0) BIOT_T3(true, MODE_RESIDUAL); else BIOT_T3(false, MODE_RESIDUAL); }
 #undef BIOT_T3
     return cudaGetLastError();
