@@ -147,8 +147,19 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K);
  * of step n uses the CURRENT sweep's X^{n-1}), run as a pipelined wavefront of
  * n_t_local + K - 1 windows.  Same preconditioner and omega as biot_iterate; the
  * residual history records, for sweep k and step n, the residual that update used.
- * Needs a structured 2D mesh (tile kernel) and world == 1, else BIOT_E_STATE. */
+ * Needs a structured 2D / 3D mesh (tile kernels), else BIOT_E_STATE.  Collective for
+ * world > 1: after each wave in which rank r-1 updated its last step it sends that
+ * slice to rank r (NCCL), K transfers per rank pair. */
 biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
+
+/* The same run one wave at a time (BIOT_FLAG_MANUAL_HALO: before wave w the caller
+ * moves the predecessor rank's biot_last_slice into biot_set_ghost of every rank
+ * whose first owned step n satisfies w - K + 2 <= n <= w + 1).
+ * biot_gs_waves: number of waves (n_t + K - 1) of the open run. */
+biot_status biot_gs_begin(biot_ctx *ctx, int32_t K);
+biot_status biot_gs_waves(const biot_ctx *ctx, int32_t *out);
+biot_status biot_gs_wave(biot_ctx *ctx);
+biot_status biot_gs_end(biot_ctx *ctx);
 
 /* Residual norms at the current iterate: out[n_t_local][2] = ||r_u||, ||r_p||
  * of the owned steps (a residual-only pass, no update). */

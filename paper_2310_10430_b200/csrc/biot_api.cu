@@ -160,7 +160,10 @@ struct biot_ctx {
     int s0 = 0;                       // tile2d/tile3d zero-storage structural-zero variant
     // 6: TMA-pipelined 3D tile kernel
     double tmpl3[15][17] = {{0}};
-    double *cls = nullptr;            // tile3d geometric-class stencils (device)
+    double *cls = nullptr;            // tile3d class stencils (device)
+    // Gauss-Seidel wavefront state (biot_gs_begin / biot_gs_wave / biot_gs_end)
+    int32_t gs_K = 0, gs_w = 0;
+    int64_t gs_k0 = 0;
     int32_t n1 = 0, z_rows = 0;
     int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
     int sR = 4, sT = 2;
@@ -463,6 +466,7 @@ struct Window {
     int t_off = 0, len = 0, t_lo = 0;   // t_lo: window steps below it are not stored (alignment)
     const double *ghost = nullptr;
     int64_t stride = 1;
+    double *send = nullptr;             // send slice (only when the window ends at the slab's last step)
 };
 
 cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, const Window *win = nullptr) {
@@ -489,6 +493,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.n_tl = win->len;
             a.ghost = win->ghost;
             a.ghost_stride = win->stride;
+            a.sendbuf = win->send;
         }
         if (mode == biot::MODE_PASS2) return biot::launch_tile3d(c->tmapz, a, c->shape, c->stream);
         return biot::launch_tile3d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
@@ -509,6 +514,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.n_tl = win->len;
             a.ghost = win->ghost;
             a.ghost_stride = win->stride;
+            a.sendbuf = win->send;
         }
         a.s0 = c->s0;
         a.dry = c->tile_dry;
@@ -536,6 +542,7 @@ cudaError_t launch_pass2_any(biot_ctx *ctx, const double *xin, double *xout, dou
     p.n_tl = win ? win->len : ctx->n_tl;
     p.t_off = win ? win->t_off : 0;
     p.t_lo = win ? win->t_lo : 0;
+    if (win) p.sendbuf = win->send;
     p.tw = ctx->tw;
     p.node_block = ctx->node_block;
     p.omega = ctx->omega;
@@ -1139,51 +1146,100 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
 }
 
 // Gauss-Seidel in time (Alg. 2 read literally: b^{n,m} =
-// A' X^{n-1,m} + f^n), pipelined as a wavefront: sweep u of step t runs in wave
-// w = t + u - 1 and needs only wave w-1 (X^{t,u-1} and X^{t-1,u}), so wave w updates
-// the window of steps max(0, w-K+1)..min(n_tl-1, w) at once.  Wave w reads panel
-// (cur + w) % 2 and writes the other, so step t's iterate of sweep u lives in panel
-// (cur + t + u) % 2: the odd columns are moved before and after (checkerboard).
-biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
+// A' X^{n-1,m} + f^n), pipelined as a wavefront over the global steps: sweep u of
+// step t runs in wave w = t + u - 1 and needs only wave w-1 (X^{t,u-1} and X^{t-1,u}),
+// so wave w updates the window of steps max(0, w-K+1)..min(N_t-1, w) at once; each
+// rank runs its part of the window.  Wave w reads panel (cur + w) % 2 and writes the
+// other, so global step t's iterate of sweep u lives in panel (cur + t + u) % 2: the
+// columns of odd global step are moved before and after (checkerboard).  Across
+// time slabs, rank r-1 sends the slice of its last step after each wave in which it
+// updated it, and rank r receives it as the ghost of the next wave (K transfers).
+namespace {
+
+bool gs_recv(const biot_ctx *c, int w) {   // this rank needs its predecessor's slice at wave w
+    const int g0 = c->first_step - 1;
+    return c->rank > 0 && w - g0 >= 0 && w - g0 <= c->gs_K - 1;
+}
+bool gs_send(const biot_ctx *c, int w) {   // rank r+1 needs this rank's last slice at wave w
+    const int g1 = c->first_step - 1 + c->n_tl;
+    return c->rank + 1 < c->world && w - g1 >= 0 && w - g1 <= c->gs_K - 1;
+}
+
+biot_status gs_parity_copy(biot_ctx *ctx, const double *src, double *dst, int parity) {
+    copy_parity_columns_kernel<<<1184, 256, 0, ctx->stream>>>(src, dst, ctx->N * ctx->nc, ctx->pitch, ctx->n_tl,
+                                                              parity);
+    CU(cudaGetLastError());
+    return BIOT_OK;
+}
+
+biot_status gs_run_wave(biot_ctx *ctx) {
+    const int w = ctx->gs_w++, K = ctx->gs_K, L = ctx->n_tl, g0 = ctx->first_step - 1;
+    const int lo = std::max(0, w - K + 1 - g0), hi = std::min(L - 1, w - g0);
+    if (lo > hi) return BIOT_OK;   // the wavefront is not in this slab
+    const int r = (ctx->cur + w) % 2;
+    Window win;
+    win.t_off = lo & ~1;                 // 16-B aligned columns; step lo-1 (if any) is not stored
+    win.t_lo = lo - win.t_off;
+    win.len = hi - win.t_off + 1;
+    if (win.t_off == 0) {
+        win.ghost = ctx->ghost;          // x_0, or the predecessor slab's slice of this wave
+        win.stride = 1;
+    } else {
+        win.ghost = ctx->x[r] + (win.t_off - 1);
+        win.stride = ctx->pitch;
+    }
+    win.send = (ctx->world > 1 && hi == L - 1) ? ctx->sendbuf : nullptr;
+    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+    CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
+    if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
+    CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, ctx->gs_k0 + w - g0,
+                                  ctx->hist_cap, L, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
+    if (win.send) ctx->send_dirty = false;
+    return BIOT_OK;
+}
+
+}  // namespace
+
+biot_status biot_gs_begin(biot_ctx *ctx, int32_t K) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
-    if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
+    if (K < 1) return fail(ctx, BIOT_E_INVALID, "K must be >= 1");
     if (ctx->kern != 4 && ctx->kern != 6)
         return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs a tile kernel (structured 2D / 3D mesh)");
-    if (ctx->world != 1)
-        return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time runs on one time slab in this version");
-    if (K == 0) return BIOT_OK;
+    if (ctx->gs_K) return fail(ctx, BIOT_E_STATE, "a Gauss-Seidel run is already open");
     CU(cudaSetDevice(ctx->device));
-    const int64_t rows = ctx->N * ctx->nc;
-    const int nt = ctx->n_tl;
-    auto parity_copy = [&](const double *src, double *dst) {
-        copy_parity_columns_kernel<<<1184, 256, 0, ctx->stream>>>(src, dst, rows, ctx->pitch, nt, 1);
-        return cudaGetLastError();
-    };
+    ctx->gs_K = K;
+    ctx->gs_w = 0;
+    ctx->gs_k0 = ctx->iterations;
+    ctx->send_dirty = true;
     CU(cudaEventRecord(ctx->ev_a, ctx->stream));
-    CU(parity_copy(ctx->x[ctx->cur], ctx->x[1 - ctx->cur]));
-    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
-    const int64_t k0 = ctx->iterations;
-    for (int w = 0; w <= nt + K - 2; ++w) {
-        const int lo = std::max(0, w - K + 1), hi = std::min(nt - 1, w);
-        const int r = (ctx->cur + w) % 2;
-        Window win;
-        win.t_off = lo & ~1;                 // 16-B aligned columns; step lo-1 (if any) is not stored
-        win.t_lo = lo - win.t_off;
-        win.len = hi - win.t_off + 1;
-        if (win.t_off == 0) {
-            win.ghost = ctx->ghost;
-            win.stride = 1;
-        } else {
-            win.ghost = ctx->x[r] + (win.t_off - 1);
-            win.stride = ctx->pitch;
-        }
-        CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
-        if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], nullptr, &win));
-        CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, k0 + w, ctx->hist_cap,
-                                      nt, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
-    }
-    ctx->cur = (ctx->cur + K) % 2;
-    CU(parity_copy(ctx->x[1 - ctx->cur], ctx->x[ctx->cur]));
+    // global step g0 + t starts in panel (cur + g0 + t) % 2
+    return gs_parity_copy(ctx, ctx->x[ctx->cur], ctx->x[1 - ctx->cur], (ctx->first_step - 1) % 2 == 0 ? 1 : 0);
+}
+
+biot_status biot_gs_waves(const biot_ctx *ctx, int32_t *out) {
+    if (!ctx || !out) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    *out = ctx->n_t + ctx->gs_K - 1;
+    return BIOT_OK;
+}
+
+biot_status biot_gs_wave(biot_ctx *ctx) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!ctx->gs_K) return fail(ctx, BIOT_E_STATE, "no Gauss-Seidel run open (biot_gs_begin)");
+    if (ctx->gs_w >= ctx->n_t + ctx->gs_K - 1) return fail(ctx, BIOT_E_STATE, "all waves of the run are done");
+    CU(cudaSetDevice(ctx->device));
+    return gs_run_wave(ctx);
+}
+
+biot_status biot_gs_end(biot_ctx *ctx) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (!ctx->gs_K) return fail(ctx, BIOT_E_STATE, "no Gauss-Seidel run open (biot_gs_begin)");
+    if (ctx->gs_w != ctx->n_t + ctx->gs_K - 1) return fail(ctx, BIOT_E_STATE, "waves of the run still pending");
+    CU(cudaSetDevice(ctx->device));
+    const int K = ctx->gs_K;
+    // global step g0 + t ends in panel (cur + g0 + t + K) % 2: gather it into cur'
+    ctx->cur = (ctx->cur + K + ctx->first_step - 1) % 2;
+    biot_status st = gs_parity_copy(ctx, ctx->x[1 - ctx->cur], ctx->x[ctx->cur], 1);
+    if (st != BIOT_OK) return st;
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
     CU(cudaEventSynchronize(ctx->ev_b));
     float tot = 0.f;
@@ -1191,12 +1247,40 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
     ctx->last_ms_iter = tot / K;
     ctx->last_ms_sweep = tot / K;
     ctx->iterations += K;
+    ctx->gs_K = 0;
     ctx->send_dirty = true;
     int nf = 0;
     CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (nf) return fail(ctx, BIOT_E_NONFINITE, "a residual norm became non-finite");
     return BIOT_OK;
+}
+
+biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
+    if (K == 0) return BIOT_OK;
+    if (ctx->world > 1 && (ctx->flags & BIOT_FLAG_MANUAL_HALO))
+        return fail(ctx, BIOT_E_STATE, "manual halo: drive the waves with biot_gs_begin/wave/end");
+    NcclApi *api = ctx->world > 1 ? nccl() : nullptr;
+    if (ctx->world > 1 && (!api || !ctx->comm)) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
+    biot_status st = biot_gs_begin(ctx, K);
+    if (st != BIOT_OK) return st;
+    const size_t n = (size_t)ctx->N * ctx->nc;
+    for (int w = 0; w < ctx->n_t + K - 1; ++w) {
+        if (api && (gs_recv(ctx, w) || gs_send(ctx, w))) {   // one slice per wave between neighbours
+            ncclResult_t r = api->GroupStart();
+            if (r == ncclSuccess && gs_send(ctx, w))
+                r = api->Send(ctx->sendbuf, n, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->stream);
+            if (r == ncclSuccess && gs_recv(ctx, w))
+                r = api->Recv(ctx->ghost, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream);
+            ncclResult_t r2 = api->GroupEnd();
+            if (r != ncclSuccess || r2 != ncclSuccess) return fail(ctx, BIOT_E_NCCL, "NCCL wave exchange failed");
+        }
+        st = gs_run_wave(ctx);
+        if (st != BIOT_OK) return st;
+    }
+    return biot_gs_end(ctx);
 }
 
 biot_status biot_residual_norms(biot_ctx *ctx, double *out) {

@@ -78,6 +78,18 @@ class BiotSolver:
     def iterate_gs(self, K):
         check(self.lib.biot_iterate_gs(self.ctx, K), self.ctx)
 
+    def gs_begin(self, K):
+        check(self.lib.biot_gs_begin(self.ctx, K), self.ctx)
+        n = ctypes.c_int32()
+        check(self.lib.biot_gs_waves(self.ctx, ctypes.byref(n)), self.ctx)
+        return n.value
+
+    def gs_wave(self):
+        check(self.lib.biot_gs_wave(self.ctx), self.ctx)
+
+    def gs_end(self):
+        check(self.lib.biot_gs_end(self.ctx), self.ctx)
+
     def iterate(self, K):
         check(self.lib.biot_iterate(self.ctx, int(K)), self.ctx)
 
