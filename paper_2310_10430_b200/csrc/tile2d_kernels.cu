@@ -198,8 +198,8 @@ __device__ __forceinline__ void start(const A &a, const double *pd, const double
 template <bool CLS, bool S0, int MODE, class A>
 __device__ __forceinline__ void finish(const A &a, const double *po, const double *pu, int p, int lane,
                                        const double *aux, const double *T, int64_t i, int t0, bool ghost,
-                                       bool full, double *carry, double (&acc)[3][kT2], double (&q)[kT2],
-                                       double (&nu)[kT2], double (&npn)[kT2]) {
+                                       bool full, double *carry, const double (&sv)[kT2], double (&acc)[3][kT2],
+                                       double (&q)[kT2], double (&nu)[kT2], double (&npn)[kT2]) {
     accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
     // q(t-1) of each half's first step: lane l-1's matching step; lane 0 of the second
     // half takes lane 31's first-half step 63, lane 0 of the first half the carry
@@ -221,9 +221,8 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2], outx[3][2], outz[3][2];
-        const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
-        sv2[0] = s2.x;
-        sv2[1] = s2.y;
+        sv2[0] = sv[2 * h];
+        sv2[1] = sv[2 * h + 1];
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             q2[tt] = q[2 * h + tt];
@@ -429,11 +428,27 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const int t0 = chunk * kCT + lane * 2;   // the lane's first half; second half at t0 + 64
             const bool ghost = chunk == 0;
             const bool whole = (chunk + 1) * kCT <= a.n_tl && (chunk > 0 || a.t_lo == 0);   // chunk inside the window
-            double nu[kT2], npn[kT2];
+            double nu[kT2], npn[kT2], sv[kT2], prev[kT2][2];
+            // load scales s_t of the lane's steps (zero past n_tl) and, issued now so its
+            // latency hides behind the march, this (CTA, column)'s running norm sums
+            const bool first = tile == (int)blockIdx.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
+                sv[2 * h] = s2.x;
+                sv[2 * h + 1] = s2.y;
+            }
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
                 nu[tt] = 0.0;
                 npn[tt] = 0.0;
+                const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
+                prev[tt][0] = prev[tt][1] = 0.0;
+                if (MODE != MODE_PASS2 && !first && t < a.n_tl) {
+                    const double *src = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
+                    prev[tt][0] = src[0];
+                    prev[tt][1] = src[1];
+                }
             }
             double acc[3][kT2], q[kT2];
             int kindP = 0;                       // pending node (row m-1): 0 none, 1 interior, 2 class
@@ -459,10 +474,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         } else {
                             if (kindP == 1)
                                 finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
-                                                                    carry, acc, q, nu, npn);
+                                                                    carry, sv, acc, q, nu, npn);
                             else
                                 finish<true, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
-                                                                   carry, acc, q, nu, npn);
+                                                                   carry, sv, acc, q, nu, npn);
                         }
                     }
                     kindP = 0;
@@ -489,7 +504,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
             it += (uint32_t)(jb - ja + 2);
             // per-step norm partials of this (CTA, column), summed over the rows and, in
             // the CTA's fixed tile order, over its tiles (the lane re-reads its own sums)
-            const bool first = tile == (int)blockIdx.x;
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
                 if constexpr (MODE == MODE_PASS2) break;   // the norms come from pass 1
@@ -497,8 +511,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 if (t < a.n_tl) {
                     double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
                     const double u = t >= a.t_lo ? nu[tt] : 0.0, v = t >= a.t_lo ? npn[tt] : 0.0;
-                    dst[0] = first ? u : dst[0] + u;
-                    dst[1] = first ? v : dst[1] + v;
+                    dst[0] = first ? u : prev[tt][0] + u;
+                    dst[1] = first ? v : prev[tt][1] + v;
                 }
             }
         }
