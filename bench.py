@@ -42,9 +42,11 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs"],
+    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs", "gmres"],
                     help="jacobi: all steps at once (BASELINE metric); gs: Gauss-Seidel in time "
-                         "(PAPER.md Alg. 2 literal) as a wavefront, one GPU")
+                         "(PAPER.md Alg. 2 literal) as a wavefront; gmres: Alg. 3 with one GMRES(k) "
+                         "cycle per step and outer iteration (left P~2)")
+    ap.add_argument("--gmres-k", type=int, default=10)
     return ap.parse_args()
 
 
@@ -153,7 +155,8 @@ def workload_config(args, prob, world):
     from workloads import DESCRIPTIONS
     ws_gb = 2 * prob.n_dof * prob.n_t * 8 / 1e9
     return {"workload": f"config{args.config}: {DESCRIPTIONS[args.config]}"
-                        + (", Gauss-Seidel in time (wavefront)" if args.method == "gs" else ""),
+                        + (", Gauss-Seidel in time (wavefront)" if args.method == "gs" else "")
+                        + (f", per-step GMRES({args.gmres_k})" if args.method == "gmres" else ""),
             "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
             "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
             "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
@@ -230,7 +233,10 @@ def main():
         if world > 1:
             dist.barrier()
 
-    step = g.iterate_gs if args.method == "gs" else g.iterate
+    if args.method == "gmres":
+        step = lambda K: g.iterate_gmres(K, args.gmres_k)
+    else:
+        step = g.iterate_gs if args.method == "gs" else g.iterate
     # warm-up (untimed)
     step(max(args.warmup, 3))
     barrier()
@@ -277,6 +283,10 @@ def main():
         pk = peaks()
         hbm = pk["hbm_gbs"] if pk else 6650.0
         algo_bytes = info.bytes_per_iter          # per launch of the sweep kernel (this rank)
+        if args.method == "gmres":
+            # one GMRES(k) cycle = 7 + 14k + 2k^2 passes over a space-time panel
+            kk = args.gmres_k
+            algo_bytes = (7 + 14 * kk + 2 * kk * kk) * 8.0 * prob.n_dof * info.n_t_local
         achieved_gbs = algo_bytes / (sweep_ms / 1e3) / 1e9
         sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
         fp64_meas_tf, fp64_nom_tf = fp64_peak(sm_max)
@@ -302,6 +312,8 @@ def main():
         launches = per_step * args.steps
         if args.method == "gs":   # n_t + K - 1 waves and two checkerboard copies per call
             launches = 2 + (info.n_t_local + args.steps - 1) * per_step
+        if args.method == "gmres":   # residual + finalize, 2 + k (1 + 2 x 3 + 3) + 1 panel kernels
+            launches = args.steps * (2 + 2 + 2 + args.gmres_k * (1 + 6 + 3) + 1)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",

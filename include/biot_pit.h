@@ -152,6 +152,15 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K);
  * slice to rank r (NCCL), K transfers per rank pair. */
 biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
 
+/* K outer iterations of PAPER.md Algorithm 3 with the per-step solver K = GMRES(k)
+ * (the paper's experiments' solver): every step at once runs one GMRES(k) cycle on
+ * AA x_n = A' x_{n-1} + f_n (Jacobi in time) from its current iterate, left-
+ * preconditioned by the diagonal P~2 (reading R23).  1 <= k <= 16; needs a structured 2D
+ * mesh and precond = 2 (BIOT_E_STATE otherwise); allocates k+1 Krylov panels on first
+ * use.  The residual history records, per iteration and step, ||b - AA x|| (u, p) at
+ * the cycle's start.  Collective for world > 1 (one slice per outer iteration). */
+biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k);
+
 /* The same run one wave at a time (BIOT_FLAG_MANUAL_HALO: before wave w the caller
  * moves the predecessor rank's biot_last_slice into biot_set_ghost of every rank
  * whose first owned step n satisfies w - K + 2 <= n <= w + 1).

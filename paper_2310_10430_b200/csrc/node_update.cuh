@@ -31,7 +31,9 @@ __device__ __forceinline__ double cload(const double *p) {
 // sweep kernel so the results are identical): r = s_t f + q(t-1) - acc, norms,
 // z = P^-1 r (P~2, or the displacement half of P~1), x^{k+1} = x^k + omega z.
 // MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
-template <int D, int T, bool MASK>
+// ZFULL: outz = z = P~2^{-1} r for every component (GMRES); else outz = (z_u, r_p)
+// (the P~1 first pass).
+template <int D, int T, bool MASK, bool ZFULL = false>
 __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[D + 1][T], const double (&q)[T],
                                               double qprev, const double (&F)[D + 1],
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
@@ -63,7 +65,7 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             outx[c][tt] = fma(omega, z[c], xs[c][tt]);
-            outz[c][tt] = (c < D) ? z[c] : r[D];
+            outz[c][tt] = (c < D || ZFULL) ? z[c] : r[D];
         }
     }
 }

@@ -16,6 +16,8 @@ enum SweepMode : int {
     MODE_P1_PASS1 = 1,    // residual, x_u update, Z = (z_u, r_p), norms
     MODE_RESIDUAL = 2,    // residual norms only (no writes)
     MODE_PASS2 = 3,       // P~1 second pass (tile kernels): x_p += omega DSinv (B^T z_u - r_p)
+    MODE_ZOUT = 4,        // GMRES start (2D tile): zbuf = P~2^{-1} r, norms of r, x untouched
+    MODE_MATVEC = 5,      // GMRES Arnoldi (2D tile): xn = P~2^{-1} AA x, no time coupling
 };
 
 struct SweepArgs {
@@ -141,6 +143,16 @@ void tile3d_box(uint32_t *box);      // {time, x*4+c, y, z}
 cudaError_t tile3d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
+
+// Per-step GMRES panel kernels (gmres_kernels.cu): column-wise (per time step) dot
+// products of a panel with nb panels (b_dev: device array of panel pointers) and
+// dst = scale_t * (base + sign * sum_i coef[i][t] b_i); rows = real panel rows.
+int gmres_max_vectors();
+int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *chunks);
+cudaError_t gmres_dots(const double *a, const double *const *b_dev, int nb, int64_t rows, int64_t pitch, int n_tl,
+                       double *scratch, double *out, cudaStream_t st);
+cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, const double *coef, int nb,
+                          double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl, cudaStream_t st);
 
 bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);

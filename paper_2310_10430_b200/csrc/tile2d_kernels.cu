@@ -234,13 +234,27 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
                 xs2[c][tt] = xs[c][2 * h + tt];
             }
         }
-        epilogue_math<2, 2, CLS>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2, sv2, nu2, np2, outx, outz);
+        epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2, sv2, nu2, np2,
+                                                    outx, outz);
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             nu[2 * h + tt] = nu2[tt];
             npn[2 * h + tt] = np2[tt];
         }
-        if constexpr (MODE != MODE_RESIDUAL) {
+        if constexpr (MODE == MODE_ZOUT) {
+            const int th = t0 + h * (kCT / 2);
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double *dst = a.zbuf + row + c * P + h * (kCT / 2);
+                if (full) {
+                    *reinterpret_cast<double2 *>(dst) = make_double2(outz[c][0], outz[c][1]);
+                } else {
+                    if (st0) dst[0] = outz[c][0];
+                    if (st1) dst[1] = outz[c][1];
+                }
+            }
+        } else if constexpr (MODE != MODE_RESIDUAL) {
             constexpr int ncw = MODE == MODE_UPDATE_P2 ? 3 : 2;   // P~1: pressure written by pass 2
             const int th = t0 + h * (kCT / 2);
             const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
@@ -337,6 +351,33 @@ __device__ __forceinline__ void finish_bt(const A &a, const double *po, const do
         if (a.sendbuf) {
             if (th == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v0;
             if (th + 1 == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v1;
+        }
+    }
+}
+
+// ---- GMRES (Alg. 3 with K = GMRES, R23): w = P~2^{-1} (AA v) on the staged
+// v panel; the slots as the residual's, no previous-step coupling.
+template <bool CLS, bool S0, class A>
+__device__ __forceinline__ void finish_mv(const A &a, const double *pu, int p, int lane, const double *aux,
+                                          const double *T, int64_t i, int t0, bool whole, double (&acc)[3][kT2],
+                                          double (&q)[kT2]) {
+    accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
+    const int64_t P = a.pitch, row = i * 3 * P + a.t_off + t0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int th = t0 + h * (kCT / 2);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double dv = aux[10 + c];
+            const double w0 = c < 2 ? dv * acc[c][2 * h] : -(dv * acc[c][2 * h]);
+            const double w1 = c < 2 ? dv * acc[c][2 * h + 1] : -(dv * acc[c][2 * h + 1]);
+            double *dst = a.xn + row + c * P + h * (kCT / 2);
+            if (whole) {
+                *reinterpret_cast<double2 *>(dst) = make_double2(w0, w1);
+            } else {
+                if (th < a.n_tl) dst[0] = w0;
+                if (th + 1 < a.n_tl) dst[1] = w1;
+            }
         }
     }
 }
@@ -444,7 +485,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 npn[tt] = 0.0;
                 const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
                 prev[tt][0] = prev[tt][1] = 0.0;
-                if (MODE != MODE_PASS2 && !first && t < a.n_tl) {
+                if (MODE != MODE_PASS2 && MODE != MODE_MATVEC && !first && t < a.n_tl) {
                     const double *src = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
                     prev[tt][0] = src[0];
                     prev[tt][1] = src[1];
@@ -471,6 +512,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         if constexpr (MODE == MODE_PASS2) {
                             if (kindP == 1) finish_bt<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, whole, q);
                             else finish_bt<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, whole, q);
+                        } else if constexpr (MODE == MODE_MATVEC) {
+                            if (kindP == 1) finish_mv<false, S0, Tile2dArgs>(a, pm, p, lane, aux, T, i, t0, whole, acc, q);
+                            else finish_mv<true, S0, Tile2dArgs>(a, pm, p, lane, aux, T, i, t0, whole, acc, q);
                         } else {
                             if (kindP == 1)
                                 finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
@@ -506,7 +550,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             // the CTA's fixed tile order, over its tiles (the lane re-reads its own sums)
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) {
-                if constexpr (MODE == MODE_PASS2) break;   // the norms come from pass 1
+                if constexpr (MODE == MODE_PASS2 || MODE == MODE_MATVEC) break;   // no norms in these passes
                 const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
                 if (t < a.n_tl) {
                     double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
@@ -543,7 +587,9 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     for (auto fn : {tile2d_kernel<false, MODE_UPDATE_P2>, tile2d_kernel<true, MODE_UPDATE_P2>,
                     tile2d_kernel<false, MODE_P1_PASS1>, tile2d_kernel<true, MODE_P1_PASS1>,
                     tile2d_kernel<false, MODE_RESIDUAL>, tile2d_kernel<true, MODE_RESIDUAL>,
-                    tile2d_kernel<false, MODE_PASS2>, tile2d_kernel<true, MODE_PASS2>}) {
+                    tile2d_kernel<false, MODE_PASS2>, tile2d_kernel<true, MODE_PASS2>,
+                    tile2d_kernel<false, MODE_ZOUT>, tile2d_kernel<true, MODE_ZOUT>,
+                    tile2d_kernel<false, MODE_MATVEC>, tile2d_kernel<true, MODE_MATVEC>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
@@ -567,6 +613,8 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2(true, MODE_UPDATE_P2); else BIOT_T2(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2(true, MODE_P1_PASS1); else BIOT_T2(false, MODE_P1_PASS1); }
     else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2(true, MODE_PASS2); else BIOT_T2(false, MODE_PASS2); }
+    else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T2(true, MODE_ZOUT); else BIOT_T2(false, MODE_ZOUT); }
+    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T2(true, MODE_MATVEC); else BIOT_T2(false, MODE_MATVEC); }
     else { if (a.s0) BIOT_T2(true, MODE_RESIDUAL); else BIOT_T2(false, MODE_RESIDUAL); }
 #undef BIOT_T2
     return cudaGetLastError();

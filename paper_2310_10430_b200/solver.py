@@ -78,6 +78,9 @@ class BiotSolver:
     def iterate_gs(self, K):
         check(self.lib.biot_iterate_gs(self.ctx, K), self.ctx)
 
+    def iterate_gmres(self, K, k):
+        check(self.lib.biot_iterate_gmres(self.ctx, K, k), self.ctx)
+
     def gs_begin(self, K):
         check(self.lib.biot_gs_begin(self.ctx, K), self.ctx)
         n = ctypes.c_int32()

@@ -268,3 +268,41 @@ def test_gs_parity_3d(precond, omega):
     (xg, hg), (xo, ho) = _gs_pair(prob, 40, 7, precond, omega)
     assert field_errors(xg, xo, 3).max() < TOL
     assert norm_errors(hg, ho).max() < TOL
+
+
+# ---- per-step GMRES (Alg. 3 with K = GMRES) ----
+
+def _gmres_pair(prob, nt, K, k):
+    from oracle import gmres as ogm
+    s = load_scales(nt, parity=True)
+    x0 = _x0(prob, np.arange(1, nt + 1))
+    g = BiotSolver(prob, n_t=nt, precond=2, omega=0.5, load_scale=s)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate_gmres(K, k)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(kk) for kk in range(K)])
+    finally:
+        g.close()
+    S = oracle.OracleSystem(prob)
+    X = np.zeros((nt + 1, S.ndof))
+    X[1:] = S.to_paper(x0)
+    Xo, ho = ogm.iterate(S, X, s, K, k)
+    return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho)
+
+
+@pytest.mark.parametrize("nt,K,k", [(32, 3, 2), (40, 2, 5), (7, 3, 10)])
+def test_gmres_parity_config1(nt, K, k):
+    """One GMRES(k) cycle per step and outer iteration (CGS2 Arnoldi on the GPU, MGS in the
+    oracle) vs the oracle's Alg. 3: x^K and the residual history at 1e-9."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gmres_pair(prob, nt, K, k)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_gmres_parity_config2():
+    prob = config_problem(2)
+    (xg, hg), (xo, ho) = _gmres_pair(prob, 64, 2, 4)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
