@@ -42,10 +42,11 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs", "gmres"],
+    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs", "gmres", "gs_gmres"],
                     help="jacobi: all steps at once (BASELINE metric); gs: Gauss-Seidel in time "
                          "(PAPER.md Alg. 2 literal) as a wavefront; gmres: Alg. 3 with one GMRES(k) "
-                         "cycle per step and outer iteration (left P~2)")
+                         "cycle per step and outer iteration (left P~2); gs_gmres: Alg. 3 literally "
+                         "(Gauss-Seidel in time + GMRES(k)) on the wavefront")
     ap.add_argument("--gmres-k", type=int, default=10)
     return ap.parse_args()
 
@@ -156,7 +157,9 @@ def workload_config(args, prob, world):
     ws_gb = 2 * prob.n_dof * prob.n_t * 8 / 1e9
     return {"workload": f"config{args.config}: {DESCRIPTIONS[args.config]}"
                         + (", Gauss-Seidel in time (wavefront)" if args.method == "gs" else "")
-                        + (f", per-step GMRES({args.gmres_k})" if args.method == "gmres" else ""),
+                        + (f", per-step GMRES({args.gmres_k})" if args.method == "gmres" else "")
+                        + (f", Alg. 3: Gauss-Seidel in time + GMRES({args.gmres_k})" if args.method == "gs_gmres"
+                           else ""),
             "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
             "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
             "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
@@ -235,6 +238,8 @@ def main():
 
     if args.method == "gmres":
         step = lambda K: g.iterate_gmres(K, args.gmres_k)
+    elif args.method == "gs_gmres":
+        step = lambda K: g.iterate_gs_gmres(K, args.gmres_k)
     else:
         step = g.iterate_gs if args.method == "gs" else g.iterate
     # warm-up (untimed)
@@ -283,7 +288,7 @@ def main():
         pk = peaks()
         hbm = pk["hbm_gbs"] if pk else 6650.0
         algo_bytes = info.bytes_per_iter          # per launch of the sweep kernel (this rank)
-        if args.method == "gmres":
+        if args.method in ("gmres", "gs_gmres"):
             # one GMRES(k) cycle = 7 + 14k + 2k^2 passes over a space-time panel
             kk = args.gmres_k
             algo_bytes = (7 + 14 * kk + 2 * kk * kk) * 8.0 * prob.n_dof * info.n_t_local
@@ -312,7 +317,7 @@ def main():
         launches = per_step * args.steps
         if args.method == "gs":   # n_t + K - 1 waves and two checkerboard copies per call
             launches = 2 + (info.n_t_local + args.steps - 1) * per_step
-        if args.method == "gmres":   # residual + finalize, 2 + k (1 + 2 x 3 + 3) + 1 panel kernels
+        if args.method in ("gmres", "gs_gmres"):   # residual + finalize, 2 + k (1 + 2 x 3 + 3) + 1 panel kernels
             launches = args.steps * (2 + 2 + 2 + args.gmres_k * (1 + 6 + 3) + 1)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True,

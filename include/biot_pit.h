@@ -161,6 +161,13 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
  * the cycle's start.  Collective for world > 1 (one slice per outer iteration). */
 biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k);
 
+/* PAPER.md Algorithm 3 literally: Gauss-Seidel in time (b^{n,m} = A' X^{n-1,m} + f^n)
+ * with one GMRES(k) cycle per step and sweep (left P~2), run as the wavefront of
+ * biot_iterate_gs.  Same conditions as biot_iterate_gmres; collective for world > 1.
+ * biot_gs_begin_gmres: its wave-level form (k = 0: the Richardson update). */
+biot_status biot_iterate_gs_gmres(biot_ctx *ctx, int32_t K, int32_t k);
+biot_status biot_gs_begin_gmres(biot_ctx *ctx, int32_t K, int32_t k);
+
 /* The same run one wave at a time (BIOT_FLAG_MANUAL_HALO: before wave w the caller
  * moves the predecessor rank's biot_last_slice into biot_set_ghost of every rank
  * whose first owned step n satisfies w - K + 2 <= n <= w + 1).

@@ -167,7 +167,7 @@ struct biot_ctx {
     double **gm_Vdev = nullptr;
     double *gm_scratch = nullptr, *gm_small = nullptr;
     // Gauss-Seidel wavefront state (biot_gs_begin / biot_gs_wave / biot_gs_end)
-    int32_t gs_K = 0, gs_w = 0;
+    int32_t gs_K = 0, gs_w = 0, gs_k = 0;   // gs_k > 0: each window update is a GMRES(gs_k) cycle
     int64_t gs_k0 = 0;
     int32_t n1 = 0, z_rows = 0;
     int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
@@ -575,6 +575,190 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
     if (ctx->world > 1) ctx->send_dirty = false;   // the sweep (and pass 2) wrote the slice of x^{k+1}
+    return BIOT_OK;
+}
+
+}  // namespace
+
+// Per-step GMRES inside the inverted scheme (PAPER.md Alg. 3, P:L345-356, with K =
+// GMRES as the paper's experiments use, P:L460; reading R23): each outer iteration
+// runs, for every time step at once, one cycle of GMRES(k) on AA x_n = b_n from
+// x_n^{m-1}, left-preconditioned by the diagonal P~2, b_n = A' x_{n-1}^{m-1} + f_n
+// (Jacobi in time).  The N_t Krylov bases live in k+1 space-time panels; Arnoldi by
+// classical Gram-Schmidt with one reorthogonalisation (CGS2), every dot product and
+// update column-wise (one value per time step); the (k+1) x k least-squares problems
+// are solved on the host by Givens rotations.
+namespace {
+
+biot_status gmres_alloc(biot_ctx *ctx, int k) {
+    if ((int)ctx->gm_V.size() >= k + 1) return BIOT_OK;
+    const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult qres;
+    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
+    if (!fn || qres != cudaDriverEntryPointSuccess)
+        return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled not available");
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    uint32_t box[2];
+    biot::tile2d_box(box);
+    while ((int)ctx->gm_V.size() < k + 1) {
+        double *base = nullptr;
+        ALLOC(base, panel_bytes);
+        CU(cudaMemsetAsync(base, 0, panel_bytes, ctx->stream));
+        ctx->gm_Vbase.push_back(base);
+        ctx->gm_V.push_back(base + ctx->pad * ctx->nc * ctx->pitch);
+        CUtensorMap m;
+        cuuint64_t dims[2] = {(cuuint64_t)ctx->pitch, (cuuint64_t)ctx->rows_alloc};
+        cuuint64_t strides[1] = {(cuuint64_t)ctx->pitch * sizeof(double)};
+        cuuint32_t bx[2] = {box[0], box[1]};
+        cuuint32_t es[2] = {1, 1};
+        CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, bx, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (V) failed");
+        ctx->gm_tmap.push_back(m);
+    }
+    const int nv = (int)ctx->gm_V.size();
+    if (ctx->gm_Vdev) cudaFree(ctx->gm_Vdev);
+    ctx->gm_Vdev = nullptr;
+    ALLOC(ctx->gm_Vdev, nv * sizeof(double *));
+    CU(h2d(ctx, ctx->gm_Vdev, ctx->gm_V.data(), nv * sizeof(double *)));
+    int64_t chunk;
+    int chunks;
+    const int64_t scr = biot::gmres_dots_scratch(ctx->N * ctx->nc, ctx->n_tl, biot::gmres_max_vectors(), &chunk, &chunks);
+    if (ctx->gm_scratch) cudaFree(ctx->gm_scratch);
+    if (ctx->gm_small) cudaFree(ctx->gm_small);
+    ctx->gm_scratch = ctx->gm_small = nullptr;
+    ALLOC(ctx->gm_scratch, scr * sizeof(double));
+    ALLOC(ctx->gm_small, (size_t)(2 * biot::gmres_max_vectors() + 2) * ctx->n_tl * sizeof(double));
+    return BIOT_OK;
+}
+
+// Least squares min || beta e1 - H y || for the (k+1) x k upper Hessenberg H (column-major
+// H[i + j*(k+1)]) by Givens rotations; zero pivots (breakdown) give zero coefficients.
+void hessenberg_lsq(int k, std::vector<double> H, double beta, double *y) {
+    std::vector<double> g(k + 1, 0.0);
+    g[0] = beta;
+    const int ld = k + 1;
+    for (int j = 0; j < k; ++j) {
+        const double a = H[j + j * ld], b = H[j + 1 + j * ld];
+        const double rr = std::hypot(a, b);
+        if (rr == 0.0) continue;
+        const double c = a / rr, s = b / rr;
+        for (int jj = j; jj < k; ++jj) {
+            const double u = H[j + jj * ld], v = H[j + 1 + jj * ld];
+            H[j + jj * ld] = c * u + s * v;
+            H[j + 1 + jj * ld] = -s * u + c * v;
+        }
+        const double gu = g[j], gv = g[j + 1];
+        g[j] = c * gu + s * gv;
+        g[j + 1] = -s * gu + c * gv;
+    }
+    for (int j = k - 1; j >= 0; --j) {
+        double v = g[j];
+        for (int jj = j + 1; jj < k; ++jj) v -= H[j + jj * ld] * y[jj];
+        const double d = H[j + j * ld];
+        y[j] = (std::fabs(d) > 1e-300) ? v / d : 0.0;
+    }
+}
+
+}  // namespace
+
+namespace {
+
+// One GMRES(k) cycle for every step of a time window (R23): x_out = x_in + V y on
+// columns [t_off + t_lo, t_off + len), the residual (with its previous-step coupling and
+// norm partials) from panel xin through tensor map `tm`.  x_out may equal x_in.
+biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const double *xin, double *xout,
+                        const Window &win) {
+    const int64_t rows = ctx->N * ctx->nc;
+    const int c0 = win.t_off + win.t_lo, nt = win.len - win.t_lo;   // columns the cycle owns
+    double *d_h = ctx->gm_small;
+    double *d_scale = ctx->gm_small + (size_t)biot::gmres_max_vectors() * ctx->n_tl;
+    std::vector<double> h1((size_t)(k + 1) * nt), hn(nt), beta(nt), scale(nt);
+    std::vector<double> H((size_t)nt * (k + 1) * k, 0.0);   // per step, column-major (k+1) x k
+    std::vector<double> y((size_t)k * nt);
+    double *const *Vd = ctx->gm_Vdev;
+    auto dots = [&](const double *a, double *const *bdev, int nb, double *out_host) -> biot_status {
+        CU(biot::gmres_dots(a + c0, bdev, c0, nb, rows, ctx->pitch, nt, ctx->gm_scratch, d_h, ctx->stream));
+        CU(cudaMemcpyAsync(out_host, d_h, (size_t)nb * nt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return BIOT_OK;
+    };
+    auto combine = [&](double *dst, const double *base, const double *coef_host, int nb, double sign,
+                       const double *scale_host) -> biot_status {
+        if (nb > 0) CU(cudaMemcpyAsync(d_h, coef_host, (size_t)nb * nt * sizeof(double), cudaMemcpyHostToDevice,
+                                       ctx->stream));
+        if (scale_host)
+            CU(cudaMemcpyAsync(d_scale, scale_host, nt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        CU(biot::gmres_combine(dst + c0, base + c0, Vd, c0, d_h, nb, sign, scale_host ? d_scale : nullptr, rows,
+                               ctx->pitch, nt, ctx->stream));
+        return BIOT_OK;
+    };
+    auto tile_args = [&](int mode, const double *x, double *xn) {
+        biot::Tile2dArgs a{};
+        static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, x, xn);
+        std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
+        a.aux = ctx->aux;
+        a.cls = ctx->cls;
+        a.pad_nodes = ctx->pad;
+        a.s0 = ctx->s0;
+        a.sendbuf = nullptr;
+        a.t_off = win.t_off;
+        a.t_lo = win.t_lo;
+        a.n_tl = win.len;
+        a.ghost = win.ghost;
+        a.ghost_stride = win.stride;
+        return a;
+    };
+    // v_0 = P~2^{-1} (b - AA x_in) with b = A' x_prev + f, and the norms of b - AA x_in
+    {
+        biot::Tile2dArgs a = tile_args(biot::MODE_ZOUT, xin, nullptr);
+        a.zbuf = ctx->gm_V[0];
+        CU(biot::launch_tile2d(tm, a, ctx->shape, ctx->stream));
+    }
+    biot_status st = dots(ctx->gm_V[0], Vd, 1, beta.data());
+    if (st != BIOT_OK) return st;
+    for (int t = 0; t < nt; ++t) {
+        beta[t] = std::sqrt(beta[t]);
+        scale[t] = beta[t] > 0.0 ? 1.0 / beta[t] : 0.0;
+    }
+    if ((st = combine(ctx->gm_V[0], ctx->gm_V[0], nullptr, 0, 1.0, scale.data())) != BIOT_OK) return st;
+    for (int j = 0; j < k; ++j) {
+        // w = P~2^{-1} AA v_j into v_{j+1}
+        biot::Tile2dArgs a = tile_args(biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1]);
+        CU(biot::launch_tile2d(ctx->gm_tmap[j], a, ctx->shape, ctx->stream));
+        // CGS2: two passes of h = V^T w, w -= V h
+        for (int pass = 0; pass < 2; ++pass) {
+            if ((st = dots(ctx->gm_V[j + 1], Vd, j + 1, h1.data())) != BIOT_OK) return st;
+            for (int i = 0; i <= j; ++i)
+                for (int t = 0; t < nt; ++t) H[(size_t)t * (k + 1) * k + i + (size_t)j * (k + 1)] += h1[(size_t)i * nt + t];
+            if ((st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], h1.data(), j + 1, -1.0, nullptr)) != BIOT_OK)
+                return st;
+        }
+        if ((st = dots(ctx->gm_V[j + 1], Vd + (j + 1), 1, hn.data())) != BIOT_OK) return st;
+        for (int t = 0; t < nt; ++t) {
+            hn[t] = std::sqrt(hn[t]);
+            H[(size_t)t * (k + 1) * k + (j + 1) + (size_t)j * (k + 1)] = hn[t];
+            scale[t] = hn[t] > 0.0 ? 1.0 / hn[t] : 0.0;
+        }
+        if ((st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], nullptr, 0, 1.0, scale.data())) != BIOT_OK) return st;
+    }
+    // y_t = argmin || beta_t e1 - H_t y ||, x_out = x_in + V y
+    for (int t = 0; t < nt; ++t) {
+        std::vector<double> Ht(H.begin() + (size_t)t * (k + 1) * k, H.begin() + (size_t)(t + 1) * (k + 1) * k);
+        double yt[32];
+        hessenberg_lsq(k, Ht, beta[t], yt);
+        for (int j = 0; j < k; ++j) y[(size_t)j * nt + t] = yt[j];
+    }
+    return combine(xout, xin, y.data(), k, 1.0, nullptr);
+}
+
+biot_status gmres_check(biot_ctx *ctx, int32_t K, int32_t k) {
+    if (K < 0 || k < 1 || k > biot::gmres_max_vectors() - 1)
+        return fail(ctx, BIOT_E_INVALID, "need K >= 0 and 1 <= k <= " + std::to_string(biot::gmres_max_vectors() - 1));
+    if (ctx->kern != 4) return fail(ctx, BIOT_E_STATE, "per-step GMRES needs the 2D tile kernel (structured 2D mesh)");
+    if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "per-step GMRES is left-preconditioned by P~2 (precond = 2)");
     return BIOT_OK;
 }
 
@@ -1196,9 +1380,17 @@ biot_status gs_run_wave(biot_ctx *ctx) {
         win.stride = ctx->pitch;
     }
     win.send = (ctx->world > 1 && hi == L - 1) ? ctx->sendbuf : nullptr;
-    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
-    CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
-    if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
+    if (ctx->gs_k > 0) {   // Alg. 3 literal: a GMRES(k) cycle per step of the window
+        biot_status st = gmres_cycle(ctx, ctx->gs_k, ctx->tmap[r], ctx->x[r], ctx->x[1 - r], win);
+        if (st != BIOT_OK) return st;
+        if (win.send)      // the slice of the slab's last step for the next slab
+            CU(cudaMemcpy2DAsync(win.send, sizeof(double), ctx->x[1 - r] + (L - 1), ctx->pitch * sizeof(double),
+                                 sizeof(double), (size_t)ctx->N * ctx->nc, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+        const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+        CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
+        if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
+    }
     CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, ctx->gs_k0 + w - g0,
                                   ctx->hist_cap, L, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
     if (win.send) ctx->send_dirty = false;
@@ -1207,14 +1399,21 @@ biot_status gs_run_wave(biot_ctx *ctx) {
 
 }  // namespace
 
-biot_status biot_gs_begin(biot_ctx *ctx, int32_t K) {
+biot_status biot_gs_begin_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (k > 0) {
+        biot_status st = gmres_check(ctx, K, k);
+        if (st != BIOT_OK) return st;
+        CU(cudaSetDevice(ctx->device));
+        if ((st = gmres_alloc(ctx, k)) != BIOT_OK) return st;
+    }
     if (K < 1) return fail(ctx, BIOT_E_INVALID, "K must be >= 1");
     if (ctx->kern != 4 && ctx->kern != 6)
         return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs a tile kernel (structured 2D / 3D mesh)");
     if (ctx->gs_K) return fail(ctx, BIOT_E_STATE, "a Gauss-Seidel run is already open");
     CU(cudaSetDevice(ctx->device));
     ctx->gs_K = K;
+    ctx->gs_k = k;
     ctx->gs_w = 0;
     ctx->gs_k0 = ctx->iterations;
     ctx->send_dirty = true;
@@ -1222,6 +1421,8 @@ biot_status biot_gs_begin(biot_ctx *ctx, int32_t K) {
     // global step g0 + t starts in panel (cur + g0 + t) % 2
     return gs_parity_copy(ctx, ctx->x[ctx->cur], ctx->x[1 - ctx->cur], (ctx->first_step - 1) % 2 == 0 ? 1 : 0);
 }
+
+biot_status biot_gs_begin(biot_ctx *ctx, int32_t K) { return biot_gs_begin_gmres(ctx, K, 0); }
 
 biot_status biot_gs_waves(const biot_ctx *ctx, int32_t *out) {
     if (!ctx || !out) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
@@ -1255,6 +1456,7 @@ biot_status biot_gs_end(biot_ctx *ctx) {
     ctx->last_ms_sweep = tot / K;
     ctx->iterations += K;
     ctx->gs_K = 0;
+    ctx->gs_k = 0;
     ctx->send_dirty = true;
     int nf = 0;
     CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1263,7 +1465,7 @@ biot_status biot_gs_end(biot_ctx *ctx) {
     return BIOT_OK;
 }
 
-biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
+biot_status biot_iterate_gs_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
     if (K == 0) return BIOT_OK;
@@ -1271,7 +1473,7 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
         return fail(ctx, BIOT_E_STATE, "manual halo: drive the waves with biot_gs_begin/wave/end");
     NcclApi *api = ctx->world > 1 ? nccl() : nullptr;
     if (ctx->world > 1 && (!api || !ctx->comm)) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
-    biot_status st = biot_gs_begin(ctx, K);
+    biot_status st = biot_gs_begin_gmres(ctx, K, k);
     if (st != BIOT_OK) return st;
     const size_t n = (size_t)ctx->N * ctx->nc;
     for (int w = 0; w < ctx->n_t + K - 1; ++w) {
@@ -1290,195 +1492,25 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) {
     return biot_gs_end(ctx);
 }
 
-// Per-step GMRES inside the inverted scheme (PAPER.md Alg. 3, P:L345-356, with K =
-// GMRES as the paper's experiments use, P:L460; reading R23): each outer iteration
-// runs, for every time step at once, one cycle of GMRES(k) on AA x_n = b_n from
-// x_n^{m-1}, left-preconditioned by the diagonal P~2, b_n = A' x_{n-1}^{m-1} + f_n
-// (Jacobi in time).  The N_t Krylov bases live in k+1 space-time panels; Arnoldi by
-// classical Gram-Schmidt with one reorthogonalisation (CGS2), every dot product and
-// update column-wise (one value per time step); the (k+1) x k least-squares problems
-// are solved on the host by Givens rotations.
-namespace {
-
-biot_status gmres_alloc(biot_ctx *ctx, int k) {
-    if ((int)ctx->gm_V.size() >= k + 1) return BIOT_OK;
-    const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
-    void *fn = nullptr;
-    cudaDriverEntryPointQueryResult qres;
-    CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
-    if (!fn || qres != cudaDriverEntryPointSuccess)
-        return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled not available");
-    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    uint32_t box[2];
-    biot::tile2d_box(box);
-    while ((int)ctx->gm_V.size() < k + 1) {
-        double *base = nullptr;
-        ALLOC(base, panel_bytes);
-        CU(cudaMemsetAsync(base, 0, panel_bytes, ctx->stream));
-        ctx->gm_Vbase.push_back(base);
-        ctx->gm_V.push_back(base + ctx->pad * ctx->nc * ctx->pitch);
-        CUtensorMap m;
-        cuuint64_t dims[2] = {(cuuint64_t)ctx->pitch, (cuuint64_t)ctx->rows_alloc};
-        cuuint64_t strides[1] = {(cuuint64_t)ctx->pitch * sizeof(double)};
-        cuuint32_t bx[2] = {box[0], box[1]};
-        cuuint32_t es[2] = {1, 1};
-        CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, bx, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS) return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (V) failed");
-        ctx->gm_tmap.push_back(m);
-    }
-    const int nv = (int)ctx->gm_V.size();
-    if (ctx->gm_Vdev) cudaFree(ctx->gm_Vdev);
-    ctx->gm_Vdev = nullptr;
-    ALLOC(ctx->gm_Vdev, nv * sizeof(double *));
-    CU(h2d(ctx, ctx->gm_Vdev, ctx->gm_V.data(), nv * sizeof(double *)));
-    int64_t chunk;
-    int chunks;
-    const int64_t scr = biot::gmres_dots_scratch(ctx->N * ctx->nc, ctx->n_tl, biot::gmres_max_vectors(), &chunk, &chunks);
-    if (ctx->gm_scratch) cudaFree(ctx->gm_scratch);
-    if (ctx->gm_small) cudaFree(ctx->gm_small);
-    ctx->gm_scratch = ctx->gm_small = nullptr;
-    ALLOC(ctx->gm_scratch, scr * sizeof(double));
-    ALLOC(ctx->gm_small, (size_t)(2 * biot::gmres_max_vectors() + 2) * ctx->n_tl * sizeof(double));
-    return BIOT_OK;
-}
-
-// Least squares min || beta e1 - H y || for the (k+1) x k upper Hessenberg H (column-major
-// H[i + j*(k+1)]) by Givens rotations; zero pivots (breakdown) give zero coefficients.
-void hessenberg_lsq(int k, std::vector<double> H, double beta, double *y) {
-    std::vector<double> g(k + 1, 0.0);
-    g[0] = beta;
-    const int ld = k + 1;
-    for (int j = 0; j < k; ++j) {
-        const double a = H[j + j * ld], b = H[j + 1 + j * ld];
-        const double rr = std::hypot(a, b);
-        if (rr == 0.0) continue;
-        const double c = a / rr, s = b / rr;
-        for (int jj = j; jj < k; ++jj) {
-            const double u = H[j + jj * ld], v = H[j + 1 + jj * ld];
-            H[j + jj * ld] = c * u + s * v;
-            H[j + 1 + jj * ld] = -s * u + c * v;
-        }
-        const double gu = g[j], gv = g[j + 1];
-        g[j] = c * gu + s * gv;
-        g[j + 1] = -s * gu + c * gv;
-    }
-    for (int j = k - 1; j >= 0; --j) {
-        double v = g[j];
-        for (int jj = j + 1; jj < k; ++jj) v -= H[j + jj * ld] * y[jj];
-        const double d = H[j + j * ld];
-        y[j] = (std::fabs(d) > 1e-300) ? v / d : 0.0;
-    }
-}
-
-}  // namespace
+biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) { return biot_iterate_gs_gmres(ctx, K, 0); }
 
 biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
-    if (K < 0 || k < 1 || k > biot::gmres_max_vectors() - 1)
-        return fail(ctx, BIOT_E_INVALID, "need K >= 0 and 1 <= k <= " + std::to_string(biot::gmres_max_vectors() - 1));
-    if (ctx->kern != 4) return fail(ctx, BIOT_E_STATE, "per-step GMRES needs the 2D tile kernel (structured 2D mesh)");
-    if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "per-step GMRES is left-preconditioned by P~2 (precond = 2)");
-    if (K == 0) return BIOT_OK;
+    biot_status st = gmres_check(ctx, K, k);
+    if (st != BIOT_OK || K == 0) return st;
     CU(cudaSetDevice(ctx->device));
-    biot_status st = gmres_alloc(ctx, k);
-    if (st != BIOT_OK) return st;
-    const int nt = ctx->n_tl;
-    const int64_t rows = ctx->N * ctx->nc;
-    double *d_h = ctx->gm_small;                                   // [<= kMaxVec][nt] coefficients
-    double *d_scale = ctx->gm_small + (size_t)biot::gmres_max_vectors() * nt;   // [nt]
-    std::vector<double> h1((size_t)(k + 1) * nt), hn(nt), beta(nt), scale(nt);
-    std::vector<double> H((size_t)nt * (k + 1) * k);               // per step, column-major (k+1) x k
-    std::vector<double> y((size_t)k * nt);
-    auto dots = [&](const double *a, double *const *bdev, int nb, double *out_host) -> biot_status {
-        CU(biot::gmres_dots(a, bdev, nb, rows, ctx->pitch, nt, ctx->gm_scratch, d_h, ctx->stream));
-        CU(cudaMemcpyAsync(out_host, d_h, (size_t)nb * nt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        return BIOT_OK;
-    };
-    auto combine = [&](double *dst, const double *base, double *const *bdev, const double *coef_host, int nb,
-                       double sign, const double *scale_host) -> biot_status {
-        if (nb > 0) CU(cudaMemcpyAsync(d_h, coef_host, (size_t)nb * nt * sizeof(double), cudaMemcpyHostToDevice,
-                                       ctx->stream));
-        if (scale_host)
-            CU(cudaMemcpyAsync(d_scale, scale_host, nt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(biot::gmres_combine(dst, base, bdev, d_h, nb, sign, scale_host ? d_scale : nullptr, rows, ctx->pitch, nt,
-                               ctx->stream));
-        return BIOT_OK;
-    };
-    double *const *Vd = ctx->gm_Vdev;
+    if ((st = gmres_alloc(ctx, k)) != BIOT_OK) return st;
     CU(cudaEventRecord(ctx->ev_a, ctx->stream));
     for (int32_t it = 0; it < K; ++it) {
-        st = halo_exchange(ctx);
-        if (st != BIOT_OK) return st;
+        if ((st = halo_exchange(ctx)) != BIOT_OK) return st;
+        Window win;
+        win.len = ctx->n_tl;
+        win.ghost = ctx->ghost;
         double *x = ctx->x[ctx->cur];
-        // v_0 = P~2^{-1} (b - AA x) and the norms of b - AA x (history)
-        {
-            biot::Tile2dArgs a{};
-            static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, biot::MODE_ZOUT, x, nullptr);
-            std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
-            a.aux = ctx->aux;
-            a.cls = ctx->cls;
-            a.pad_nodes = ctx->pad;
-            a.ghost_stride = 1;
-            a.s0 = ctx->s0;
-            a.zbuf = ctx->gm_V[0];
-            a.sendbuf = nullptr;
-            CU(biot::launch_tile2d(ctx->tmap[ctx->cur], a, ctx->shape, ctx->stream));
-            double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * nt * 2;
-            CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, nt, hslot, ctx->nonfinite, ctx->fin_scratch,
-                                     ctx->stream));
-        }
-        st = dots(ctx->gm_V[0], Vd, 1, beta.data());
-        if (st != BIOT_OK) return st;
-        for (int t = 0; t < nt; ++t) {
-            beta[t] = std::sqrt(beta[t]);
-            scale[t] = beta[t] > 0.0 ? 1.0 / beta[t] : 0.0;
-        }
-        st = combine(ctx->gm_V[0], ctx->gm_V[0], Vd, nullptr, 0, 1.0, scale.data());
-        if (st != BIOT_OK) return st;
-        std::fill(H.begin(), H.end(), 0.0);
-        for (int j = 0; j < k; ++j) {
-            // w = P~2^{-1} AA v_j into v_{j+1}
-            biot::Tile2dArgs a{};
-            static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1]);
-            std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
-            a.aux = ctx->aux;
-            a.cls = ctx->cls;
-            a.pad_nodes = ctx->pad;
-            a.ghost_stride = 1;
-            a.s0 = ctx->s0;
-            a.sendbuf = nullptr;
-            CU(biot::launch_tile2d(ctx->gm_tmap[j], a, ctx->shape, ctx->stream));
-            // CGS2: two passes of h = V^T w, w -= V h
-            for (int pass = 0; pass < 2; ++pass) {
-                st = dots(ctx->gm_V[j + 1], Vd, j + 1, h1.data());
-                if (st != BIOT_OK) return st;
-                for (int i = 0; i <= j; ++i)
-                    for (int t = 0; t < nt; ++t) H[(size_t)t * (k + 1) * k + i + (size_t)j * (k + 1)] += h1[(size_t)i * nt + t];
-                st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], Vd, h1.data(), j + 1, -1.0, nullptr);
-                if (st != BIOT_OK) return st;
-            }
-            st = dots(ctx->gm_V[j + 1], Vd + (j + 1), 1, hn.data());
-            if (st != BIOT_OK) return st;
-            for (int t = 0; t < nt; ++t) {
-                hn[t] = std::sqrt(hn[t]);
-                H[(size_t)t * (k + 1) * k + (j + 1) + (size_t)j * (k + 1)] = hn[t];
-                scale[t] = hn[t] > 0.0 ? 1.0 / hn[t] : 0.0;
-            }
-            st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], Vd, nullptr, 0, 1.0, scale.data());
-            if (st != BIOT_OK) return st;
-        }
-        // y_t = argmin || beta_t e1 - H_t y ||, x += V y
-        for (int t = 0; t < nt; ++t) {
-            std::vector<double> Ht(H.begin() + (size_t)t * (k + 1) * k, H.begin() + (size_t)(t + 1) * (k + 1) * k);
-            double yt[32];
-            hessenberg_lsq(k, Ht, beta[t], yt);
-            for (int j = 0; j < k; ++j) y[(size_t)j * nt + t] = yt[j];
-        }
-        st = combine(x, x, Vd, y.data(), k, 1.0, nullptr);
-        if (st != BIOT_OK) return st;
+        if ((st = gmres_cycle(ctx, k, ctx->tmap[ctx->cur], x, x, win)) != BIOT_OK) return st;
+        double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
+        CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite, ctx->fin_scratch,
+                                 ctx->stream));
         ctx->send_dirty = true;
         ctx->iterations++;
     }

@@ -19,7 +19,7 @@ constexpr int kMaxVec = 17;   // Krylov vectors a dot / combine call may touch (
 // Stage 1: block (column block bx, row chunk by) sums rows [by*chunk, ..) of
 // a[row][t] * b_i[row][t] for i < nb, in a fixed split over the kRowsY row lanes,
 // then in fixed lane order; out[(by * nb + i) * n_tl + t].
-__global__ void dots_stage1(const double *__restrict__ a, const double *const *__restrict__ b, int nb,
+__global__ void dots_stage1(const double *__restrict__ a, const double *const *__restrict__ b, int boff, int nb,
                             int64_t rows, int64_t pitch, int n_tl, int64_t chunk, double *__restrict__ out) {
     __shared__ double sm[kRowsY][kMaxVec][kCols];
     const int t = blockIdx.x * kCols + threadIdx.x;
@@ -32,7 +32,7 @@ __global__ void dots_stage1(const double *__restrict__ a, const double *const *_
             const double av = a[r * pitch + t];
 #pragma unroll
             for (int i = 0; i < kMaxVec; ++i)
-                if (i < nb) acc[i] = fma(av, b[i][r * pitch + t], acc[i]);
+                if (i < nb) acc[i] = fma(av, b[i][r * pitch + boff + t], acc[i]);
         }
     }
 #pragma unroll
@@ -58,9 +58,9 @@ __global__ void dots_stage2(const double *__restrict__ part, int chunks, int nb,
     out[(int64_t)i * n_tl + t] = s;
 }
 
-// dst[row][t] = scale[t] * (base[row][t] + sign * sum_i coef[i][t] * b_i[row][t])
+// dst[row][t] = scale[t] * (base[row][t] + sign * sum_i coef[i][t] * b_i[row][boff + t])
 // (scale == nullptr: 1; base may alias dst).
-__global__ void combine_kernel(double *dst, const double *base, const double *const *__restrict__ b,
+__global__ void combine_kernel(double *dst, const double *base, const double *const *__restrict__ b, int boff,
                                const double *__restrict__ coef, int nb, double sign,
                                const double *__restrict__ scale, int64_t rows, int64_t pitch, int n_tl) {
     const int t = blockIdx.x * kCols + threadIdx.x;
@@ -73,7 +73,7 @@ __global__ void combine_kernel(double *dst, const double *base, const double *co
         double v = base[r * pitch + t];
 #pragma unroll
         for (int i = 0; i < kMaxVec; ++i)
-            if (i < nb) v = fma(c[i], b[i][r * pitch + t], v);
+            if (i < nb) v = fma(c[i], b[i][r * pitch + boff + t], v);
         dst[r * pitch + t] = sc * v;
     }
 }
@@ -91,25 +91,26 @@ int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *
     return (int64_t)(*chunks) * nb * n_tl;
 }
 
-cudaError_t gmres_dots(const double *a, const double *const *b_dev, int nb, int64_t rows, int64_t pitch, int n_tl,
-                       double *scratch, double *out, cudaStream_t st) {
+cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, int nb, int64_t rows, int64_t pitch,
+                       int n_tl, double *scratch, double *out, cudaStream_t st) {
     if (nb < 1 || nb > kMaxVec) return cudaErrorInvalidValue;
     int64_t chunk;
     int chunks;
     gmres_dots_scratch(rows, n_tl, nb, &chunk, &chunks);
-    dots_stage1<<<dim3((n_tl + kCols - 1) / kCols, chunks), dim3(kCols, kRowsY), 0, st>>>(a, b_dev, nb, rows, pitch,
-                                                                                          n_tl, chunk, scratch);
+    dots_stage1<<<dim3((n_tl + kCols - 1) / kCols, chunks), dim3(kCols, kRowsY), 0, st>>>(a, b_dev, boff, nb, rows,
+                                                                                          pitch, n_tl, chunk, scratch);
     const int64_t n = (int64_t)nb * n_tl;
     dots_stage2<<<(int)((n + 255) / 256), 256, 0, st>>>(scratch, chunks, nb, n_tl, out);
     return cudaGetLastError();
 }
 
-cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, const double *coef, int nb,
-                          double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl, cudaStream_t st) {
+cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, int boff, const double *coef,
+                          int nb, double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl,
+                          cudaStream_t st) {
     if (nb < 0 || nb > kMaxVec) return cudaErrorInvalidValue;
     const int gy = (int)((rows + 7) / 8 < 4096 ? (rows + 7) / 8 : 4096);
-    combine_kernel<<<dim3((n_tl + kCols - 1) / kCols, gy), dim3(kCols, 8), 0, st>>>(dst, base, b_dev, coef, nb, sign,
-                                                                                    scale, rows, pitch, n_tl);
+    combine_kernel<<<dim3((n_tl + kCols - 1) / kCols, gy), dim3(kCols, 8), 0, st>>>(dst, base, b_dev, boff, coef, nb,
+                                                                                    sign, scale, rows, pitch, n_tl);
     return cudaGetLastError();
 }
 

@@ -149,10 +149,12 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
 // dst = scale_t * (base + sign * sum_i coef[i][t] b_i); rows = real panel rows.
 int gmres_max_vectors();
 int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *chunks);
-cudaError_t gmres_dots(const double *a, const double *const *b_dev, int nb, int64_t rows, int64_t pitch, int n_tl,
-                       double *scratch, double *out, cudaStream_t st);
-cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, const double *coef, int nb,
-                          double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl, cudaStream_t st);
+// (boff: column offset applied to the b panels -- a time window of them)
+cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, int nb, int64_t rows, int64_t pitch,
+                       int n_tl, double *scratch, double *out, cudaStream_t st);
+cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, int boff, const double *coef,
+                          int nb, double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl,
+                          cudaStream_t st);
 
 bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);

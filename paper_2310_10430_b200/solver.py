@@ -81,8 +81,11 @@ class BiotSolver:
     def iterate_gmres(self, K, k):
         check(self.lib.biot_iterate_gmres(self.ctx, K, k), self.ctx)
 
-    def gs_begin(self, K):
-        check(self.lib.biot_gs_begin(self.ctx, K), self.ctx)
+    def iterate_gs_gmres(self, K, k):
+        check(self.lib.biot_iterate_gs_gmres(self.ctx, K, k), self.ctx)
+
+    def gs_begin(self, K, gmres_k=0):
+        check(self.lib.biot_gs_begin_gmres(self.ctx, K, gmres_k), self.ctx)
         n = ctypes.c_int32()
         check(self.lib.biot_gs_waves(self.ctx, ctypes.byref(n)), self.ctx)
         return n.value

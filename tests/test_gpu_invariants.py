@@ -213,3 +213,25 @@ def test_gs_time_slabs_bitwise(dim, world):
     assert np.array_equal(xs, xr)
     hs = np.concatenate([np.concatenate([g.residual_history(k) for g in ranks]) for k in range(K)])
     assert np.allclose(hs, hr, rtol=1e-12, atol=0)
+
+
+def test_gs_gmres_time_slabs_bitwise():
+    """Alg. 3 (Gauss-Seidel + GMRES) split over two time slabs equals one slab bitwise."""
+    prob = config_problem(1)
+    nt, K, k, world = prob.n_t, 4, 3, 2
+    ref = _seeded(prob, nt, precond=2)
+    ref.iterate_gs_gmres(K, k)
+    xr = ref.solution()
+    ranks = [_seeded(prob, nt, precond=2, rank=r, world=world, flags=FLAG_MANUAL_HALO) for r in range(world)]
+    waves = [g.gs_begin(K, k) for g in ranks][0]
+    for w in range(waves):
+        slices = [g.last_slice() for g in ranks]
+        for r in range(1, world):
+            first = ranks[r].first_step
+            if w - K + 2 <= first <= w + 1:
+                ranks[r].set_ghost(slices[r - 1])
+        for g in ranks:
+            g.gs_wave()
+    for g in ranks:
+        g.gs_end()
+    assert np.array_equal(np.concatenate([g.solution() for g in ranks]), xr)

@@ -306,3 +306,51 @@ def test_gmres_parity_config2():
     (xg, hg), (xo, ho) = _gmres_pair(prob, 64, 2, 4)
     assert field_errors(xg, xo, 2).max() < TOL
     assert norm_errors(hg, ho).max() < TOL
+
+
+def _gs_gmres_pair(prob, nt, K, k):
+    from oracle import gmres as ogm
+    s = load_scales(nt, parity=True)
+    x0 = _x0(prob, np.arange(1, nt + 1))
+    g = BiotSolver(prob, n_t=nt, precond=2, omega=0.5, load_scale=s)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate_gs_gmres(K, k)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(kk) for kk in range(K)])
+    finally:
+        g.close()
+    S = oracle.OracleSystem(prob)
+    X = np.zeros((nt + 1, S.ndof))
+    X[1:] = S.to_paper(x0)
+    Xo, ho = ogm.iterate(S, X, s, K, k, gauss_seidel=True)
+    return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho)
+
+
+@pytest.mark.parametrize("nt,K,k", [(32, 3, 4), (5, 7, 3)])
+def test_gs_gmres_parity_config1(nt, K, k):
+    """Alg. 3 literally (Gauss-Seidel in time, GMRES(k) per step) on the wavefront vs the
+    oracle: x^K and every update's residual at 1e-9."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gs_gmres_pair(prob, nt, K, k)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_gs_gmres_exact_solves_are_backward_euler_in_one_sweep():
+    """with exact per-step solves (k >= the free DoFs) ONE Gauss-Seidel sweep of
+    Alg. 3 is the sequential backward-Euler solution (checked on the GPU)."""
+    from oracle import extras
+    prob = make_problem(2, 2, 6, 1.0 / 6, 1, storage=1e-3, kappa_median=1e-2)
+    S = oracle.OracleSystem(prob)
+    assert (S.free > 0).sum() <= 16
+    s = load_scales(6, parity=True)
+    g = BiotSolver(prob, precond=2, omega=0.5, load_scale=s)
+    try:
+        g.iterate_gs_gmres(1, 16)
+        xg = g.solution()
+    finally:
+        g.close()
+    Xbe = extras.sequential_be(S, np.zeros(S.ndof), s, 6)
+    xbe = np.stack([S.from_paper(v) for v in Xbe[1:]])
+    assert field_errors(xg, xbe, 2).max() < 1e-9
