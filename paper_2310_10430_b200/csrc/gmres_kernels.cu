@@ -17,33 +17,40 @@ constexpr int kRowsY = 4;     // row lanes per block
 constexpr int kMaxVec = 17;   // Krylov vectors a dot / combine call may touch (k <= 16)
 
 // Stage 1: block (column block bx, row chunk by) sums rows [by*chunk, ..) of
-// a[row][t] * b_i[row][t] for i < nb, in a fixed split over the kRowsY row lanes,
-// then in fixed lane order; out[(by * nb + i) * n_tl + t].
-__global__ void dots_stage1(const double *__restrict__ a, const double *const *__restrict__ b, int boff, int nb,
-                            int64_t rows, int64_t pitch, int n_tl, int64_t chunk, double *__restrict__ out) {
-    __shared__ double sm[kRowsY][kMaxVec][kCols];
+// a[row][t] * b_i[row][boff + t] for i < NB, in a fixed split over the kRowsY row lanes,
+// then in fixed lane order; out[(by * NB + i) * n_tl + t].  NB is a template parameter
+// so the loads of one row are issued together (no predicates), 4 rows per iteration.
+template <int NB>
+__global__ void __launch_bounds__(kCols * kRowsY)
+    dots_stage1(const double *__restrict__ a, const double *const *__restrict__ b, int boff, int64_t rows,
+                int64_t pitch, int n_tl, int64_t chunk, double *__restrict__ out) {
+    extern __shared__ double sm[];   // [kRowsY][NB][kCols]
     const int t = blockIdx.x * kCols + threadIdx.x;
     const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
-    double acc[kMaxVec];
+    const double *bp[NB];
 #pragma unroll
-    for (int i = 0; i < kMaxVec; ++i) acc[i] = 0.0;
+    for (int i = 0; i < NB; ++i) bp[i] = b[i] + boff;
+    double acc[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc[i] = 0.0;
     if (t < n_tl) {
+#pragma unroll 4
         for (int64_t r = r0 + threadIdx.y; r < r1; r += kRowsY) {
-            const double av = a[r * pitch + t];
+            const int64_t o = r * pitch + t;
+            const double av = a[o];
 #pragma unroll
-            for (int i = 0; i < kMaxVec; ++i)
-                if (i < nb) acc[i] = fma(av, b[i][r * pitch + boff + t], acc[i]);
+            for (int i = 0; i < NB; ++i) acc[i] = fma(av, bp[i][o], acc[i]);
         }
     }
 #pragma unroll
-    for (int i = 0; i < kMaxVec; ++i)
-        if (i < nb) sm[threadIdx.y][i][threadIdx.x] = acc[i];
+    for (int i = 0; i < NB; ++i) sm[(threadIdx.y * NB + i) * kCols + threadIdx.x] = acc[i];
     __syncthreads();
     if (threadIdx.y == 0 && t < n_tl) {
-        for (int i = 0; i < nb; ++i) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
             double s = 0.0;
-            for (int y = 0; y < kRowsY; ++y) s += sm[y][i][threadIdx.x];
-            out[((int64_t)blockIdx.y * nb + i) * n_tl + t] = s;
+            for (int y = 0; y < kRowsY; ++y) s += sm[(y * NB + i) * kCols + threadIdx.x];
+            out[((int64_t)blockIdx.y * NB + i) * n_tl + t] = s;
         }
     }
 }
@@ -60,21 +67,28 @@ __global__ void dots_stage2(const double *__restrict__ part, int chunks, int nb,
 
 // dst[row][t] = scale[t] * (base[row][t] + sign * sum_i coef[i][t] * b_i[row][boff + t])
 // (scale == nullptr: 1; base may alias dst).
-__global__ void combine_kernel(double *dst, const double *base, const double *const *__restrict__ b, int boff,
-                               const double *__restrict__ coef, int nb, double sign,
-                               const double *__restrict__ scale, int64_t rows, int64_t pitch, int n_tl) {
+template <int NB>
+__global__ void __launch_bounds__(kCols * 8)
+    combine_kernel(double *dst, const double *base, const double *const *__restrict__ b, int boff,
+                   const double *__restrict__ coef, double sign, const double *__restrict__ scale, int64_t rows,
+                   int64_t pitch, int n_tl) {
     const int t = blockIdx.x * kCols + threadIdx.x;
     if (t >= n_tl) return;
-    double c[kMaxVec];
+    double c[NB > 0 ? NB : 1];
+    const double *bp[NB > 0 ? NB : 1];
 #pragma unroll
-    for (int i = 0; i < kMaxVec; ++i) c[i] = i < nb ? sign * coef[(int64_t)i * n_tl + t] : 0.0;
+    for (int i = 0; i < NB; ++i) {
+        c[i] = sign * coef[(int64_t)i * n_tl + t];
+        bp[i] = b[i] + boff;
+    }
     const double sc = scale ? scale[t] : 1.0;
+#pragma unroll 2
     for (int64_t r = blockIdx.y * (int64_t)blockDim.y + threadIdx.y; r < rows; r += (int64_t)gridDim.y * blockDim.y) {
-        double v = base[r * pitch + t];
+        const int64_t o = r * pitch + t;
+        double v = base[o];
 #pragma unroll
-        for (int i = 0; i < kMaxVec; ++i)
-            if (i < nb) v = fma(c[i], b[i][r * pitch + boff + t], v);
-        dst[r * pitch + t] = sc * v;
+        for (int i = 0; i < NB; ++i) v = fma(c[i], bp[i][o], v);
+        dst[o] = sc * v;
     }
 }
 
@@ -97,8 +111,14 @@ cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, in
     int64_t chunk;
     int chunks;
     gmres_dots_scratch(rows, n_tl, nb, &chunk, &chunks);
-    dots_stage1<<<dim3((n_tl + kCols - 1) / kCols, chunks), dim3(kCols, kRowsY), 0, st>>>(a, b_dev, boff, nb, rows,
-                                                                                          pitch, n_tl, chunk, scratch);
+    const dim3 g1((n_tl + kCols - 1) / kCols, chunks), b1(kCols, kRowsY);
+    const size_t sh = (size_t)kRowsY * nb * kCols * sizeof(double);
+    switch (nb) {
+#define BIOT_D(N) case N: dots_stage1<N><<<g1, b1, sh, st>>>(a, b_dev, boff, rows, pitch, n_tl, chunk, scratch); break;
+        BIOT_D(1) BIOT_D(2) BIOT_D(3) BIOT_D(4) BIOT_D(5) BIOT_D(6) BIOT_D(7) BIOT_D(8) BIOT_D(9)
+        BIOT_D(10) BIOT_D(11) BIOT_D(12) BIOT_D(13) BIOT_D(14) BIOT_D(15) BIOT_D(16) BIOT_D(17)
+#undef BIOT_D
+    }
     const int64_t n = (int64_t)nb * n_tl;
     dots_stage2<<<(int)((n + 255) / 256), 256, 0, st>>>(scratch, chunks, nb, n_tl, out);
     return cudaGetLastError();
@@ -109,8 +129,13 @@ cudaError_t gmres_combine(double *dst, const double *base, const double *const *
                           cudaStream_t st) {
     if (nb < 0 || nb > kMaxVec) return cudaErrorInvalidValue;
     const int gy = (int)((rows + 7) / 8 < 4096 ? (rows + 7) / 8 : 4096);
-    combine_kernel<<<dim3((n_tl + kCols - 1) / kCols, gy), dim3(kCols, 8), 0, st>>>(dst, base, b_dev, boff, coef, nb,
-                                                                                    sign, scale, rows, pitch, n_tl);
+    const dim3 g2((n_tl + kCols - 1) / kCols, gy), b2(kCols, 8);
+    switch (nb) {
+#define BIOT_C(N) case N: combine_kernel<N><<<g2, b2, 0, st>>>(dst, base, b_dev, boff, coef, sign, scale, rows, pitch, n_tl); break;
+        BIOT_C(0) BIOT_C(1) BIOT_C(2) BIOT_C(3) BIOT_C(4) BIOT_C(5) BIOT_C(6) BIOT_C(7) BIOT_C(8) BIOT_C(9)
+        BIOT_C(10) BIOT_C(11) BIOT_C(12) BIOT_C(13) BIOT_C(14) BIOT_C(15) BIOT_C(16) BIOT_C(17)
+#undef BIOT_C
+    }
     return cudaGetLastError();
 }
 
