@@ -62,12 +62,12 @@ def lib():
         L.oracle_iterate.restype = ctypes.c_int
         L.oracle_iterate.argtypes = ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32]
                                      + [_i64, _i32, _d] * 3
-                                     + [_d, _d, _d, _d, ctypes.c_int32, ctypes.c_double, _d, _d,
+                                     + [ctypes.c_int32, _d, _d, _d, _d, ctypes.c_int32, ctypes.c_double, _d, _d,
                                         ctypes.c_int32])
         L.oracle_residual_norms.restype = ctypes.c_int
         L.oracle_residual_norms.argtypes = ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int32]
                                             + [_i64, _i32, _d] * 2
-                                            + [_d, _d, _d, _d, _d, ctypes.c_int32])
+                                            + [ctypes.c_int32, _d, _d, _d, _d, _d, ctypes.c_int32])
         _lib = L
     return _lib
 
@@ -165,12 +165,55 @@ def traction_load(dim, coords, facets, traction) -> np.ndarray:
     return F
 
 
+# Quadrature of the source loads (reading R24): barycentric points, weights relative to
+# the cell measure.  Triangles: the symmetric 7-point rule exact for degree 5
+# (Strang & Fix / Dunavant); tetrahedra: the symmetric 4-point degree-2 rule.
+_TRI7_A1, _TRI7_B1 = 0.059715871789770, 0.470142064105115
+_TRI7_A2, _TRI7_B2 = 0.797426985353087, 0.101286507323456
+_QUAD = {
+    2: (np.array([[1 / 3, 1 / 3, 1 / 3],
+                  [_TRI7_A1, _TRI7_B1, _TRI7_B1], [_TRI7_B1, _TRI7_A1, _TRI7_B1], [_TRI7_B1, _TRI7_B1, _TRI7_A1],
+                  [_TRI7_A2, _TRI7_B2, _TRI7_B2], [_TRI7_B2, _TRI7_A2, _TRI7_B2], [_TRI7_B2, _TRI7_B2, _TRI7_A2]]),
+        np.array([0.225] + [0.132394152788506] * 3 + [0.125939180544827] * 3)),
+    3: (np.array([[0.5854101966249685] + [0.1381966011250105] * 3,
+                  [0.1381966011250105, 0.5854101966249685, 0.1381966011250105, 0.1381966011250105],
+                  [0.1381966011250105, 0.1381966011250105, 0.5854101966249685, 0.1381966011250105],
+                  [0.1381966011250105] * 3 + [0.5854101966249685]]),
+        np.full(4, 0.25)),
+}
+
+
+def source_load(dim, coords, cells, fn, q, dt):
+    """[int f_q . phi_a ; -dt int g_q phi_a] (f^m = [F^m; -tau G^m], G^m = (g, q_h))
+    for source field q of fn (fn(q, xyz) -> [npts, dim+1]) by the quadrature _QUAD.
+    Returns paper order [U (node-major); P]."""
+    lam, w = _QUAD[dim]
+    X = coords[cells]                                     # (nc, d+1, d)
+    E = X[:, 1:, :] - X[:, :1, :]                         # edge matrix rows
+    vol = np.abs(np.linalg.det(E)) / (2.0 if dim == 2 else 6.0)
+    xq = np.einsum("ka,cad->ckd", lam, X)                 # (nc, nq, d)
+    vals = np.asarray(fn(q, xq.reshape(-1, dim)), dtype=np.float64).reshape(cells.shape[0], len(w), dim + 1)
+    # contribution of cell c to its vertex a: |T| sum_k w_k lam_k[a] v(x_k)
+    contrib = np.einsum("c,k,ka,ckv->cav", vol, w, lam, vals)   # (nc, d+1, d+1 comps)
+    nn = coords.shape[0]
+    out = np.zeros((nn, dim + 1))
+    np.add.at(out, cells.reshape(-1), contrib.reshape(-1, dim + 1))
+    return np.concatenate([out[:, :dim].reshape(-1), -dt * out[:, dim]])
+
+
 class OracleSystem:
     """The per-step operators AA, A' and load f of one problem (free DoFs only).
 
     Built from a workloads.Problem-like object (fields dim, coords, cells,
-    lam, mu, alpha, storage, kappa, h, dt, dirichlet, facets, traction).
+    lam, mu, alpha, storage, kappa, h, dt, dirichlet, facets, traction; optional
+    sources / source_coef / dirichlet_values / dirichlet_coef of §4.1).
     `beta_override` replaces the printed beta formula (R5).
+
+    Load of step n ("f^m"): f^n = sum_j coef_j(n) loads[j] with
+    loads[0] = F (traction, coefficient s_n, R16) and, for §4.1 problems (R24),
+    one term [(f_q, phi); -tau (g_q, phi)] per source field q (source_load) with
+    coefficient source_coef[q][n-1], then the Dirichlet lifting -AA_{free,D} x_D
+    (coefficient c_n) and A'_{free,D} x_D (coefficient c_{n-1}), x_D(t_n) = c_n x_D.
     """
 
     def __init__(self, prob, dt=None, beta_override=None, dirichlet=None):
@@ -199,6 +242,24 @@ class OracleSystem:
         self.AP = (Df @ AP @ Df).tocsr(); self.AP.eliminate_zeros()
         Fu = traction_load(d, prob.coords, prob.facets, prob.traction)
         self.F = np.concatenate([Fu, np.zeros(self.np)]) * self.free
+        # further load terms of §4.1 (R24); kinds: ("src", q), ("dnow",), ("dprev",)
+        self.loads = [self.F]
+        self.kinds = [("scale",)]
+        self.prob = prob
+        fn = getattr(prob, "source_fn", None)
+        if fn is not None:
+            for q in range(int(prob.n_sources)):
+                self.loads.append(source_load(d, np.asarray(prob.coords, dtype=np.float64),
+                                              np.asarray(prob.cells), fn, q, self.dt) * self.free)
+                self.kinds.append(("src", q))
+        dv = getattr(prob, "dirichlet_values", None)
+        if dv is not None:
+            xD = self.to_paper(np.asarray(dv, dtype=np.float64)) * (1.0 - self.free)
+            self.loads.append(-(AA @ xD) * self.free)
+            self.kinds.append(("dnow",))
+            self.loads.append((AP @ xD) * self.free)
+            self.kinds.append(("dprev",))
+        self.Fall = np.ascontiguousarray(np.array(self.loads))
         fu, fp = self.free[:self.nu], self.free[self.nu:]
         self.BT = (sp.diags(fp) @ bl.B.T.tocsr() @ sp.diags(fu)).tocsr(); self.BT.eliminate_zeros()
         dA = bl.A.diagonal()
@@ -224,6 +285,37 @@ class OracleSystem:
         out[..., d] = X[..., d * nn:]
         return out.reshape(X.shape[:-1] + (nn * (d + 1),))
 
+    # -- loads -------------------------------------------------------------------
+    def coefs(self, s, first_step=1, nt=None):
+        """[J, nt] coefficients of the load terms for global steps first_step..: row 0 is
+        the traction scale s (length nt, the window's own), the rest from the problem."""
+        s = np.asarray(s, dtype=np.float64)
+        nt = s.shape[-1] if nt is None else nt
+        C = np.zeros((len(self.loads), nt))
+        C[0] = s
+        n = np.arange(first_step, first_step + nt)
+        for j, k in enumerate(self.kinds):
+            if k[0] == "src":
+                C[j] = np.asarray(self.prob.source_coef)[k[1]][n - 1]
+            elif k[0] == "dnow":
+                dc = getattr(self.prob, "dirichlet_coef", None)
+                C[j] = 1.0 if dc is None else np.asarray(dc)[n]
+            elif k[0] == "dprev":
+                dc = getattr(self.prob, "dirichlet_coef", None)
+                C[j] = 1.0 if dc is None else np.asarray(dc)[n - 1]
+        return C
+
+    def _loadset(self, s):
+        S = np.ascontiguousarray(np.atleast_2d(np.asarray(s, dtype=np.float64)))
+        Fm = self.F[None] if S.shape[0] == 1 else self.Fall
+        assert S.shape[0] == Fm.shape[0], "coefficient rows must match the load terms"
+        return S, np.ascontiguousarray(Fm)
+
+    def load_vec(self, s, n):
+        """f^n = sum_j S[j, n-1] loads[j] for s of shape (nt,) (traction only) or (J, nt)."""
+        S, Fm = self._loadset(s)
+        return S[:, n - 1] @ Fm
+
     # -- the iteration ------------------------------------------------------------
     def iterate(self, X, s, K, precond=2, omega=0.5, history=True, nthreads=0):
         """K Jacobi-in-time outer iterations in place on X[(nt+1), ndof] (paper order).
@@ -233,14 +325,14 @@ class OracleSystem:
         """
         X = np.ascontiguousarray(X, dtype=np.float64)
         nt = X.shape[0] - 1
-        s = np.ascontiguousarray(s, dtype=np.float64)
-        assert s.shape == (nt,) and X.shape[1] == self.ndof and precond in (1, 2)
+        S, Fm = self._loadset(s)
+        assert S.shape[1] == nt and X.shape[1] == self.ndof and precond in (1, 2)
         hist = np.zeros((max(K, 1), nt, 2)) if history else None
         rc = lib().oracle_iterate(self.nu, self.np, nt, K,
                                   _p(self._AA[0], _i64), _p(self._AA[1], _i32), _p(self._AA[2]),
                                   _p(self._AP[0], _i64), _p(self._AP[1], _i32), _p(self._AP[2]),
                                   _p(self._BT[0], _i64), _p(self._BT[1], _i32), _p(self._BT[2]),
-                                  _p(self.F), _p(s), _p(self.DAinv), _p(self.DSinv),
+                                  S.shape[0], _p(Fm), _p(S), _p(self.DAinv), _p(self.DSinv),
                                   precond, omega, _p(X), _p(hist) if history else None, nthreads)
         if rc != 0:
             raise MemoryError("oracle_iterate failed")
@@ -250,13 +342,14 @@ class OracleSystem:
         """||r_{n,u}||, ||r_{n,p}|| at X without updating (R12); [nt, 2]."""
         X = np.ascontiguousarray(X, dtype=np.float64)
         nt = X.shape[0] - 1
-        s = np.ascontiguousarray(s, dtype=np.float64)
+        S, Fm = self._loadset(s)
+        assert S.shape[1] == nt
         out = np.zeros((nt, 2))
         r = np.zeros((nt, self.ndof)) if return_r else None
         rc = lib().oracle_residual_norms(self.nu, self.np, nt,
                                          _p(self._AA[0], _i64), _p(self._AA[1], _i32), _p(self._AA[2]),
                                          _p(self._AP[0], _i64), _p(self._AP[1], _i32), _p(self._AP[2]),
-                                         _p(self.F), _p(s), _p(X), _p(out),
+                                         S.shape[0], _p(Fm), _p(S), _p(X), _p(out),
                                          _p(r) if return_r else None, nthreads)
         if rc != 0:
             raise MemoryError("oracle_residual_norms failed")

@@ -193,20 +193,27 @@ static void csr_mv(int64_t nrows, const int64_t *rp, const int32_t *ci, const do
 
 /*
  * Residual of step n (Alg. 2 lines 1-2, Jacobi form R4):
- *   r = A' x_prev + s_n f - AA x_cur
+ *   r = A' x_prev + f^n - AA x_cur,   f^n = sum_{j<J} s[j][n-1] F[j]
  * with AA = [[A, B], [B^T, -(S M + tau C + beta L)]] and
  * A' = [[0, 0], [B^T, -(S M + beta L)]] (eqs. fullysystem/axb, P:L156-231,
- * R8/R9), both already restricted to free DoFs by the caller (R11).
+ * R8/R9), both already restricted to free DoFs by the caller (R11).  The load
+ * f^n ("f^m") is a sum of J fixed vectors with per-step coefficients:
+ * J = 1 is the traction load s_n F (R16); §4.1's sources and Dirichlet lifting
+ * add terms (R24).  F is [J][ndof], s is [J][nt].
  */
-static void step_residual(int64_t ndof,
+static void step_residual(int64_t ndof, int32_t J, int32_t nt, int32_t n,
                           const int64_t *Arp, const int32_t *Aci, const double *Av,
                           const int64_t *Prp, const int32_t *Pci, const double *Pv,
-                          const double *F, double s_n, const double *x_prev,
+                          const double *F, const double *s, const double *x_prev,
                           const double *x_cur, double *r, double *tmp)
 {
     csr_mv(ndof, Prp, Pci, Pv, x_prev, r);        /* A' x_{n-1} */
     csr_mv(ndof, Arp, Aci, Av, x_cur, tmp);       /* AA x_n     */
-    for (int64_t i = 0; i < ndof; i++) r[i] = r[i] + s_n * F[i] - tmp[i];
+    for (int64_t i = 0; i < ndof; i++) {
+        double f = 0.0;
+        for (int32_t j = 0; j < J; j++) f += s[(size_t)j * nt + (n - 1)] * F[(size_t)j * ndof + i];
+        r[i] = r[i] + f - tmp[i];
+    }
 }
 
 /*
@@ -234,7 +241,7 @@ static void apply_precond(int precond, int64_t nu, int64_t np, const double *DAi
  * K outer iterations of the inverted time-stepping method over all steps at
  * once, Jacobi in time (Alg. 2; BJ north star; R1, R3, R4):
  *   for k: for n = 1..nt (independent, may run in parallel):
- *       r_n = A' x_{n-1}^k + s_n f - AA x_n^k
+ *       r_n = A' x_{n-1}^k + f^n - AA x_n^k       (f^n as in step_residual)
  *       x_n^{k+1} = x_n^k + omega P^{-1} r_n
  * X holds rows 0..nt of length ndof; row 0 (x_0, or a window's ghost step)
  * is never updated.  hist (optional) receives ||r_{n,u}||_2, ||r_{n,p}||_2 of
@@ -244,7 +251,7 @@ int oracle_iterate(int64_t nu, int64_t np, int32_t nt, int32_t K,
                    const int64_t *Arp, const int32_t *Aci, const double *Av,
                    const int64_t *Prp, const int32_t *Pci, const double *Pv,
                    const int64_t *Brp, const int32_t *Bci, const double *Bv,
-                   const double *F, const double *s, const double *DAinv, const double *DSinv,
+                   int32_t J, const double *F, const double *s, const double *DAinv, const double *DSinv,
                    int32_t precond, double omega, double *X, double *hist, int32_t nthreads)
 {
     int64_t ndof = nu + np;
@@ -273,7 +280,7 @@ int oracle_iterate(int64_t nu, int64_t np, int32_t nt, int32_t K,
                     const double *xp = cur + (size_t)(n - 1) * ndof;
                     const double *xc = cur + (size_t)n * ndof;
                     double *xn = nxt + (size_t)n * ndof;
-                    step_residual(ndof, Arp, Aci, Av, Prp, Pci, Pv, F, s[n - 1], xp, xc, r, t);
+                    step_residual(ndof, J, nt, n, Arp, Aci, Av, Prp, Pci, Pv, F, s, xp, xc, r, t);
                     apply_precond(precond, nu, np, DAinv, DSinv, Brp, Bci, Bv, r, z, t);
                     for (int64_t i = 0; i < ndof; i++) xn[i] = xc[i] + omega * z[i];
                     if (hist) {
@@ -302,7 +309,7 @@ int oracle_iterate(int64_t nu, int64_t np, int32_t nt, int32_t K,
 int oracle_residual_norms(int64_t nu, int64_t np, int32_t nt,
                           const int64_t *Arp, const int32_t *Aci, const double *Av,
                           const int64_t *Prp, const int32_t *Pci, const double *Pv,
-                          const double *F, const double *s, const double *X, double *out,
+                          int32_t J, const double *F, const double *s, const double *X, double *out,
                           double *r_out, int32_t nthreads)
 {
     int64_t ndof = nu + np;
@@ -322,7 +329,7 @@ int oracle_residual_norms(int64_t nu, int64_t np, int32_t nt,
         } else {
 #pragma omp for schedule(static)
             for (int32_t n = 1; n <= nt; n++) {
-                step_residual(ndof, Arp, Aci, Av, Prp, Pci, Pv, F, s[n - 1],
+                step_residual(ndof, J, nt, n, Arp, Aci, Av, Prp, Pci, Pv, F, s,
                               X + (size_t)(n - 1) * ndof, X + (size_t)n * ndof, r, t);
                 double su = 0.0, sp = 0.0;
                 for (int64_t i = 0; i < nu; i++) su += r[i] * r[i];

@@ -89,9 +89,9 @@ def iterate(sysm, X, s, K, m, precond=2, omega=0.5, alpha=30.0):
     nu = sysm.nu
     P = ChebyshevPrecond(sysm, m, alpha)
     hist = np.zeros((K, nt, 2))
-    F = sysm.F
+    S, Fm = sysm._loadset(s)
     for k in range(K):
-        R = (sysm.AP @ X[:-1].T).T + np.outer(s, F) - (sysm.AA @ X[1:].T).T
+        R = (sysm.AP @ X[:-1].T).T + S.T @ Fm - (sysm.AA @ X[1:].T).T
         hist[k, :, 0] = np.linalg.norm(R[:, :nu], axis=1)
         hist[k, :, 1] = np.linalg.norm(R[:, nu:], axis=1)
         X[1:] += omega * P.apply(R, precond)

@@ -33,7 +33,7 @@ def sequential_be(sysm, x0, s, nt):
     X = np.zeros((nt + 1, sysm.ndof))
     X[0] = x0
     for n in range(1, nt + 1):
-        b = sysm.AP @ X[n - 1] + s[n - 1] * sysm.F
+        b = sysm.AP @ X[n - 1] + sysm.load_vec(s, n)
         X[n, free] = lu.solve(b[free])
     return X
 
@@ -105,7 +105,7 @@ def gauss_seidel_in_time(sysm, X, s, K, precond=2, omega=0.5, history=False):
     hist = np.zeros((K, nt, 2))
     for m in range(K):
         for n in range(1, nt + 1):
-            r = sysm.AP @ X[n - 1] + s[n - 1] * sysm.F - sysm.AA @ X[n]
+            r = sysm.AP @ X[n - 1] + sysm.load_vec(s, n) - sysm.AA @ X[n]
             hist[m, n - 1] = np.linalg.norm(r[:nu]), np.linalg.norm(r[nu:])
             z = np.empty_like(r)
             z[:nu] = sysm.DAinv * r[:nu]

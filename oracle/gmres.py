@@ -68,7 +68,7 @@ def iterate(sysm, X, s, K, k, gauss_seidel=False):
         Xold = X.copy()
         for n in range(1, nt + 1):
             prev = X[n - 1] if gauss_seidel else Xold[n - 1]
-            b = sysm.AP @ prev + s[n - 1] * sysm.F
+            b = sysm.AP @ prev + sysm.load_vec(s, n)
             r = b - sysm.AA @ Xold[n]
             hist[m, n - 1] = np.linalg.norm(r[:nu]), np.linalg.norm(r[nu:])
             X[n] = gmres_cycle(sysm, Xold[n], b, k)[0]

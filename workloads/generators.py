@@ -195,6 +195,130 @@ def load_scales(n_t: int, parity: bool) -> np.ndarray:
 # problem bundle
 # --------------------------------------------------------------------------
 
+# --------------------------------------------------------------------------
+# manufactured-solution inputs (§4.1)
+# --------------------------------------------------------------------------
+
+def lame_from_young(E: float, nu: float):
+    """Problem parameters E, nu -> (lambda, mu), the conversion P:L66-69 states."""
+    return E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), E / (2.0 * (1.0 + nu))
+
+
+def all_boundary_dirichlet(coords: np.ndarray) -> np.ndarray:
+    """Every DoF of every boundary node fixed ("Dirichlet boundary conditions
+    are used at all boundaries")."""
+    nn, d = coords.shape
+    eps = 1e-12
+    on = np.zeros(nn, dtype=bool)
+    for ax in range(d):
+        on |= (coords[:, ax] < eps) | (coords[:, ax] > 1 - eps)
+    mask = np.zeros((nn, d + 1), dtype=np.uint8)
+    mask[on, :] = 1
+    return mask.reshape(-1)
+
+
+def trig_source(lam, mu, alpha, K):
+    """§4.1's data as a function of position: source_fn(q, xyz) -> [npts, 3]
+    node-interleaved (f_1, f_2, g); q = 0 the cos(t) parts, q = 1 the sin(t) part:
+
+      f = -3 pi cos t (alpha s_x c_y - 3 pi (lam + 3 mu) c c + 3 pi (lam + mu) s s,
+                       alpha c_x s_y - 3 pi (lam + 3 mu) c c + 3 pi (lam + mu) s s),
+      g = 3 alpha pi sin t (c_x s_y + s_x c_y) + 18 K pi^2 cos t c c
+    (c_x = cos 3 pi x, s_x = sin 3 pi x, ...).  The printed minus sign in g is a
+    typo (reading R13): the stated exact solution needs the plus."""
+    pi = math.pi
+
+    def fn(q, xyz):
+        x, y = xyz[:, 0], xyz[:, 1]
+        cx, cy = np.cos(3 * pi * x), np.cos(3 * pi * y)
+        sx, sy = np.sin(3 * pi * x), np.sin(3 * pi * y)
+        cc, ss = cx * cy, sx * sy
+        out = np.zeros((xyz.shape[0], 3))
+        if q == 0:
+            out[:, 0] = -3 * pi * (alpha * sx * cy - 3 * pi * (lam + 3 * mu) * cc + 3 * pi * (lam + mu) * ss)
+            out[:, 1] = -3 * pi * (alpha * cx * sy - 3 * pi * (lam + 3 * mu) * cc + 3 * pi * (lam + mu) * ss)
+            out[:, 2] = 18 * K * pi ** 2 * cc
+        else:
+            out[:, 2] = 3 * alpha * pi * (cx * sy + sx * cy)
+        return out
+    return fn
+
+
+def trig_exact(xyz, t):
+    """The exact solution of §4.1: p = u_1 = u_2 = cos t cos 3 pi x cos 3 pi y."""
+    return math.cos(t) * np.cos(3 * math.pi * xyz[:, 0]) * np.cos(3 * math.pi * xyz[:, 1])
+
+
+def trig_problem(k: int, n_t: int, dt: float, name: str = ""):
+    """§4.1 trigonometric test: unit square, h = 2^-k, E = 1, nu = 0.3,
+    alpha = 1, K = 1, Dirichlet data on all boundaries, no storage term.  Steps
+    t_n = n dt, n = 1..n_t; sources with per-step coefficients (cos t_n, sin t_n),
+    Dirichlet values x_D = cos 3 pi x cos 3 pi y (every component) with c_n = cos t_n,
+    x_0 = the initial condition.
+    """
+    n = 2 ** k
+    coords, cells = mesh_square(n)
+    lam, mu = lame_from_young(1.0, 0.3)
+    alpha, K = 1.0, 1.0
+    prof = np.repeat(trig_exact(coords, 0.0), 3)
+    t = np.arange(0, n_t + 1, dtype=np.float64) * dt
+    p = Problem(dim=2, n=n, n_t=n_t, dt=dt, K=0, lam=lam, mu=mu, alpha=alpha, storage=0.0,
+                kappa=np.full(cells.shape[0], K), h=1.0 / n, coords=coords, cells=cells,
+                dirichlet=all_boundary_dirichlet(coords), facets=np.zeros((0, 2), np.int32),
+                traction=np.zeros(2), x0_seed=0, name=name or f"trig_h{n}")
+    p.source_fn = trig_source(lam, mu, alpha, K)
+    p.n_sources = 2
+    p.source_coef = np.stack([np.cos(t[1:]), np.sin(t[1:])])
+    p.dirichlet_values = prof
+    p.dirichlet_coef = np.cos(t)
+    p.x_initial = prof.copy()
+    p.meta = dict(E=1.0, nu=0.3, K=K)
+    return p
+
+
+_PATCH = dict(A=(0.3, -0.7, 0.2), B=(-0.1, 0.4, 0.9), C=(0.5, 1.3, -0.6))
+
+
+def patch_exact(xyz, t):
+    """Exact solution of linear_patch_problem at time t, node-interleaved [u_1, u_2, p]."""
+    A, B, C = _PATCH["A"], _PATCH["B"], _PATCH["C"]
+    x, y = xyz[:, 0], xyz[:, 1]
+    prof = np.stack([A[0] + A[1] * x + A[2] * y, B[0] + B[1] * x + B[2] * y,
+                     C[0] + C[1] * x + C[2] * y], axis=1)
+    return ((1.0 + t) * prof).reshape(-1)
+
+
+def linear_patch_problem(n: int, n_t: int, dt: float, lam=1.0, mu=1.0, alpha=1.0, K=1.0):
+    """A manufactured solution that P1-P1 backward Euler reproduces exactly (test input):
+    u_1 = (1+t) a(x), u_2 = (1+t) b(x), p = (1+t) c(x) with a, b, c affine.  Then
+    -div sigma = 0, f = alpha grad p = (1+t) alpha grad c (constant in space),
+    g = alpha div u_t - K lap p = alpha div (a, b) (constant); all boundaries Dirichlet.
+    Sources: q = 0 the f-part (coefficient 1 + t_n), q = 1 the g-part (coefficient 1)."""
+    coords, cells = mesh_square(n)
+    A, B, C = _PATCH["A"], _PATCH["B"], _PATCH["C"]
+
+    def fn(q, xyz):
+        out = np.zeros((xyz.shape[0], 3))
+        if q == 0:
+            out[:, 0] = alpha * C[1]
+            out[:, 1] = alpha * C[2]
+        else:
+            out[:, 2] = alpha * (A[1] + B[2])
+        return out
+    t = np.arange(0, n_t + 1, dtype=np.float64) * dt
+    p = Problem(dim=2, n=n, n_t=n_t, dt=dt, K=0, lam=lam, mu=mu, alpha=alpha, storage=0.0,
+                kappa=np.full(cells.shape[0], K), h=1.0 / n, coords=coords, cells=cells,
+                dirichlet=all_boundary_dirichlet(coords), facets=np.zeros((0, 2), np.int32),
+                traction=np.zeros(2), x0_seed=0, name=f"patch_h{n}")
+    p.source_fn = fn
+    p.n_sources = 2
+    p.source_coef = np.stack([1.0 + t[1:], np.ones(n_t)])
+    p.dirichlet_values = patch_exact(coords, 0.0)
+    p.dirichlet_coef = 1.0 + t
+    p.x_initial = p.dirichlet_values.copy()
+    return p
+
+
 @dataclass
 class Problem:
     dim: int
@@ -216,6 +340,15 @@ class Problem:
     x0_seed: int
     name: str = ""
     meta: dict = field(default_factory=dict)
+    # §4.1 data (optional): source_fn(q, xyz [npts, d]) -> [npts, d+1] for q < n_sources
+    # with [n_sources][n_t] coefficients; Dirichlet values x_D with coefficients
+    # c_0..c_{n_t}; x_0
+    source_fn: object = None
+    n_sources: int = 0
+    source_coef: np.ndarray = None
+    dirichlet_values: np.ndarray = None
+    dirichlet_coef: np.ndarray = None
+    x_initial: np.ndarray = None
 
     @property
     def n_nodes(self) -> int:
