@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define BIOT_PIT_ABI_VERSION 2
+#define BIOT_PIT_ABI_VERSION 3
 
 typedef struct biot_ctx biot_ctx;   /* opaque; owned by the library until biot_destroy */
 
@@ -90,6 +90,26 @@ typedef struct {
     double traction[3];              /* constant traction on those facets (first dim used)  */
     const double *load_scale;        /* host, n_t values s_n (n = 1..n_t), or NULL => 1      */
     const double *x_initial;         /* host, x_0 (n_nodes*(dim+1)), or NULL => 0            */
+    /* Time-dependent body force / source and non-homogeneous Dirichlet data (PAPER.md
+     * §4.1: the trigonometric test; reading R24).  The load of step n becomes
+     *   f_n = s_n [F_traction; 0]
+     *       + sum_q source_coef[q*n_t + n-1] [ int f_q . phi ; -dt int g_q phi ]
+     *       + dirichlet_coef[n]   (-AA_{free,D} x_D)      (lifting of x_D(t_n) = c_n x_D)
+     *       + dirichlet_coef[n-1] ( A'_{free,D} x_D)      (x_D(t_{n-1}) through A')
+     * (free rows only).  The integrals use a fixed quadrature per cell (triangles: the
+     * 7-point degree-5 rule; tetrahedra: the 4-point degree-2 rule) at points the
+     * library passes to source_eval.  The iterate keeps the homogeneous form: Dirichlet
+     * DoFs of x stay 0 and the caller adds dirichlet_coef[n] x_D to recover the field.
+     * At most 4 of these load terms (counting the traction term) may be nonzero. */
+    int32_t n_sources;               /* source fields (>= 0)                                 */
+    /* Called during biot_setup only: fill vals[k*(dim+1) + c] with component c of source
+     * field q (f_1..f_d, g) at point xyz[k*dim ..], k < npts.  Must not call the library. */
+    void (*source_eval)(int32_t q, int64_t npts, const double *xyz, double *vals, void *user);
+    void *source_user;               /* passed through to source_eval                        */
+    const double *source_coef;       /* host, [n_sources][n_t], finite                       */
+    const double *dirichlet_values;  /* host, n_nodes*(dim+1) x_D (read on Dirichlet DoFs),
+                                        or NULL => homogeneous                              */
+    const double *dirichlet_coef;    /* host, n_t+1 values c_0..c_{n_t}, or NULL => all 1    */
 } biot_bc;
 
 #define BIOT_FLAG_MANUAL_HALO 1u     /* world > 1 without NCCL: caller moves the halo with

@@ -37,10 +37,16 @@ class BiotMaterial(ctypes.Structure):
                 ("beta", ctypes.c_double), ("h", ctypes.c_double)]
 
 
+# void (*source_eval)(int32_t q, int64_t npts, const double *xyz, double *vals, void *user)
+SOURCE_EVAL = ctypes.CFUNCTYPE(None, ctypes.c_int32, ctypes.c_int64, _d, _d, ctypes.c_void_p)
+
+
 class BiotBC(ctypes.Structure):
     _fields_ = [("dirichlet", _u8), ("n_traction_facets", ctypes.c_int64),
                 ("traction_facets", _i32), ("traction", ctypes.c_double * 3),
-                ("load_scale", _d), ("x_initial", _d)]
+                ("load_scale", _d), ("x_initial", _d), ("n_sources", ctypes.c_int32),
+                ("source_eval", SOURCE_EVAL), ("source_user", ctypes.c_void_p), ("source_coef", _d),
+                ("dirichlet_values", _d), ("dirichlet_coef", _d)]
 
 
 class BiotOpts(ctypes.Structure):
@@ -148,6 +154,8 @@ class Inputs:
         self.dirichlet = np.ascontiguousarray(prob.dirichlet, dtype=np.uint8)
         self.facets = np.ascontiguousarray(prob.facets, dtype=np.int32)
         self.load_scale = None if load_scale is None else np.ascontiguousarray(load_scale, dtype=np.float64)
+        if x_initial is None:
+            x_initial = getattr(prob, "x_initial", None)
         self.x_initial = None if x_initial is None else np.ascontiguousarray(x_initial, dtype=np.float64)
         d = prob.dim
         self.mesh = BiotMesh(d, self.coords.shape[0], ptr(self.coords), self.cells.shape[0],
@@ -155,5 +163,27 @@ class Inputs:
         self.mat = BiotMaterial(prob.lam, prob.mu, prob.alpha, prob.storage, ptr(self.kappa), 0.0,
                                 -1.0 if beta is None else beta, prob.h)
         tr = (ctypes.c_double * 3)(*([float(v) for v in prob.traction] + [0.0] * (3 - d)))
+        # time-dependent sources and Dirichlet data (§4.1; optional Problem fields):
+        # prob.source_fn(q, xyz [npts, d]) -> [npts, d+1] is evaluated by the library at its
+        # quadrature points through the source_eval callback
+        fn = getattr(prob, "source_fn", None)
+        n_src = 0 if fn is None else int(prob.n_sources)
+        self.source_coef = None if fn is None else np.ascontiguousarray(prob.source_coef, dtype=np.float64)
+        self.cb_error = None
+
+        def _eval(q, npts, xyz, vals, user):
+            try:
+                X = np.ctypeslib.as_array(xyz, shape=(npts, d))
+                V = np.ctypeslib.as_array(vals, shape=(npts, d + 1))
+                V[:] = fn(q, X)
+            except Exception as e:      # leave NaNs: the library rejects them
+                self.cb_error = e
+
+        self.source_eval = SOURCE_EVAL(_eval) if fn is not None else SOURCE_EVAL()
+        dv = getattr(prob, "dirichlet_values", None)
+        self.dirichlet_values = None if dv is None else np.ascontiguousarray(dv, dtype=np.float64)
+        dc = getattr(prob, "dirichlet_coef", None)
+        self.dirichlet_coef = None if dc is None else np.ascontiguousarray(dc, dtype=np.float64)
         self.bc = BiotBC(ptr(self.dirichlet, _u8), self.facets.shape[0], ptr(self.facets, _i32), tr,
-                         ptr(self.load_scale), ptr(self.x_initial))
+                         ptr(self.load_scale), ptr(self.x_initial), n_src, self.source_eval, None,
+                         ptr(self.source_coef), ptr(self.dirichlet_values), ptr(self.dirichlet_coef))

@@ -35,9 +35,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return OUT
     os.makedirs(BUILD, exist_ok=True)
-    objs = []
-    report = []
-    for src in SOURCES:
+    def compile_one(src):
         path = os.path.join(CSRC, src)
         obj = os.path.join(BUILD, src + ".o")
         if src.endswith(".cu"):
@@ -46,6 +44,15 @@ def build(force: bool = False, verbose: bool = False) -> str:
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-c", path, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, cmd, r
+
+    # translation units compile in parallel (the tile kernels dominate the build time)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    objs = []
+    report = []
+    for src, obj, cmd, r in results:
         report.append(f"$ {' '.join(cmd)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)

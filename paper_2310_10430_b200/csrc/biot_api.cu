@@ -130,6 +130,10 @@ struct biot_ctx {
     double *blk = nullptr;
     int32_t *cols = nullptr;
     double *load = nullptr, *dinv = nullptr, *s = nullptr;
+    double *loadx = nullptr;          // load terms 1..n_load-1 (R24), [(j-1)*N + i][nc]
+    int n_load = 1;                   // load terms (s rows); > 1 selects the kMaxLoads kernels
+    int trac_term = 0;                // s row of the traction term (biot_set_load_scale), -1: none
+    int64_t s_pitch = 0;              // doubles between the rows of s
     uint8_t *fixed = nullptr;
     double *sendbuf = nullptr;
     double *partial = nullptr;
@@ -218,7 +222,7 @@ biot_status dev_alloc(biot_ctx *ctx, void **p, size_t bytes) {
 void free_all(biot_ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
-                    (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->dinv, (void *)c->s,
+                    (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->loadx, (void *)c->dinv, (void *)c->s,
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
@@ -251,6 +255,9 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.load = c->load;
     a.dinv = c->dinv;
     a.s = c->s;
+    a.loadx = c->loadx;
+    a.s_pitch = c->s_pitch;
+    a.n_load = c->n_load;
     a.zbuf = c->z;
     a.sendbuf = (c->world > 1 && mode != biot::MODE_RESIDUAL) ? c->sendbuf : nullptr;
     a.partial = c->partial;
@@ -872,9 +879,48 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             if (!std::isfinite(bc->load_scale[n]))
                 return fail(nullptr, BIOT_E_INVALID, "load_scale must be finite");
 
+    if (bc->n_sources > 0)
+        for (int64_t k = 0; k < (int64_t)bc->n_sources * n_t; ++k)
+            if (!std::isfinite(bc->source_coef[k])) return fail(nullptr, BIOT_E_INVALID, "source_coef must be finite");
+    if (bc->dirichlet_coef)
+        for (int32_t n = 0; n <= n_t; ++n)
+            if (!std::isfinite(bc->dirichlet_coef[n]))
+                return fail(nullptr, BIOT_E_INVALID, "dirichlet_coef must be finite");
+
     auto op = std::make_unique<biot::HostOperator>();
     std::string m = biot::assemble(*mesh, *mat, *bc, dt, *op);
     if (!m.empty()) return fail(nullptr, BIOT_E_INVALID, m);
+
+    // load terms f_n = sum_j coef_j(n) F_j (R16, R24): the traction term (unless it is zero
+    // and others exist), then the sources and the Dirichlet lifting; term 0 travels in the
+    // per-node records, the rest in loadx
+    std::vector<std::vector<double>> lterm_f, lterm_c;   // [term][N*nc], [term][n_t]
+    int trac_term = -1;
+    {
+        bool trac_nz = false;
+        for (double v : op->load) trac_nz |= (v != 0.0);
+        if (trac_nz || op->extra.empty()) {
+            trac_term = 0;
+            lterm_f.push_back(op->load);
+            std::vector<double> c(n_t);
+            for (int32_t n = 0; n < n_t; ++n) c[n] = bc->load_scale ? bc->load_scale[n] : 1.0;
+            lterm_c.push_back(std::move(c));
+        }
+        for (auto &t : op->extra) {
+            std::vector<double> c(n_t);
+            for (int32_t n = 1; n <= n_t; ++n) {
+                if (t.kind == 0) c[n - 1] = bc->source_coef[(size_t)t.src * n_t + (n - 1)];
+                else if (t.kind == 1) c[n - 1] = bc->dirichlet_coef ? bc->dirichlet_coef[n] : 1.0;
+                else c[n - 1] = bc->dirichlet_coef ? bc->dirichlet_coef[n - 1] : 1.0;
+            }
+            lterm_f.push_back(t.f);
+            lterm_c.push_back(std::move(c));
+        }
+        if ((int)lterm_f.size() > biot::kMaxLoads)
+            return fail(nullptr, BIOT_E_INVALID, "at most " + std::to_string(biot::kMaxLoads) +
+                                                     " nonzero load terms (traction, sources, Dirichlet lifting)");
+        op->load = lterm_f[0];
+    }
 
     std::unique_ptr<biot_ctx> holder(new biot_ctx());
     biot_ctx *ctx = holder.get();
@@ -906,6 +952,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->flags = opts->flags;
     ctx->precond = opts->precond;
     ctx->omega = opts->omega;
+    ctx->n_load = (int)lterm_f.size();
+    ctx->trac_term = trac_term;
     ctx->beta = op->beta;
     ctx->nnz_AA = op->nnz_AA;
     ctx->nnz_AP = op->nnz_AP;
@@ -949,6 +997,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             }
         }
     }
+    if (ctx->n_load > 1 && ctx->kern != 1 && ctx->kern != 4) ctx->kern = 1;   // kMaxLoads kernels: generic, tile2d
     const int64_t chunk = ctx->kern == 2 ? 32 * ctx->sT
                         : ctx->kern == 3 ? 32 * ctx->mT
                         : ctx->kern == 4 ? biot::tile2d_chunk()
@@ -1012,11 +1061,24 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ALLOC(ctx->fixed, (size_t)ctx->N * nc);
     CU(h2d(ctx, ctx->fixed, op->fixed.data(), (size_t)ctx->N * nc));
     {
-        std::vector<double> sl(ctx->pitch + 128, 0.0);   // zero past n_tl (window reads may overrun)
-        for (int32_t t = 0; t < ctx->n_tl; ++t)
-            sl[t] = bc->load_scale ? bc->load_scale[ctx->first_step - 1 + t] : 1.0;
+        // one row per load term (the kMaxLoads kernels read them all: unused rows are zero),
+        // zero past n_tl (window reads may overrun)
+        ctx->s_pitch = ctx->pitch + 128;
+        const int rows = ctx->n_load > 1 ? biot::kMaxLoads : 1;
+        std::vector<double> sl((size_t)rows * ctx->s_pitch, 0.0);
+        for (int j = 0; j < ctx->n_load; ++j)
+            for (int32_t t = 0; t < ctx->n_tl; ++t)
+                sl[(size_t)j * ctx->s_pitch + t] = lterm_c[j][ctx->first_step - 1 + t];
         ALLOC(ctx->s, sl.size() * sizeof(double));
         CU(h2d(ctx, ctx->s, sl.data(), sl.size() * sizeof(double)));
+        if (ctx->n_load > 1) {
+            // load vectors of terms 1..kMaxLoads-1; unused terms are zero vectors
+            std::vector<double> lx((size_t)(biot::kMaxLoads - 1) * ctx->N * nc, 0.0);
+            for (int j = 1; j < ctx->n_load; ++j)
+                std::copy(lterm_f[j].begin(), lterm_f[j].end(), lx.begin() + (size_t)(j - 1) * ctx->N * nc);
+            ALLOC(ctx->loadx, lx.size() * sizeof(double));
+            CU(h2d(ctx, ctx->loadx, lx.data(), lx.size() * sizeof(double)));
+        }
     }
     ALLOC(ctx->sendbuf, vec_bytes);
     CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
@@ -1235,13 +1297,13 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             }
         }
     } else {
-        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &ctx->shape));
+        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->n_load > 1, ctx->device, &ctx->shape));
         ctx->groups = ctx->shape.grid;
     }
     // P~1 pass 2 uses the generic shape
     {
         biot::LaunchShape p2{0, 0};
-        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, ctx->device, &p2));
+        CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, false, ctx->device, &p2));
         ctx->pass2_grid = p2.grid;
     }
     ALLOC(ctx->partial, (size_t)ctx->groups * ctx->n_tl * 2 * sizeof(double));
@@ -1296,9 +1358,11 @@ biot_status biot_set_iterate(biot_ctx *ctx, int32_t n, int32_t count, const doub
 biot_status biot_set_load_scale(biot_ctx *ctx, const double *s) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (!s) return fail(ctx, BIOT_E_INVALID, "s is NULL");
+    if (ctx->trac_term < 0) return fail(ctx, BIOT_E_STATE, "the problem has no traction load term");
     CU(cudaSetDevice(ctx->device));
-    CU(cudaMemcpyAsync(ctx->s, s + (ctx->first_step - 1), (size_t)ctx->n_tl * sizeof(double),
-                       cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaMemcpyAsync(ctx->s + (size_t)ctx->trac_term * ctx->s_pitch, s + (ctx->first_step - 1),
+                       (size_t)ctx->n_tl * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
     return BIOT_OK;
 }
 

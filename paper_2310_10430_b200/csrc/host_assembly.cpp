@@ -14,6 +14,7 @@
 #include "host_assembly.h"
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <limits>
 #include <cstring>
@@ -95,6 +96,8 @@ std::string assemble(const biot_mesh &mesh, const biot_material &mat, const biot
     if (!bc.dirichlet) return "bc.dirichlet mask is required";
     if (bc.n_traction_facets < 0 || (bc.n_traction_facets > 0 && !bc.traction_facets))
         return "bc: traction facets missing";
+    if (bc.n_sources < 0 || (bc.n_sources > 0 && (!bc.source_eval || !bc.source_coef)))
+        return "bc: n_sources > 0 needs source_eval and source_coef";
 
     const int d = mesh.dim, nc = d + 1, nv = d + 1;
     const int64_t N = mesh.n_nodes, NC = mesh.n_cells;
@@ -275,6 +278,114 @@ std::string assemble(const biot_mesh &mesh, const biot_material &mat, const biot
     // ---------------- Dirichlet elimination, diagonals, load ----------------
     op.fixed.assign(bc.dirichlet, bc.dirichlet + (size_t)N * nc);
     for (auto &m : op.fixed) m = m ? 1 : 0;
+
+    // further load terms (R24), from the blocks before the Dirichlet columns are dropped
+    {
+        auto column_of = [&](int64_t i, int s) -> int64_t {
+            if (op.path == PATH_BDIA) {
+                const int64_t j = i + op.offsets[s];
+                return (j < 0 || j >= N) ? -1 : j;
+            }
+            return op.cols[(size_t)i * S + s];
+        };
+        auto nonzero = [](const std::vector<double> &v) {
+            for (double x : v)
+                if (x != 0.0) return true;
+            return false;
+        };
+        // sources: [ int f . phi_a ; -dt int g phi_a ] on free rows, by a fixed quadrature
+        // per cell (R24): triangles the 7-point degree-5 rule, tetrahedra the 4-point
+        // degree-2 rule; barycentric points, weights relative to |T|
+        if (bc.n_sources > 0) {
+            std::vector<std::array<double, 4>> qp;
+            std::vector<double> qw;
+            if (d == 2) {
+                const double a1 = 0.059715871789770, b1 = 0.470142064105115;
+                const double a2 = 0.797426985353087, b2 = 0.101286507323456;
+                const double w1 = 0.132394152788506, w2 = 0.125939180544827;
+                qp = {{1.0 / 3, 1.0 / 3, 1.0 / 3, 0}, {a1, b1, b1, 0}, {b1, a1, b1, 0}, {b1, b1, a1, 0},
+                      {a2, b2, b2, 0}, {b2, a2, b2, 0}, {b2, b2, a2, 0}};
+                qw = {0.225, w1, w1, w1, w2, w2, w2};
+            } else {
+                const double a = 0.5854101966249685, b = 0.1381966011250105;
+                qp = {{a, b, b, b}, {b, a, b, b}, {b, b, a, b}, {b, b, b, a}};
+                qw = {0.25, 0.25, 0.25, 0.25};
+            }
+            const int nq = (int)qw.size();
+            std::vector<double> xyz((size_t)NC * nq * d), vol(NC);
+#pragma omp parallel for schedule(static)
+            for (int64_t e = 0; e < NC; ++e) {
+                const int32_t *cn = mesh.cells + e * nv;
+                const double *X[4];
+                for (int a = 0; a < nv; ++a) X[a] = mesh.coords + (size_t)cn[a] * d;
+                double g[4][3];
+                vol[e] = simplex_gradients(d, X, g);
+                for (int k = 0; k < nq; ++k)
+                    for (int c = 0; c < d; ++c) {
+                        double v = 0.0;
+                        for (int a = 0; a < nv; ++a) v += qp[k][a] * X[a][c];
+                        xyz[((size_t)e * nq + k) * d + c] = v;
+                    }
+            }
+            std::vector<double> vals((size_t)NC * nq * nc);
+            for (int q = 0; q < bc.n_sources; ++q) {
+                std::fill(vals.begin(), vals.end(), std::numeric_limits<double>::quiet_NaN());
+                bc.source_eval(q, NC * nq, xyz.data(), vals.data(), bc.source_user);
+                for (double v : vals)
+                    if (!std::isfinite(v)) return "bc: source_eval returned a non-finite value";
+                HostOperator::LoadTerm t;
+                t.kind = 0;
+                t.src = q;
+                t.f.assign((size_t)N * nc, 0.0);
+#pragma omp parallel for schedule(dynamic, 1024)
+                for (int64_t i = 0; i < N; ++i)
+                    for (int64_t r = inc_ptr[i]; r < inc_ptr[i + 1]; ++r) {
+                        const int64_t e = inc[r];
+                        const int32_t *cn = mesh.cells + e * nv;
+                        int a = 0;
+                        while (cn[a] != i) ++a;
+                        for (int k = 0; k < nq; ++k) {
+                            const double wk = vol[e] * qw[k] * qp[k][a];
+                            const double *fv = vals.data() + ((size_t)e * nq + k) * nc;
+                            for (int c = 0; c < d; ++c) t.f[(size_t)i * nc + c] += wk * fv[c];
+                            t.f[(size_t)i * nc + d] += -tau * wk * fv[d];
+                        }
+                    }
+                for (size_t k = 0; k < t.f.size(); ++k)
+                    if (op.fixed[k]) t.f[k] = 0.0;
+                if (nonzero(t.f)) op.extra.push_back(std::move(t));
+            }
+        }
+        // Dirichlet lifting: the columns of fixed DoFs times x_D
+        if (bc.dirichlet_values) {
+            const double *xd = bc.dirichlet_values;
+            for (size_t k = 0; k < (size_t)N * nc; ++k)
+                if (op.fixed[k] && !std::isfinite(xd[k])) return "bc: dirichlet_values must be finite";
+            HostOperator::LoadTerm now, prev;
+            now.kind = 1;
+            prev.kind = 2;
+            now.f.assign((size_t)N * nc, 0.0);
+            prev.f.assign((size_t)N * nc, 0.0);
+#pragma omp parallel for schedule(static)
+            for (int64_t i = 0; i < N; ++i)
+                for (int s = 0; s < S; ++s) {
+                    const int64_t j = column_of(i, s);
+                    if (j < 0) continue;
+                    const double *b = op.blk.data() + ((size_t)i * S + s) * W;
+                    for (int cc = 0; cc < nc; ++cc) {
+                        if (!op.fixed[(size_t)j * nc + cc]) continue;
+                        const double v = xd[(size_t)j * nc + cc];
+                        for (int c = 0; c < nc; ++c) now.f[(size_t)i * nc + c] -= b[c * nc + cc] * v;
+                        // A' row p: B^T columns (= AA's), H column for the pressure
+                        prev.f[(size_t)i * nc + d] += (cc < d ? b[d * nc + cc] : b[nc * nc]) * v;
+                    }
+                }
+            for (size_t k = 0; k < (size_t)N * nc; ++k)
+                if (op.fixed[k]) now.f[k] = prev.f[k] = 0.0;
+            if (nonzero(now.f)) op.extra.push_back(std::move(now));
+            if (nonzero(prev.f)) op.extra.push_back(std::move(prev));
+        }
+    }
     op.dinv.assign((size_t)N * nc, 0.0);
     // diagonals before masking (only read on free DoFs)
     for (int64_t i = 0; i < N; ++i) {

@@ -30,6 +30,14 @@ struct HostOperator {
     std::vector<double> load;       // f, n_nodes * nc
     std::vector<double> dinv;       // n_nodes * nc; 1/diag(A), 1/diag(S~p) on free DoFs, else 0
     std::vector<uint8_t> fixed;     // n_nodes * nc
+    // further load terms (R24): sources (kind 0, coefficient row `src` of bc.source_coef) and
+    // the Dirichlet lifting (kind 1: -AA_{free,D} x_D with c_n; kind 2: A'_{free,D} x_D with
+    // c_{n-1}); free rows only, all-zero terms dropped
+    struct LoadTerm {
+        std::vector<double> f;      // n_nodes * nc
+        int kind = 0, src = 0;
+    };
+    std::vector<LoadTerm> extra;
     double beta = 0.0;
     int64_t nnz_AA = 0, nnz_AP = 0; // nonzeros (free rows/cols, explicit zeros dropped)
 };

@@ -88,12 +88,12 @@ __global__ void __launch_bounds__(kThreads, 2) march2d_kernel(const SweepArgs a)
         const int64_t seg = grp % n_seg, jr = grp / n_seg;
         const int t0 = chunk * CH + lane * T;
         const int64_t col = seg * kRowNodes + warp;
-        double nu[T], npn[T], sv[T];
+        double nu[T], npn[T], sv[1][T];
 #pragma unroll
         for (int tt = 0; tt < T; ++tt) {
             nu[tt] = 0.0;
             npn[tt] = 0.0;
-            sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
+            sv[0][tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
         }
         const int ja = (int)(jr * a.rows_per_tile);
         const int jb = min(a.n_rows, ja + a.rows_per_tile);

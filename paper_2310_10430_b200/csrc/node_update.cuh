@@ -33,11 +33,36 @@ __device__ __forceinline__ double cload(const double *p) {
 // MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
 // ZFULL: outz = z = P~2^{-1} r for every component (GMRES); else outz = (z_u, r_p)
 // (the P~1 first pass).
-template <int D, int T, bool MASK, bool ZFULL = false>
+// The load of step t at one node: f_t = sum_j s_j(t) F_j (NL terms; NL = 1 is the
+// traction load s_t F of R16, NL = kMaxLoads the time-dependent sources and Dirichlet
+// lifting of R24).  Unused terms carry F_j = 0.
+template <int NC, int T, int NL>
+struct Loads {
+    double F[NL][NC];
+    double sv[NL][T];
+    __device__ __forceinline__ double at(int c, int tt) const {
+        double l = sv[0][tt] * F[0][c];
+#pragma unroll
+        for (int j = 1; j < NL; ++j) l = fma(sv[j][tt], F[j][c], l);
+        return l;
+    }
+};
+
+template <int NC, int T>
+__device__ __forceinline__ Loads<NC, T, 1> single_load(const double (&F)[NC], const double (&sv)[T]) {
+    Loads<NC, T, 1> ld;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) ld.F[0][c] = F[c];
+#pragma unroll
+    for (int tt = 0; tt < T; ++tt) ld.sv[0][tt] = sv[tt];
+    return ld;
+}
+
+template <int D, int T, bool MASK, bool ZFULL = false, class LD>
 __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[D + 1][T], const double (&q)[T],
-                                              double qprev, const double (&F)[D + 1],
+                                              double qprev, const LD &ld,
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
-                                              const double (&sv)[T], double (&nu)[T], double (&npn)[T],
+                                              double (&nu)[T], double (&npn)[T],
                                               double (&outx)[D + 1][T], double (&outz)[D + 1][T]) {
     constexpr int NC = D + 1;
 #pragma unroll
@@ -45,8 +70,8 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
         const double qp = (tt == 0) ? qprev : q[tt - 1];
         double r[NC];
 #pragma unroll
-        for (int c = 0; c < D; ++c) r[c] = sv[tt] * F[c] - acc[c][tt];
-        r[D] = (sv[tt] * F[D] + qp) - acc[D][tt];
+        for (int c = 0; c < D; ++c) r[c] = ld.at(c, tt) - acc[c][tt];
+        r[D] = (ld.at(D, tt) + qp) - acc[D][tt];
         // Dirichlet rows (D^{-1} = 0) carry no residual: kernels that apply a shared
         // stencil to such rows (tile3d class templates) rely on this mask
         if constexpr (MASK) {
@@ -72,17 +97,17 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
 
 // Epilogue of one node over the lane's T steps: the shared arithmetic, then the
 // stores (x^{k+1}, the P~1 Z panel, the send slice) by mode.
-template <int D, int T, class A, bool MASK = true>
+template <int D, int T, class A, bool MASK = true, class LD>
 __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
                                               const double (&acc)[D + 1][T], const double (&q)[T],
-                                              double qprev, const double (&F)[D + 1],
+                                              double qprev, const LD &ld,
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
-                                              const double (&sv)[T], double (&nu)[T], double (&npn)[T]) {
+                                              double (&nu)[T], double (&npn)[T]) {
     constexpr int NC = D + 1;
     const int64_t P = a.pitch;
     const int mode = a.mode;
     double outx[NC][T], outz[NC][T];
-    epilogue_math<D, T, MASK>(a.omega, acc, q, qprev, F, Dv, xs, sv, nu, npn, outx, outz);
+    epilogue_math<D, T, MASK>(a.omega, acc, q, qprev, ld, Dv, xs, nu, npn, outx, outz);
     if (mode == MODE_RESIDUAL) return;
 
     const int n_tl = a.n_tl;
@@ -143,9 +168,9 @@ __device__ __forceinline__ void node_epilogue(const A &a, int64_t i, int t0,
 // One row node i over the lane's T steps.  bp -> the node's S coefficient blocks
 // (global memory, or a shared-memory copy when SMEM_CF).  The FMA order (slots in
 // storage order, components ascending) is the same for every kernel that calls it.
-template <int D, int S, bool ELL, int T, bool SMEM_CF>
+template <int D, int S, bool ELL, int T, bool SMEM_CF, int NL = 1>
 __device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, const double *__restrict__ bp,
-                                            int t0, int lane, const double (&sv)[T], double (&nu)[T],
+                                            int t0, int lane, const double (&sv)[NL][T], double (&nu)[T],
                                             double (&npn)[T]) {
     constexpr int NC = D + 1;
     constexpr int W = (NC * NC + 2) / 2 * 2;   // block pitch: (d+1)^2 + 1 padded to 16 B
@@ -206,12 +231,19 @@ __device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, const
         qprev = qg;
     }
 
-    double F[NC], Dv[NC];
+    Loads<NC, T, NL> ld;
+    double Dv[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-        F[c] = __ldg(a.load + i * NC + c);
+        ld.F[0][c] = __ldg(a.load + i * NC + c);
+#pragma unroll
+        for (int j = 1; j < NL; ++j) ld.F[j][c] = __ldg(a.loadx + ((j - 1) * a.n_nodes + i) * NC + c);
         Dv[c] = __ldg(a.dinv + i * NC + c);
     }
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+#pragma unroll
+        for (int tt = 0; tt < T; ++tt) ld.sv[j][tt] = sv[j][tt];
     double xs[NC][T];   // own x_i(t0..t0+3): reloaded (L1 hit) instead of held across the slot loop
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
@@ -223,7 +255,7 @@ __device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, const
             xs[c][h + 1] = w2.y;
         }
     }
-    node_epilogue<D, T>(a, i, t0, acc, q, qprev, F, Dv, xs, sv, nu, npn);
+    node_epilogue<D, T>(a, i, t0, acc, q, qprev, ld, Dv, xs, nu, npn);
 }
 
 

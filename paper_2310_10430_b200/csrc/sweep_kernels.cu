@@ -29,7 +29,7 @@ namespace {
 
 using namespace dev;
 
-template <int D, int S, bool ELL>
+template <int D, int S, bool ELL, int NL>
 __global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const SweepArgs a) {
     extern __shared__ double red[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -42,17 +42,18 @@ __global__ void __launch_bounds__(kThreads, (D == 2 ? 2 : 1)) sweep_kernel(const
 
     for (int chunk = cw; chunk < n_chunks; chunk += tw) {
         const int t0 = chunk * kChunk + lane * kT;
-        double nu[kT], npn[kT], sv[kT];
+        double nu[kT], npn[kT], sv[NL][kT];
 #pragma unroll
         for (int tt = 0; tt < kT; ++tt) {
             nu[tt] = 0.0;
             npn[tt] = 0.0;
-            sv[tt] = (t0 + tt < a.n_tl) ? a.s[t0 + tt] : 0.0;
+#pragma unroll
+            for (int j = 0; j < NL; ++j) sv[j][tt] = (t0 + tt < a.n_tl) ? a.s[j * a.s_pitch + t0 + tt] : 0.0;
         }
         for (int64_t b = blockIdx.x; b * nb < N; b += gridDim.x) {
             const int64_t i_end = min(N, (b + 1) * nb);
             for (int64_t i = b * nb + nw; i < i_end; i += nwp)
-                node_update<D, S, ELL, kT, false>(a, i, a.blk + i * (int64_t)(S * block_pitch<D>()), t0,
+                node_update<D, S, ELL, kT, false, NL>(a, i, a.blk + i * (int64_t)(S * block_pitch<D>()), t0,
                                                   lane, sv, nu, npn);
         }
 #pragma unroll
@@ -224,10 +225,10 @@ __global__ void finalize_wave_kernel(const double *__restrict__ partial, int gro
 using SweepFn = void (*)(const SweepArgs);
 using Pass2Fn = void (*)(const Pass2Args);
 
-bool pick(int dim, int path, int S, SweepFn *sf, Pass2Fn *pf) {
+bool pick(int dim, int path, int S, bool ml, SweepFn *sf, Pass2Fn *pf) {
 #define BIOT_CASE(D_, S_, ELL_)              \
     if (dim == D_ && S == S_ && (path == 2) == ELL_) { \
-        *sf = sweep_kernel<D_, S_, ELL_>;   \
+        *sf = ml ? sweep_kernel<D_, S_, ELL_, kMaxLoads> : sweep_kernel<D_, S_, ELL_, 1>; \
         *pf = pass2_kernel<D_, S_, ELL_>;   \
         return true;                          \
     }
@@ -245,10 +246,10 @@ bool pick(int dim, int path, int S, SweepFn *sf, Pass2Fn *pf) {
 
 }  // namespace
 
-cudaError_t sweep_shape(int dim, int path, int n_slots, int device, LaunchShape *out) {
+cudaError_t sweep_shape(int dim, int path, int n_slots, bool ml, int device, LaunchShape *out) {
     SweepFn sf;
     Pass2Fn pf;
-    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    if (!pick(dim, path, n_slots, ml, &sf, &pf)) return cudaErrorInvalidValue;
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
@@ -269,7 +270,7 @@ cudaError_t launch_sweep(int dim, int path, int n_slots, const SweepArgs &a, con
                          cudaStream_t st) {
     SweepFn sf;
     Pass2Fn pf;
-    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    if (!pick(dim, path, n_slots, a.n_load > 1, &sf, &pf)) return cudaErrorInvalidValue;
     sf<<<sh.grid, kThreads, sh.smem, st>>>(a);
     return cudaGetLastError();
 }
@@ -278,7 +279,7 @@ cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int
                          cudaStream_t st) {
     SweepFn sf;
     Pass2Fn pf;
-    if (!pick(dim, path, n_slots, &sf, &pf)) return cudaErrorInvalidValue;
+    if (!pick(dim, path, n_slots, false, &sf, &pf)) return cudaErrorInvalidValue;
     pf<<<grid, kThreads, 0, st>>>(a);
     return cudaGetLastError();
 }

@@ -10,6 +10,7 @@ namespace biot {
 constexpr int kThreads = 256;   // 8 warps per CTA
 constexpr int kT = 4;           // consecutive time steps per lane (2 x 16-B loads)
 constexpr int kChunk = 32 * kT; // time steps per warp chunk
+constexpr int kMaxLoads = 4;    // load terms of the multi-load kernels (R24)
 
 enum SweepMode : int {
     MODE_UPDATE_P2 = 0,   // fused residual + P~2 + update + norms
@@ -28,7 +29,10 @@ struct SweepArgs {
     const int32_t *cols;    // ELL columns [i][slot] (null for BDIA)
     const double *load;     // f [i*nc + c]
     const double *dinv;     // inverse preconditioner diagonals [i*nc + c]
-    const double *s;        // load scales of the local steps [n_tl]
+    const double *s;        // load coefficients of the local steps: term j at s[j * s_pitch + t]
+    const double *loadx;    // load vectors of terms j = 1..kMaxLoads-1: [(j-1) * n_nodes + i][nc]
+    int64_t s_pitch;        // doubles between the coefficient rows of s
+    int32_t n_load;         // load terms (1: s_t f; > 1: the kMaxLoads-term kernels, unused terms zero)
     double *zbuf;           // P~1: Z panel (z_u in u rows, r_p in p row)
     double *sendbuf;        // x^{k+1} of the last local step [i*nc + c] (null: not needed)
     double *partial;        // per-CTA norm partials [gridDim.x][n_tl][2]
@@ -107,7 +111,7 @@ struct LaunchShape {
 };
 
 // dim in {2,3}; path 1 = BDIA, 2 = ELL; n_slots must match the instantiations.
-cudaError_t sweep_shape(int dim, int path, int n_slots, int device, LaunchShape *out);
+cudaError_t sweep_shape(int dim, int path, int n_slots, bool ml, int device, LaunchShape *out);
 cudaError_t launch_sweep(int dim, int path, int n_slots, const SweepArgs &a, const LaunchShape &sh,
                          cudaStream_t st);
 cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int grid,

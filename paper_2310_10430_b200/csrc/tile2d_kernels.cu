@@ -195,7 +195,7 @@ __device__ __forceinline__ void start(const A &a, const double *pd, const double
 // The epilogue runs on each half (2 consecutive steps) of the lane's steps: the shared
 // arithmetic (dev::epilogue_math), then stores through one row pointer per node (the
 // mode is a compile-time parameter; `full`: the whole chunk lies inside the slab).
-template <bool CLS, bool S0, int MODE, class A>
+template <bool CLS, bool S0, int MODE, int NL, class A>
 __device__ __forceinline__ void finish(const A &a, const double *po, const double *pu, int p, int lane,
                                        const double *aux, const double *T, int64_t i, int t0, bool ghost,
                                        bool full, double *carry, const double (&sv)[kT2], double (&acc)[3][kT2],
@@ -208,10 +208,12 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
-    double F[3], Dv[3], xs[3][kT2];
+    double F[NL][3], Dv[3], xs[3][kT2];
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
-        F[c] = aux[7 + c];
+        F[0][c] = aux[7 + c];
+#pragma unroll
+        for (int j = 1; j < NL; ++j) F[j][c] = __ldg(a.loadx + ((j - 1) * a.n_nodes + i) * 3 + c);
         Dv[c] = aux[10 + c];
     }
     load_v(xs, po, p, lane);
@@ -220,9 +222,21 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     const int64_t row = i * 3 * P + a.t_off + t0;   // t0: step within the window
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-        double acc2[3][2], q2[2], xs2[3][2], sv2[2], nu2[2], np2[2], outx[3][2], outz[3][2];
-        sv2[0] = sv[2 * h];
-        sv2[1] = sv[2 * h + 1];
+        double acc2[3][2], q2[2], xs2[3][2], nu2[2], np2[2], outx[3][2], outz[3][2];
+        Loads<3, 2, NL> ld;
+        ld.sv[0][0] = sv[2 * h];
+        ld.sv[0][1] = sv[2 * h + 1];
+#pragma unroll
+        for (int j = 1; j < NL; ++j) {   // further terms' coefficients: L1 hits, not held per chunk
+            const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + j * a.s_pitch + a.t_off + t0 +
+                                                                       h * (kCT / 2)));
+            ld.sv[j][0] = s2.x;
+            ld.sv[j][1] = s2.y;
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ld.F[j][c] = F[j][c];
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             q2[tt] = q[2 * h + tt];
@@ -234,7 +248,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
                 xs2[c][tt] = xs[c][2 * h + tt];
             }
         }
-        epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, F, Dv, xs2, sv2, nu2, np2,
+        epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2,
                                                     outx, outz);
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
@@ -408,7 +422,7 @@ __device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v
 constexpr int kThreads2 = (kSeg + 4) * 32;
 constexpr int kProducerRegs = 24, kConsumerRegs = 160;
 
-template <bool S0, int MODE>
+template <bool S0, int MODE, int NL>
 __global__ void __launch_bounds__(kThreads2, 1)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -517,10 +531,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                             else finish_mv<true, S0, Tile2dArgs>(a, pm, p, lane, aux, T, i, t0, whole, acc, q);
                         } else {
                             if (kindP == 1)
-                                finish<false, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                finish<false, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
                                                                     carry, sv, acc, q, nu, npn);
                             else
-                                finish<true, S0, MODE, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                finish<true, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
                                                                    carry, sv, acc, q, nu, npn);
                         }
                     }
@@ -584,17 +598,22 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
     int sms = 0;
     cudaError_t e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (e != cudaSuccess) return e;
-    for (auto fn : {tile2d_kernel<false, MODE_UPDATE_P2>, tile2d_kernel<true, MODE_UPDATE_P2>,
-                    tile2d_kernel<false, MODE_P1_PASS1>, tile2d_kernel<true, MODE_P1_PASS1>,
-                    tile2d_kernel<false, MODE_RESIDUAL>, tile2d_kernel<true, MODE_RESIDUAL>,
-                    tile2d_kernel<false, MODE_PASS2>, tile2d_kernel<true, MODE_PASS2>,
-                    tile2d_kernel<false, MODE_ZOUT>, tile2d_kernel<true, MODE_ZOUT>,
-                    tile2d_kernel<false, MODE_MATVEC>, tile2d_kernel<true, MODE_MATVEC>}) {
+    constexpr int ML = kMaxLoads;
+    for (auto fn : {tile2d_kernel<false, MODE_UPDATE_P2, 1>, tile2d_kernel<true, MODE_UPDATE_P2, 1>,
+                    tile2d_kernel<false, MODE_P1_PASS1, 1>, tile2d_kernel<true, MODE_P1_PASS1, 1>,
+                    tile2d_kernel<false, MODE_RESIDUAL, 1>, tile2d_kernel<true, MODE_RESIDUAL, 1>,
+                    tile2d_kernel<false, MODE_PASS2, 1>, tile2d_kernel<true, MODE_PASS2, 1>,
+                    tile2d_kernel<false, MODE_ZOUT, 1>, tile2d_kernel<true, MODE_ZOUT, 1>,
+                    tile2d_kernel<false, MODE_MATVEC, 1>, tile2d_kernel<true, MODE_MATVEC, 1>,
+                    tile2d_kernel<false, MODE_UPDATE_P2, ML>, tile2d_kernel<true, MODE_UPDATE_P2, ML>,
+                    tile2d_kernel<false, MODE_P1_PASS1, ML>, tile2d_kernel<true, MODE_P1_PASS1, ML>,
+                    tile2d_kernel<false, MODE_RESIDUAL, ML>, tile2d_kernel<true, MODE_RESIDUAL, ML>,
+                    tile2d_kernel<false, MODE_ZOUT, ML>, tile2d_kernel<true, MODE_ZOUT, ML>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false, MODE_UPDATE_P2>, kThreads2,
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tile2d_kernel<false, MODE_UPDATE_P2, 1>, kThreads2,
                                                       kSmemBytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
@@ -609,13 +628,15 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
     const int64_t tiles = tile2d_tiles(a);
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);   // = tile2d_groups / kSeg
     const dim3 block(kThreads2);
-#define BIOT_T2(S0_, M_) tile2d_kernel<S0_, M_><<<grid, block, sh.smem, st>>>(tmx, a)
-    if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2(true, MODE_UPDATE_P2); else BIOT_T2(false, MODE_UPDATE_P2); }
-    else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2(true, MODE_P1_PASS1); else BIOT_T2(false, MODE_P1_PASS1); }
-    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2(true, MODE_PASS2); else BIOT_T2(false, MODE_PASS2); }
-    else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T2(true, MODE_ZOUT); else BIOT_T2(false, MODE_ZOUT); }
-    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T2(true, MODE_MATVEC); else BIOT_T2(false, MODE_MATVEC); }
-    else { if (a.s0) BIOT_T2(true, MODE_RESIDUAL); else BIOT_T2(false, MODE_RESIDUAL); }
+#define BIOT_T2(S0_, M_, NL_) tile2d_kernel<S0_, M_, NL_><<<grid, block, sh.smem, st>>>(tmx, a)
+#define BIOT_T2L(S0_, M_) { if (a.n_load > 1) BIOT_T2(S0_, M_, kMaxLoads); else BIOT_T2(S0_, M_, 1); }
+    if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2L(true, MODE_UPDATE_P2) else BIOT_T2L(false, MODE_UPDATE_P2) }
+    else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2L(true, MODE_P1_PASS1) else BIOT_T2L(false, MODE_P1_PASS1) }
+    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2(true, MODE_PASS2, 1); else BIOT_T2(false, MODE_PASS2, 1); }
+    else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T2L(true, MODE_ZOUT) else BIOT_T2L(false, MODE_ZOUT) }
+    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T2(true, MODE_MATVEC, 1); else BIOT_T2(false, MODE_MATVEC, 1); }
+    else { if (a.s0) BIOT_T2L(true, MODE_RESIDUAL) else BIOT_T2L(false, MODE_RESIDUAL) }
+#undef BIOT_T2L
 #undef BIOT_T2
     return cudaGetLastError();
 }

@@ -237,7 +237,7 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
             acc1[c][0] = acc[n][c];
         }
         double outx[4][1], outz[4][1];
-        epilogue_math<3, 1, CLS>(a.omega, acc1, q1, qp[n], F, Dv, xs, sv1, nu1, np1, outx, outz);
+        epilogue_math<3, 1, CLS>(a.omega, acc1, q1, qp[n], single_load(F, sv1), Dv, xs, nu1, np1, outx, outz);
         nu += nu1[0];
         npn += np1[0];
         if constexpr (MODE != MODE_RESIDUAL) {   // stores through one row pointer per node

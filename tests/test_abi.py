@@ -58,6 +58,19 @@ def test_info_struct_matches_header():
     assert [f[0] for f in _lib.BiotInfo._fields_] == names
 
 
+def test_bc_struct_matches_header():
+    """The ctypes mirror of biot_bc has the header's field names in order (ABI v3 added
+    the §4.1 sources and Dirichlet data)."""
+    hdr = open(os.path.join(ROOT, "include", "biot_pit.h")).read()
+    body = hdr[hdr.index("typedef struct {\n    const uint8_t *dirichlet;"):hdr.index("} biot_bc;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    body = re.sub(r"void \(\*\w+\)\([^;]*\);", "void *source_eval;", body)
+    body = re.sub(r"\[\d+\]", "", body)                     # arrays: keep the name
+    names = [re.split(r"[\s*]+", d.strip())[-1] for d in re.findall(r"([^;{]+);", body)]
+    names = [n for n in names if n]
+    assert [f[0] for f in _lib.BiotBC._fields_] == names
+
+
 def test_no_torch_in_signatures_and_no_oracle_link():
     out = subprocess.run(["ldd", _lib.LIB_PATH], capture_output=True, text=True).stdout
     assert "torch" not in out and "oracle" not in out and "python" not in out

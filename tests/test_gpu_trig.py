@@ -1,0 +1,154 @@
+"""§4.1 trigonometric test on the GPU -- needs a B200.
+
+Multi-term loads (sources with cos/sin coefficients, Dirichlet lifting at c_n and
+c_{n-1}; reading R24) through every iteration of the library, against the oracle at
+1e-9 per field (R17): Jacobi in time with P~2 / P~1 on the 2D tile kernel and the
+generic kernel, Gauss-Seidel in time, per-step GMRES and Alg. 3 (GS + GMRES).  Then
+two consistency checks with closed forms: the affine patch solution is reproduced
+exactly, and the converged h = 1/16, tau = 1/1024 solution has the oracle's backward-
+Euler L2 error (Table 1 row 1 within the golden band).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import extras
+from oracle import gmres as ogm
+from paper_2310_10430_b200 import BiotSolver
+from workloads import trig_problem, linear_patch_problem, patch_exact, initial_iterate
+
+from _parity import TOL, field_errors, norm_errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _x0(prob, nt):
+    return initial_iterate(prob.dirichlet, np.arange(1, nt + 1), 31)
+
+
+def _oracle_start(prob, nt, x0):
+    S = oracle.OracleSystem(prob)
+    C = S.coefs(np.zeros(nt), 1, nt)
+    X = np.zeros((nt + 1, S.ndof))
+    X[0] = S.to_paper(prob.x_initial) * S.free
+    X[1:] = S.to_paper(x0)
+    return S, C, X
+
+
+def _solver(prob, nt, precond, omega, monkeypatch=None, generic=False):
+    if monkeypatch is not None:
+        if generic:
+            monkeypatch.setenv("BIOT_KERNEL", "generic")
+        else:
+            monkeypatch.delenv("BIOT_KERNEL", raising=False)
+    return BiotSolver(prob, n_t=nt, precond=precond, omega=omega)
+
+
+@pytest.mark.parametrize("generic", [False, True])
+@pytest.mark.parametrize("precond,omega", [(2, 0.5), (1, 0.3)])
+@pytest.mark.parametrize("k,nt,K", [(4, 40, 20), (5, 300, 6)])
+def test_trig_parity_jacobi(monkeypatch, generic, precond, omega, k, nt, K):
+    prob = trig_problem(k, nt, 1.0 / 64)
+    x0 = _x0(prob, nt)
+    g = _solver(prob, nt, precond, omega, monkeypatch, generic)
+    try:
+        assert g.info.kernel_path == (1 if generic else 5)
+        g.set_iterate(1, x0)
+        g.iterate(K)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(kk) for kk in range(K)])
+        rg = g.residual_norms()
+    finally:
+        g.close()
+    S, C, X = _oracle_start(prob, nt, x0)
+    Xo, ho = S.iterate(X, C, K, precond, omega)
+    ro = S.residual_norms(Xo, C)
+    xo = np.stack([S.from_paper(v) for v in Xo[1:]])
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+    assert norm_errors(rg, ro).max() < TOL
+
+
+@pytest.mark.parametrize("precond,omega", [(2, 0.5), (1, 0.3)])
+def test_trig_parity_gs(precond, omega):
+    nt, K = 50, 7
+    prob = trig_problem(4, nt, 1.0 / 64)
+    x0 = _x0(prob, nt)
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate_gs(K)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(kk) for kk in range(K)])
+    finally:
+        g.close()
+    S, C, X = _oracle_start(prob, nt, x0)
+    Xo, ho = extras.gauss_seidel_in_time(S, X, C, K, precond, omega, history=True)
+    xo = np.stack([S.from_paper(v) for v in Xo[1:]])
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+@pytest.mark.parametrize("gs", [False, True])
+def test_trig_parity_gmres(gs):
+    nt, K, k = 33, 3, 5
+    prob = trig_problem(4, nt, 1.0 / 64)
+    x0 = _x0(prob, nt)
+    g = BiotSolver(prob, n_t=nt, precond=2, omega=0.5)
+    try:
+        g.set_iterate(1, x0)
+        (g.iterate_gs_gmres if gs else g.iterate_gmres)(K, k)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(kk) for kk in range(K)])
+    finally:
+        g.close()
+    S, C, X = _oracle_start(prob, nt, x0)
+    Xo, ho = ogm.iterate(S, X, C, K, k, gauss_seidel=gs)
+    xo = np.stack([S.from_paper(v) for v in Xo[1:]])
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_patch_solution_exact_on_gpu():
+    """The affine-in-space-and-time solution is a fixed point of the GPU iteration: from
+    x^0 = 0 the Jacobi iteration converges to it (every load term enters)."""
+    prob = linear_patch_problem(4, 8, 0.125)
+    g = BiotSolver(prob, precond=2, omega=0.5)
+    try:
+        g.iterate(8000)
+        x = g.solution()
+    finally:
+        g.close()
+    fixed = np.asarray(prob.dirichlet, dtype=np.float64)
+    for n in range(1, prob.n_t + 1):
+        full = x[n - 1] + prob.dirichlet_coef[n] * prob.dirichlet_values * fixed
+        ref = patch_exact(prob.coords, n * prob.dt)
+        assert np.abs(full - ref).max() < 1e-9 * np.abs(ref).max()
+
+
+def test_trig_converged_matches_backward_euler():
+    """h = 1/16, tau = 1/1024, t = 1 (Table 1 row 1): Alg. 3 (GS + GMRES(16) per step)
+    swept to convergence equals the oracle's sequential backward Euler, so its L2 error
+    of p is the oracle's (pinned against Table 1 in test_oracle_trig)."""
+    from test_oracle_trig import l2_error_p, full_field, be_solution
+    nt = 1024
+    prob = trig_problem(4, nt, 1.0 / 1024)
+    S, C, Xbe = be_solution(prob)
+    g = BiotSolver(prob, precond=2, omega=0.5)
+    try:
+        g.iterate_gs_gmres(1, 16)
+        r0 = g.residual_norms().max()
+        for sweep in range(60):
+            g.iterate_gs_gmres(1, 16)
+            if g.residual_norms().max() < 1e-11 * r0:
+                break
+        x = g.solution()
+    finally:
+        g.close()
+    xbe = np.stack([S.from_paper(v) for v in Xbe[1:]])
+    assert field_errors(x, xbe, 2).max() < 1e-8
+    fixed = np.asarray(prob.dirichlet, dtype=np.float64)
+    p = (x[nt - 1] + prob.dirichlet_coef[nt] * prob.dirichlet_values * fixed).reshape(-1, 3)[:, 2]
+    pbe = full_field(prob, S, Xbe, nt).reshape(-1, 3)[:, 2]
+    e, ebe = l2_error_p(prob, p, 1.0), l2_error_p(prob, pbe, 1.0)
+    assert abs(e - ebe) < 1e-6 * ebe
