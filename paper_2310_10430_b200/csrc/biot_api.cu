@@ -1120,7 +1120,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         tmp.rows_per_tile = ctx->rows_per_tile;
         ctx->groups = biot::tile2d_groups(tmp, ctx->shape.grid);
         // interior template + per-node aux records
-        const int S = 7, WB = 10, KA = biot::Tile2dArgs::kAux;
+        const int S = 7, WB = 10, KA = ctx->n_load > 1 ? biot::Tile2dArgs::kAuxML : biot::Tile2dArgs::kAux;
         const int64_t tnode = (int64_t)(ctx->n_rows / 2) * ctx->row_w + ctx->row_w / 2;
         const double *tb = op->blk.data() + (size_t)tnode * S * WB;
         for (int q = 0; q < S; ++q)
@@ -1155,6 +1155,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
                 r[10 + c] = op->dinv[(size_t)i * 3 + c];
             }
             r[13] = same ? 1.0 : 2.0;   // path flag: 1 interior template, 2 geometric-class stencil
+            for (int j = 1; j < ctx->n_load; ++j)   // further load vectors (kMaxLoads kernels)
+                for (int c = 0; c < 3; ++c) r[16 + 3 * (j - 1) + c] = lterm_f[j][(size_t)i * 3 + c];
             n_int += same;
         }
         ctx->n_interior = n_int;

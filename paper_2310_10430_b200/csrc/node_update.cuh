@@ -33,9 +33,9 @@ __device__ __forceinline__ double cload(const double *p) {
 // MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
 // ZFULL: outz = z = P~2^{-1} r for every component (GMRES); else outz = (z_u, r_p)
 // (the P~1 first pass).
-// The load of step t at one node: f_t = sum_j s_j(t) F_j (NL terms; NL = 1 is the
-// traction load s_t F of R16, NL = kMaxLoads the time-dependent sources and Dirichlet
-// lifting of R24).  Unused terms carry F_j = 0.
+// The load of step t at one node: f_t = sum_j s_j(t) F_j.  The epilogue applies term 0
+// (the traction load s_t F of R16, or the first term of R24); the kMaxLoads kernels
+// subtract the further terms from the accumulators before it.
 template <int NC, int T, int NL>
 struct Loads {
     double F[NL][NC];
@@ -231,19 +231,25 @@ __device__ __forceinline__ void node_update(const SweepArgs &a, int64_t i, const
         qprev = qg;
     }
 
-    Loads<NC, T, NL> ld;
+    // load terms j >= 1 folded into the accumulators (acc - sum_j s_j F_j); term 0 is
+    // applied by the epilogue as in the single-load kernels
+#pragma unroll
+    for (int j = 1; j < NL; ++j)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const double fj = __ldg(a.loadx + ((j - 1) * a.n_nodes + i) * NC + c);
+#pragma unroll
+            for (int tt = 0; tt < T; ++tt) acc[c][tt] = fma(-sv[j][tt], fj, acc[c][tt]);
+        }
+    Loads<NC, T, 1> ld;
     double Dv[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
         ld.F[0][c] = __ldg(a.load + i * NC + c);
-#pragma unroll
-        for (int j = 1; j < NL; ++j) ld.F[j][c] = __ldg(a.loadx + ((j - 1) * a.n_nodes + i) * NC + c);
         Dv[c] = __ldg(a.dinv + i * NC + c);
     }
 #pragma unroll
-    for (int j = 0; j < NL; ++j)
-#pragma unroll
-        for (int tt = 0; tt < T; ++tt) ld.sv[j][tt] = sv[j][tt];
+    for (int tt = 0; tt < T; ++tt) ld.sv[0][tt] = sv[0][tt];
     double xs[NC][T];   // own x_i(t0..t0+3): reloaded (L1 hit) instead of held across the slot loop
 #pragma unroll
     for (int c = 0; c < NC; ++c) {

@@ -48,16 +48,25 @@ constexpr int kSeg = 12;                    // grid columns per tile = consumer 
 constexpr int kStrip = kSeg + 2;            // + halo columns
 constexpr int kT2 = 4;                      // time steps per lane
 constexpr int kCT = 32 * kT2;               // time steps per chunk
-constexpr int kStages = 5;
 constexpr int kMaxRR = 32;                  // rows per tile (q carry capacity)
-constexpr int kAuxRec = Tile2dArgs::kAux;   // doubles per aux record
 constexpr int kCW = Tile2dArgs::kClsW;      // doubles per class-stencil slot
-constexpr uint32_t kXBytes = kStrip * 3 * kCT * 8;                                 // 52224
-constexpr uint32_t kAuxBytes = kSeg * kAuxRec * 8;                                 // 1920
-constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;          // 54144
-constexpr uint32_t kClsOff = kStages * kStageBytes;
-constexpr uint32_t kCarryOff = kClsOff + 9 * 7 * kCW * 8;
-constexpr uint32_t kSmemBytes = kCarryOff + kMaxRR * kSeg * 8;
+constexpr uint32_t kXBytes = kStrip * 3 * kCT * 8;                                 // 43008
+
+// Shared-memory layout by load-term count: single-load kernels stream 16-double aux
+// records through a 5-stage ring; the kMaxLoads kernels carry the further load vectors
+// in 32-double records (F_j at [16 + 3 (j-1) + c]) through 4 stages.
+template <int NL>
+struct Lay {
+    static constexpr int kStages = NL == 1 ? 5 : 4;
+    static constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
+    static constexpr uint32_t kAuxBytes = kSeg * kAuxRec * 8;
+    static constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;
+    static constexpr uint32_t kClsOff = kStages * kStageBytes;
+    static constexpr uint32_t kCarryOff = kClsOff + 9 * 7 * kCW * 8;
+    static constexpr uint32_t kSmemBytes = kCarryOff + kMaxRR * kSeg * 8;
+};
+constexpr uint32_t kSmemBytes = Lay<1>::kSmemBytes > Lay<kMaxLoads>::kSmemBytes ? Lay<1>::kSmemBytes
+                                                                               : Lay<kMaxLoads>::kSmemBytes;
 
 // (row delta, column delta) of the 7 BDIA slots in storage order
 __host__ __device__ constexpr int sdr(int s) { return (s == 1 || s == 2) ? -1 : (s >= 5) ? 1 : 0; }
@@ -201,6 +210,23 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
                                        bool full, double *carry, const double (&sv)[kT2], double (&acc)[3][kT2],
                                        double (&q)[kT2], double (&nu)[kT2], double (&npn)[kT2]) {
     accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
+    if constexpr (NL > 1) {
+        // load terms j >= 1 folded into the accumulators now (acc - sum_j s_j F_j), while
+        // only acc is live: the epilogue then applies term 0 as the single-load kernels do
+#pragma unroll
+        for (int j = 1; j < NL; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + j * a.s_pitch + a.t_off + t0 +
+                                                                           h * (kCT / 2)));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double fj = aux[16 + 3 * (j - 1) + c];
+                    acc[c][2 * h] = fma(-s2.x, fj, acc[c][2 * h]);
+                    acc[c][2 * h + 1] = fma(-s2.y, fj, acc[c][2 * h + 1]);
+                }
+            }
+    }
     // q(t-1) of each half's first step: lane l-1's matching step; lane 0 of the second
     // half takes lane 31's first-half step 63, lane 0 of the first half the carry
     double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
@@ -208,14 +234,9 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
-    double F[NL][3], Dv[3], xs[3][kT2];
+    double Dv[3], xs[3][kT2];
 #pragma unroll
-    for (int c = 0; c < 3; ++c) {
-        F[0][c] = aux[7 + c];
-#pragma unroll
-        for (int j = 1; j < NL; ++j) F[j][c] = __ldg(a.loadx + ((j - 1) * a.n_nodes + i) * 3 + c);
-        Dv[c] = aux[10 + c];
-    }
+    for (int c = 0; c < 3; ++c) Dv[c] = aux[10 + c];
     load_v(xs, po, p, lane);
     const int64_t P = a.pitch;
     const int n_tl = a.n_tl;
@@ -223,20 +244,12 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         double acc2[3][2], q2[2], xs2[3][2], nu2[2], np2[2], outx[3][2], outz[3][2];
-        Loads<3, 2, NL> ld;
+        // load term 0 of the half's two steps (further terms are already in acc)
+        Loads<3, 2, 1> ld;
         ld.sv[0][0] = sv[2 * h];
         ld.sv[0][1] = sv[2 * h + 1];
 #pragma unroll
-        for (int j = 1; j < NL; ++j) {   // further terms' coefficients: L1 hits, not held per chunk
-            const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + j * a.s_pitch + a.t_off + t0 +
-                                                                       h * (kCT / 2)));
-            ld.sv[j][0] = s2.x;
-            ld.sv[j][1] = s2.y;
-        }
-#pragma unroll
-        for (int j = 0; j < NL; ++j)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) ld.F[j][c] = F[j][c];
+        for (int c = 0; c < 3; ++c) ld.F[0][c] = aux[7 + c];
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             q2[tt] = q[2 * h + tt];
@@ -425,6 +438,10 @@ constexpr int kProducerRegs = 24, kConsumerRegs = 160;
 template <bool S0, int MODE, int NL>
 __global__ void __launch_bounds__(kThreads2, 1)
     tile2d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
+    using L = Lay<NL>;
+    constexpr int kStages = L::kStages, kAuxRec = L::kAuxRec;
+    constexpr uint32_t kAuxBytes = L::kAuxBytes, kStageBytes = L::kStageBytes;
+    constexpr uint32_t kClsOff = L::kClsOff, kCarryOff = L::kCarryOff;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     double *cls_sm = reinterpret_cast<double *>(smem + kClsOff);     // [9][7][kCW]
@@ -608,7 +625,9 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
                     tile2d_kernel<false, MODE_UPDATE_P2, ML>, tile2d_kernel<true, MODE_UPDATE_P2, ML>,
                     tile2d_kernel<false, MODE_P1_PASS1, ML>, tile2d_kernel<true, MODE_P1_PASS1, ML>,
                     tile2d_kernel<false, MODE_RESIDUAL, ML>, tile2d_kernel<true, MODE_RESIDUAL, ML>,
-                    tile2d_kernel<false, MODE_ZOUT, ML>, tile2d_kernel<true, MODE_ZOUT, ML>}) {
+                    tile2d_kernel<false, MODE_ZOUT, ML>, tile2d_kernel<true, MODE_ZOUT, ML>,
+                    tile2d_kernel<false, MODE_PASS2, ML>, tile2d_kernel<true, MODE_PASS2, ML>,
+                    tile2d_kernel<false, MODE_MATVEC, ML>, tile2d_kernel<true, MODE_MATVEC, ML>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
@@ -629,12 +648,13 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
     const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);   // = tile2d_groups / kSeg
     const dim3 block(kThreads2);
 #define BIOT_T2(S0_, M_, NL_) tile2d_kernel<S0_, M_, NL_><<<grid, block, sh.smem, st>>>(tmx, a)
+// NL = kMaxLoads also selects the aux-record layout (Lay), so every mode follows n_load
 #define BIOT_T2L(S0_, M_) { if (a.n_load > 1) BIOT_T2(S0_, M_, kMaxLoads); else BIOT_T2(S0_, M_, 1); }
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2L(true, MODE_UPDATE_P2) else BIOT_T2L(false, MODE_UPDATE_P2) }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2L(true, MODE_P1_PASS1) else BIOT_T2L(false, MODE_P1_PASS1) }
-    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2(true, MODE_PASS2, 1); else BIOT_T2(false, MODE_PASS2, 1); }
+    else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2L(true, MODE_PASS2) else BIOT_T2L(false, MODE_PASS2) }
     else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T2L(true, MODE_ZOUT) else BIOT_T2L(false, MODE_ZOUT) }
-    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T2(true, MODE_MATVEC, 1); else BIOT_T2(false, MODE_MATVEC, 1); }
+    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T2L(true, MODE_MATVEC) else BIOT_T2L(false, MODE_MATVEC) }
     else { if (a.s0) BIOT_T2L(true, MODE_RESIDUAL) else BIOT_T2L(false, MODE_RESIDUAL) }
 #undef BIOT_T2L
 #undef BIOT_T2
