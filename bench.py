@@ -72,25 +72,49 @@ class ClockSampler:
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line))
 
     def start(self):
+        """Start sampling every 100 ms (before the warm-up) and wait for the first sample;
+        mark() opens the timed region, stop() keeps the samples taken inside it (or, for a
+        region shorter than the sampling period, the last one before it, under warm-up load)."""
+        import threading
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 5.0 and self.proc.poll() is None:
+            time.sleep(0.01)
+
+    def mark(self):
+        self.t0 = time.time()
 
     def stop(self):
         if self.proc is None:
             return None
-        time.sleep(0.05)
+        t1 = time.time()
         self.proc.terminate()
         try:
-            out, _ = self.proc.communicate(timeout=5)
+            self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
-            out = ""
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        t0 = getattr(self, "t0", 0.0)
+        inside = [ln for ts, ln in self.lines if t0 <= ts <= t1 + 0.05]
+        before = [ln for ts, ln in self.lines if ts < t0]
+        out = "".join(inside if inside else before[-1:])
         sms, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
@@ -108,7 +132,7 @@ class ClockSampler:
         if not sms:
             return None
         return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sms)}
+                "samples": len(sms), "in_region": bool(inside)}
 
 
 KERNELS = {1: "sweep_kernel<BDIA> (generic, fused residual + P~ + update + norms)",
@@ -129,7 +153,7 @@ def fp64_peak(sm_mhz):
 def load_traffic(cid):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(f"config{cid}")
+        return json.load(open(p)).get(cid if isinstance(cid, str) else f"config{cid}")
     except Exception:
         return None
 
@@ -262,13 +286,14 @@ def main():
         step = lambda K: g.iterate_gs_gmres(K, args.gmres_k)
     else:
         step = g.iterate_gs if args.method == "gs" else g.iterate
+    clk = ClockSampler(local)
+    clk.start()
     # warm-up (untimed)
     step(max(args.warmup, 3))
     barrier()
-    clk = ClockSampler(local)
-    clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    clk.mark()
     ev0.record(stream)
     step(args.steps)                   # K outer iterations, one library call, no host sync inside
     ev1.record(stream)
@@ -321,7 +346,7 @@ def main():
         if prob.dim == 2:
             roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                     "frac": achieved_gbs / hbm,
-                    "traffic": None if args.workload == "trig" else load_traffic(args.config),
+                    "traffic": load_traffic("trig" if args.workload == "trig" else args.config),
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
                     "fp64_tflops": achieved_tf, "fp64_peak_tflops_measured": fp64_meas_tf}
         else:
