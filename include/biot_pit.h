@@ -227,6 +227,16 @@ biot_status biot_assemble_host(const biot_mesh *mesh, const biot_material *mat,
                                int64_t *nnz_AP, int64_t *AP_i, int64_t *AP_j, double *AP_v,
                                double *f, double *dinv);
 
+/* Host-only: the further load terms of R24 (§4.1 sources, Dirichlet lifting) as the
+ * library assembles them, node-interleaved on free DoFs (no device needed).  *n_terms
+ * receives their number (<= 8); F (may be NULL to query) receives [n_terms][n_dof] and
+ * kinds[j] (may be NULL) the kind of term j: 0 = source field (index src[j]), 1 = lifting
+ * -AA_fD x_D (coefficient c_n), 2 = lifting A'_fD x_D (coefficient c_{n-1}).  All-zero
+ * terms are omitted; the traction load is biot_assemble_host's f. */
+biot_status biot_assemble_loads_host(const biot_mesh *mesh, const biot_material *mat,
+                                     const biot_bc *bc, double dt, int32_t *n_terms, double *F,
+                                     int32_t *kinds, int32_t *src);
+
 biot_status biot_get_info(const biot_ctx *ctx, biot_info *out);
 
 /* Device time of the kernels of the last biot_iterate call, per iteration,

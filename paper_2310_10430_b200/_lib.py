@@ -70,7 +70,7 @@ EXPORTS = ["biot_setup", "biot_set_iterate", "biot_set_load_scale", "biot_iterat
            "biot_iterate_gs_gmres", "biot_gs_begin_gmres",
            "biot_gs_begin", "biot_gs_waves", "biot_gs_wave", "biot_gs_end",
            "biot_residual_norms", "biot_residual_history", "biot_solution", "biot_last_slice",
-           "biot_set_ghost", "biot_assemble_host", "biot_get_info", "biot_last_timing",
+           "biot_set_ghost", "biot_assemble_host", "biot_assemble_loads_host", "biot_get_info", "biot_last_timing",
            "biot_nccl_unique_id", "biot_destroy", "biot_last_error", "biot_status_string",
            "biot_abi_version"]
 
@@ -109,6 +109,8 @@ def load():
     L.biot_set_ghost.argtypes = [ctx_p, _d]
     L.biot_assemble_host.argtypes = [P(BiotMesh), P(BiotMaterial), P(BiotBC), ctypes.c_double,
                                      _i64, _i64, _i64, _d, _i64, _i64, _i64, _d, _d, _d]
+    L.biot_assemble_loads_host.argtypes = [P(BiotMesh), P(BiotMaterial), P(BiotBC), ctypes.c_double,
+                                           P(ctypes.c_int32), _d, P(ctypes.c_int32), P(ctypes.c_int32)]
     L.biot_get_info.argtypes = [ctx_p, P(BiotInfo)]
     L.biot_last_timing.argtypes = [ctx_p, _d]
     L.biot_nccl_unique_id.argtypes = [ctypes.c_void_p]

@@ -637,36 +637,10 @@ biot_status gmres_alloc(biot_ctx *ctx, int k) {
     if (ctx->gm_small) cudaFree(ctx->gm_small);
     ctx->gm_scratch = ctx->gm_small = nullptr;
     ALLOC(ctx->gm_scratch, scr * sizeof(double));
-    ALLOC(ctx->gm_small, (size_t)(2 * biot::gmres_max_vectors() + 2) * ctx->n_tl * sizeof(double));
+    // small per-step arrays: dot results, scale, beta, y, and the Hessenberg matrices
+    const int mv = biot::gmres_max_vectors();
+    ALLOC(ctx->gm_small, (size_t)(2 * mv + 2 + mv * (mv - 1)) * ctx->n_tl * sizeof(double));
     return BIOT_OK;
-}
-
-// Least squares min || beta e1 - H y || for the (k+1) x k upper Hessenberg H (column-major
-// H[i + j*(k+1)]) by Givens rotations; zero pivots (breakdown) give zero coefficients.
-void hessenberg_lsq(int k, std::vector<double> H, double beta, double *y) {
-    std::vector<double> g(k + 1, 0.0);
-    g[0] = beta;
-    const int ld = k + 1;
-    for (int j = 0; j < k; ++j) {
-        const double a = H[j + j * ld], b = H[j + 1 + j * ld];
-        const double rr = std::hypot(a, b);
-        if (rr == 0.0) continue;
-        const double c = a / rr, s = b / rr;
-        for (int jj = j; jj < k; ++jj) {
-            const double u = H[j + jj * ld], v = H[j + 1 + jj * ld];
-            H[j + jj * ld] = c * u + s * v;
-            H[j + 1 + jj * ld] = -s * u + c * v;
-        }
-        const double gu = g[j], gv = g[j + 1];
-        g[j] = c * gu + s * gv;
-        g[j + 1] = -s * gu + c * gv;
-    }
-    for (int j = k - 1; j >= 0; --j) {
-        double v = g[j];
-        for (int jj = j + 1; jj < k; ++jj) v -= H[j + jj * ld] * y[jj];
-        const double d = H[j + j * ld];
-        y[j] = (std::fabs(d) > 1e-300) ? v / d : 0.0;
-    }
 }
 
 }  // namespace
@@ -678,29 +652,28 @@ namespace {
 // norm partials) from panel xin through tensor map `tm`.  x_out may equal x_in.
 biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const double *xin, double *xout,
                         const Window &win) {
+    // Everything stays on the device (no host round trip): the dot kernels accumulate the
+    // Hessenberg columns and produce the normalisation scales, the least-squares problems
+    // are solved by one thread per step, and the combination kernels read the
+    // coefficients where the dots left them.
     const int64_t rows = ctx->N * ctx->nc;
     const int c0 = win.t_off + win.t_lo, nt = win.len - win.t_lo;   // columns the cycle owns
-    double *d_h = ctx->gm_small;
-    double *d_scale = ctx->gm_small + (size_t)biot::gmres_max_vectors() * ctx->n_tl;
-    std::vector<double> h1((size_t)(k + 1) * nt), hn(nt), beta(nt), scale(nt);
-    std::vector<double> H((size_t)nt * (k + 1) * k, 0.0);   // per step, column-major (k+1) x k
-    std::vector<double> y((size_t)k * nt);
+    const int mv = biot::gmres_max_vectors();
+    double *d_h = ctx->gm_small;                           // [mv][nt] dot results
+    double *d_scale = d_h + (size_t)mv * ctx->n_tl;        // [nt]
+    double *d_beta = d_scale + ctx->n_tl;                  // [nt]
+    double *d_y = d_beta + ctx->n_tl;                      // [mv][nt]
+    double *d_H = d_y + (size_t)mv * ctx->n_tl;            // [(k+1) k][nt]
     double *const *Vd = ctx->gm_Vdev;
-    auto dots = [&](const double *a, double *const *bdev, int nb, double *out_host) -> biot_status {
-        CU(biot::gmres_dots(a + c0, bdev, c0, nb, rows, ctx->pitch, nt, ctx->gm_scratch, d_h, ctx->stream));
-        CU(cudaMemcpyAsync(out_host, d_h, (size_t)nb * nt * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        CU(cudaStreamSynchronize(ctx->stream));
-        return BIOT_OK;
+    auto hcol = [&](int i, int j) { return d_H + (size_t)(i + j * (k + 1)) * nt; };
+    auto dots = [&](const double *a, double *const *bdev, int nb, double *out, double *hacc, bool norm) {
+        return biot::gmres_dots(a + c0, bdev, c0, nb, rows, ctx->pitch, nt, ctx->gm_scratch, out, hacc, norm,
+                                ctx->stream);
     };
-    auto combine = [&](double *dst, const double *base, const double *coef_host, int nb, double sign,
-                       const double *scale_host) -> biot_status {
-        if (nb > 0) CU(cudaMemcpyAsync(d_h, coef_host, (size_t)nb * nt * sizeof(double), cudaMemcpyHostToDevice,
-                                       ctx->stream));
-        if (scale_host)
-            CU(cudaMemcpyAsync(d_scale, scale_host, nt * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
-        CU(biot::gmres_combine(dst + c0, base + c0, Vd, c0, d_h, nb, sign, scale_host ? d_scale : nullptr, rows,
-                               ctx->pitch, nt, ctx->stream));
-        return BIOT_OK;
+    auto combine = [&](double *dst, const double *base, const double *coef, int nb, double sign,
+                       const double *scale) {
+        return biot::gmres_combine(dst + c0, base + c0, Vd, c0, coef, nb, sign, scale, rows, ctx->pitch, nt,
+                                   ctx->stream);
     };
     auto tile_args = [&](int mode, const double *x, double *xn) {
         biot::Tile2dArgs a{};
@@ -718,47 +691,31 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
         a.ghost_stride = win.stride;
         return a;
     };
+    CU(cudaMemsetAsync(d_H, 0, (size_t)(k + 1) * k * nt * sizeof(double), ctx->stream));
     // v_0 = P~2^{-1} (b - AA x_in) with b = A' x_prev + f, and the norms of b - AA x_in
     {
         biot::Tile2dArgs a = tile_args(biot::MODE_ZOUT, xin, nullptr);
         a.zbuf = ctx->gm_V[0];
         CU(biot::launch_tile2d(tm, a, ctx->shape, ctx->stream));
     }
-    biot_status st = dots(ctx->gm_V[0], Vd, 1, beta.data());
-    if (st != BIOT_OK) return st;
-    for (int t = 0; t < nt; ++t) {
-        beta[t] = std::sqrt(beta[t]);
-        scale[t] = beta[t] > 0.0 ? 1.0 / beta[t] : 0.0;
-    }
-    if ((st = combine(ctx->gm_V[0], ctx->gm_V[0], nullptr, 0, 1.0, scale.data())) != BIOT_OK) return st;
+    CU(dots(ctx->gm_V[0], Vd, 1, d_scale, d_beta, true));              // beta_t, 1 / beta_t
+    CU(combine(ctx->gm_V[0], ctx->gm_V[0], nullptr, 0, 1.0, d_scale));
     for (int j = 0; j < k; ++j) {
         // w = P~2^{-1} AA v_j into v_{j+1}
         biot::Tile2dArgs a = tile_args(biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1]);
         CU(biot::launch_tile2d(ctx->gm_tmap[j], a, ctx->shape, ctx->stream));
-        // CGS2: two passes of h = V^T w, w -= V h
+        // CGS2: two passes of h = V^T w (accumulated into column j of H), w -= V h
         for (int pass = 0; pass < 2; ++pass) {
-            if ((st = dots(ctx->gm_V[j + 1], Vd, j + 1, h1.data())) != BIOT_OK) return st;
-            for (int i = 0; i <= j; ++i)
-                for (int t = 0; t < nt; ++t) H[(size_t)t * (k + 1) * k + i + (size_t)j * (k + 1)] += h1[(size_t)i * nt + t];
-            if ((st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], h1.data(), j + 1, -1.0, nullptr)) != BIOT_OK)
-                return st;
+            CU(dots(ctx->gm_V[j + 1], Vd, j + 1, d_h, hcol(0, j), false));
+            CU(combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], d_h, j + 1, -1.0, nullptr));
         }
-        if ((st = dots(ctx->gm_V[j + 1], Vd + (j + 1), 1, hn.data())) != BIOT_OK) return st;
-        for (int t = 0; t < nt; ++t) {
-            hn[t] = std::sqrt(hn[t]);
-            H[(size_t)t * (k + 1) * k + (j + 1) + (size_t)j * (k + 1)] = hn[t];
-            scale[t] = hn[t] > 0.0 ? 1.0 / hn[t] : 0.0;
-        }
-        if ((st = combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], nullptr, 0, 1.0, scale.data())) != BIOT_OK) return st;
+        CU(dots(ctx->gm_V[j + 1], Vd + (j + 1), 1, d_scale, hcol(j + 1, j), true));   // h_{j+1,j}
+        CU(combine(ctx->gm_V[j + 1], ctx->gm_V[j + 1], nullptr, 0, 1.0, d_scale));
     }
     // y_t = argmin || beta_t e1 - H_t y ||, x_out = x_in + V y
-    for (int t = 0; t < nt; ++t) {
-        std::vector<double> Ht(H.begin() + (size_t)t * (k + 1) * k, H.begin() + (size_t)(t + 1) * (k + 1) * k);
-        double yt[32];
-        hessenberg_lsq(k, Ht, beta[t], yt);
-        for (int j = 0; j < k; ++j) y[(size_t)j * nt + t] = yt[j];
-    }
-    return combine(xout, xin, y.data(), k, 1.0, nullptr);
+    CU(biot::gmres_lsq(d_H, d_beta, k, nt, d_y, ctx->stream));
+    CU(combine(xout, xin, d_y, k, 1.0, nullptr));
+    return BIOT_OK;
 }
 
 biot_status gmres_check(biot_ctx *ctx, int32_t K, int32_t k) {
@@ -798,6 +755,21 @@ biot_status biot_nccl_unique_id(void *out) {
     ncclResult_t r = api->GetUniqueId(&id);
     if (r != ncclSuccess) return fail(nullptr, BIOT_E_NCCL, "ncclGetUniqueId failed");
     std::memcpy(out, &id, sizeof(id));
+    return BIOT_OK;
+}
+
+biot_status biot_assemble_loads_host(const biot_mesh *mesh, const biot_material *mat, const biot_bc *bc,
+                                     double dt, int32_t *n_terms, double *F, int32_t *kinds, int32_t *src) {
+    if (!mesh || !mat || !bc || !n_terms) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    biot::HostOperator op;
+    std::string m = biot::assemble(*mesh, *mat, *bc, dt, op);
+    if (!m.empty()) return fail(nullptr, BIOT_E_INVALID, m);
+    *n_terms = (int32_t)op.extra.size();
+    for (size_t j = 0; j < op.extra.size(); ++j) {
+        if (F) std::memcpy(F + j * op.extra[j].f.size(), op.extra[j].f.data(), op.extra[j].f.size() * sizeof(double));
+        if (kinds) kinds[j] = op.extra[j].kind;
+        if (src) src[j] = op.extra[j].src;
+    }
     return BIOT_OK;
 }
 

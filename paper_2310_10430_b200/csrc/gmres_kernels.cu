@@ -55,14 +55,60 @@ __global__ void __launch_bounds__(kCols * kRowsY)
     }
 }
 
-// Stage 2: fixed-order sum over the row chunks.
-__global__ void dots_stage2(const double *__restrict__ part, int chunks, int nb, int n_tl, double *__restrict__ out) {
+// Stage 2: fixed-order sum over the row chunks, then by mode:
+//   dots: out[i][t] = s, and (hacc != null) hacc[i * n_tl + t] += s  (Hessenberg column);
+//   norm (nb = 1): n = sqrt(s), out[t] = 1 / n (0 if n = 0: the normalisation scale),
+//                  and (hacc != null) hacc[t] = n  (beta or the subdiagonal entry).
+__global__ void dots_stage2(const double *__restrict__ part, int chunks, int nb, int n_tl, double *__restrict__ out,
+                            double *__restrict__ hacc, int norm) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= (int64_t)nb * n_tl) return;
     const int i = (int)(k / n_tl), t = (int)(k % n_tl);
     double s = 0.0;
     for (int c = 0; c < chunks; ++c) s += part[((int64_t)c * nb + i) * n_tl + t];
-    out[(int64_t)i * n_tl + t] = s;
+    if (norm) {
+        const double n = sqrt(s);
+        out[t] = n > 0.0 ? 1.0 / n : 0.0;
+        if (hacc) hacc[t] = n;
+    } else {
+        out[(int64_t)i * n_tl + t] = s;
+        if (hacc) hacc[(int64_t)i * n_tl + t] += s;
+    }
+}
+
+// Per time step t: y = argmin || beta e1 - H y || for the (k+1) x k upper Hessenberg H of
+// step t (entry (i, j) at H[(i + j (k+1)) n_tl + t]) by Givens rotations, then back
+// substitution; zero pivots (breakdown) give zero coefficients.  y[j * n_tl + t].
+__global__ void lsq_kernel(const double *__restrict__ H, const double *__restrict__ beta, int k, int n_tl,
+                           double *__restrict__ y) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_tl) return;
+    const int ld = k + 1;
+    double h[(kMaxVec) * (kMaxVec - 1)], g[kMaxVec], yy[kMaxVec - 1];
+    for (int e = 0; e < ld * k; ++e) h[e] = H[(int64_t)e * n_tl + t];
+    for (int i = 0; i <= k; ++i) g[i] = 0.0;
+    g[0] = beta[t];
+    for (int j = 0; j < k; ++j) {
+        const double a = h[j + j * ld], b = h[j + 1 + j * ld];
+        const double rr = hypot(a, b);
+        if (rr == 0.0) continue;
+        const double c = a / rr, sn = b / rr;
+        for (int jj = j; jj < k; ++jj) {
+            const double u = h[j + jj * ld], v = h[j + 1 + jj * ld];
+            h[j + jj * ld] = c * u + sn * v;
+            h[j + 1 + jj * ld] = -sn * u + c * v;
+        }
+        const double gu = g[j], gv = g[j + 1];
+        g[j] = c * gu + sn * gv;
+        g[j + 1] = -sn * gu + c * gv;
+    }
+    for (int j = k - 1; j >= 0; --j) {
+        double v = g[j];
+        for (int jj = j + 1; jj < k; ++jj) v -= h[j + jj * ld] * yy[jj];
+        const double d = h[j + j * ld];
+        yy[j] = (fabs(d) > 1e-300) ? v / d : 0.0;
+    }
+    for (int j = 0; j < k; ++j) y[(int64_t)j * n_tl + t] = yy[j];
 }
 
 // dst[row][t] = scale[t] * (base[row][t] + sign * sum_i coef[i][t] * b_i[row][boff + t])
@@ -96,6 +142,12 @@ __global__ void __launch_bounds__(kCols * 8)
 
 int gmres_max_vectors() { return kMaxVec; }
 
+cudaError_t gmres_lsq(const double *H, const double *beta, int k, int n_tl, double *y, cudaStream_t st) {
+    if (k < 1 || k > kMaxVec - 1) return cudaErrorInvalidValue;
+    lsq_kernel<<<(n_tl + 127) / 128, 128, 0, st>>>(H, beta, k, n_tl, y);
+    return cudaGetLastError();
+}
+
 int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *chunks) {
     // ~512 row chunks: enough blocks for the GPU at any n_tl
     int64_t ch = (rows + 511) / 512;
@@ -106,7 +158,8 @@ int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *
 }
 
 cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, int nb, int64_t rows, int64_t pitch,
-                       int n_tl, double *scratch, double *out, cudaStream_t st) {
+                       int n_tl, double *scratch, double *out, double *hacc, bool norm, cudaStream_t st) {
+    if (norm && nb != 1) return cudaErrorInvalidValue;
     if (nb < 1 || nb > kMaxVec) return cudaErrorInvalidValue;
     int64_t chunk;
     int chunks;
@@ -120,7 +173,7 @@ cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, in
 #undef BIOT_D
     }
     const int64_t n = (int64_t)nb * n_tl;
-    dots_stage2<<<(int)((n + 255) / 256), 256, 0, st>>>(scratch, chunks, nb, n_tl, out);
+    dots_stage2<<<(int)((n + 255) / 256), 256, 0, st>>>(scratch, chunks, nb, n_tl, out, hacc, norm ? 1 : 0);
     return cudaGetLastError();
 }
 

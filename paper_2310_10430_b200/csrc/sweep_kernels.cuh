@@ -156,10 +156,13 @@ int gmres_max_vectors();
 int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *chunks);
 // (boff: column offset applied to the b panels -- a time window of them)
 cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, int nb, int64_t rows, int64_t pitch,
-                       int n_tl, double *scratch, double *out, cudaStream_t st);
+                       int n_tl, double *scratch, double *out, double *hacc, bool norm, cudaStream_t st);
 cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, int boff, const double *coef,
                           int nb, double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl,
                           cudaStream_t st);
+// per step t: y = argmin || beta_t e1 - H_t y ||, H_t (k+1) x k upper Hessenberg at
+// H[(i + j (k+1)) n_tl + t] (Givens rotations on the device, one thread per step)
+cudaError_t gmres_lsq(const double *H, const double *beta, int k, int n_tl, double *y, cudaStream_t st);
 
 bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);

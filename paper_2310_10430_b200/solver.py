@@ -38,6 +38,27 @@ def assemble_host(prob, dt, beta=None):
     return (Ai, Aj, Av), (Pi, Pj, Pv), f, dinv
 
 
+def assemble_loads_host(prob, dt, beta=None):
+    """biot_assemble_loads_host: the library's further load terms (R24), node-interleaved
+    [n_terms, n_dof], with their kinds (0 source, 1 lifting at c_n, 2 at c_{n-1}) and
+    source indices."""
+    L = _lib.load()
+    inp = Inputs(prob, beta=beta)
+    n = ctypes.c_int32()
+    I32 = ctypes.POINTER(ctypes.c_int32)
+    check(L.biot_assemble_loads_host(ctypes.byref(inp.mesh), ctypes.byref(inp.mat), ctypes.byref(inp.bc), dt,
+                                     ctypes.byref(n), None, None, None))
+    ndof = prob.coords.shape[0] * (prob.dim + 1)
+    F = np.zeros((n.value, ndof))
+    kinds = np.zeros(n.value, np.int32)
+    src = np.zeros(n.value, np.int32)
+    check(L.biot_assemble_loads_host(ctypes.byref(inp.mesh), ctypes.byref(inp.mat), ctypes.byref(inp.bc), dt,
+                                     ctypes.byref(n), ptr(F), ptr(kinds, I32), ptr(src, I32)))
+    if inp.cb_error is not None:
+        raise inp.cb_error
+    return F, kinds, src
+
+
 class BiotSolver:
     def __init__(self, prob, n_t=None, dt=None, precond=2, omega=0.5, device=0, rank=0, world=1,
                  nccl_id=None, stream=None, flags=0, history=0, load_scale=None, x_initial=None,
