@@ -12,21 +12,31 @@ namespace biot {
 
 namespace {
 
-constexpr int kCols = 64;     // time steps per block (threads along t: coalesced rows)
-constexpr int kRowsY = 4;     // row lanes per block
+// Block shapes: COLS threads along t (coalesced row segments) x 256 / COLS row lanes.
+// Wide windows use COLS = 64; the narrow windows of the Gauss-Seidel wavefront (a few
+// steps) use COLS = 8 or 2 so that most threads still have a column to work on.
+constexpr int kThr = 256;
 constexpr int kMaxVec = 17;   // Krylov vectors a dot / combine call may touch (k <= 16)
 
-// Stage 1: block (column block bx, row chunk by) sums rows [by*chunk, ..) of
-// a[row][t] * b_i[row][boff + t] for i < NB, in a fixed split over the kRowsY row lanes,
-// then in fixed lane order; out[(by * NB + i) * n_tl + t].  NB is a template parameter
-// so the loads of one row are issued together (no predicates), 4 rows per iteration.
-template <int NB>
-__global__ void __launch_bounds__(kCols * kRowsY)
+// Stage 1: for every row chunk c (rows [c*chunk, ..)) the partial sums of
+// a[row][t] * b_i[row][boff + t], i < NB, in a fixed split over kLanes = 4 row lanes and then
+// in fixed lane order; out[(c * NB + i) * n_tl + t].  A block holds kCols columns x 4
+// lanes x kCPB = 256 / (4 kCols) chunks, so the summation order of a column depends only on
+// the (fixed) chunk size, not on the block shape chosen for the window width: results are
+// independent of how many columns a call covers (time slabs stay bitwise).  NB is a template
+// parameter so the loads of one row are issued together (no predicates).
+constexpr int kLanes = 4;
+
+template <int NB, int kCols>
+__global__ void __launch_bounds__(kThr)
     dots_stage1(const double *__restrict__ a, const double *const *__restrict__ b, int boff, int64_t rows,
-                int64_t pitch, int n_tl, int64_t chunk, double *__restrict__ out) {
-    extern __shared__ double sm[];   // [kRowsY][NB][kCols]
+                int64_t pitch, int n_tl, int64_t chunk, int chunks, double *__restrict__ out) {
+    constexpr int kCPB = kThr / (kCols * kLanes);
+    extern __shared__ double sm[];   // [kCPB][kLanes][NB][kCols]
+    const int lane = threadIdx.y % kLanes, z = threadIdx.y / kLanes;
     const int t = blockIdx.x * kCols + threadIdx.x;
-    const int64_t r0 = blockIdx.y * chunk, r1 = min(rows, r0 + chunk);
+    const int c = blockIdx.y * kCPB + z;
+    const int64_t r0 = (int64_t)c * chunk, r1 = c < chunks ? min(rows, r0 + chunk) : r0;
     const double *bp[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) bp[i] = b[i] + boff;
@@ -35,37 +45,50 @@ __global__ void __launch_bounds__(kCols * kRowsY)
     for (int i = 0; i < NB; ++i) acc[i] = 0.0;
     if (t < n_tl) {
 #pragma unroll 4
-        for (int64_t r = r0 + threadIdx.y; r < r1; r += kRowsY) {
+        for (int64_t r = r0 + lane; r < r1; r += kLanes) {
             const int64_t o = r * pitch + t;
             const double av = a[o];
 #pragma unroll
             for (int i = 0; i < NB; ++i) acc[i] = fma(av, bp[i][o], acc[i]);
         }
     }
+    double *smz = sm + (size_t)z * kLanes * NB * kCols;
 #pragma unroll
-    for (int i = 0; i < NB; ++i) sm[(threadIdx.y * NB + i) * kCols + threadIdx.x] = acc[i];
+    for (int i = 0; i < NB; ++i) smz[(lane * NB + i) * kCols + threadIdx.x] = acc[i];
     __syncthreads();
-    if (threadIdx.y == 0 && t < n_tl) {
-#pragma unroll
-        for (int i = 0; i < NB; ++i) {
+    // lane l of each chunk sums vector i = l, l + 4, ... over the lanes in fixed order
+    if (t < n_tl && c < chunks)
+        for (int i = lane; i < NB; i += kLanes) {
             double s = 0.0;
-            for (int y = 0; y < kRowsY; ++y) s += sm[(y * NB + i) * kCols + threadIdx.x];
-            out[((int64_t)blockIdx.y * NB + i) * n_tl + t] = s;
+#pragma unroll
+            for (int y = 0; y < kLanes; ++y) s += smz[(y * NB + i) * kCols + threadIdx.x];
+            out[((int64_t)c * NB + i) * n_tl + t] = s;
         }
-    }
 }
 
 // Stage 2: fixed-order sum over the row chunks, then by mode:
 //   dots: out[i][t] = s, and (hacc != null) hacc[i * n_tl + t] += s  (Hessenberg column);
 //   norm (nb = 1): n = sqrt(s), out[t] = 1 / n (0 if n = 0: the normalisation scale),
 //                  and (hacc != null) hacc[t] = n  (beta or the subdiagonal entry).
-__global__ void dots_stage2(const double *__restrict__ part, int chunks, int nb, int n_tl, double *__restrict__ out,
-                            double *__restrict__ hacc, int norm) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= (int64_t)nb * n_tl) return;
-    const int i = (int)(k / n_tl), t = (int)(k % n_tl);
+// One block of kS2 threads per output (i, t): thread j sums chunks j, j + kS2, ... in order,
+// then a fixed shared-memory tree (the order depends on the chunk count only).
+constexpr int kS2 = 128;
+
+__global__ void __launch_bounds__(kS2) dots_stage2(const double *__restrict__ part, int chunks, int nb, int n_tl,
+                                                   double *__restrict__ out, double *__restrict__ hacc, int norm) {
+    __shared__ double red[kS2];
+    const int i = blockIdx.x / n_tl, t = blockIdx.x % n_tl;
     double s = 0.0;
-    for (int c = 0; c < chunks; ++c) s += part[((int64_t)c * nb + i) * n_tl + t];
+    for (int c = threadIdx.x; c < chunks; c += kS2) s += part[((int64_t)c * nb + i) * n_tl + t];
+    red[threadIdx.x] = s;
+    __syncthreads();
+#pragma unroll
+    for (int w = kS2 / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    s = red[0];
     if (norm) {
         const double n = sqrt(s);
         out[t] = n > 0.0 ? 1.0 / n : 0.0;
@@ -113,8 +136,8 @@ __global__ void lsq_kernel(const double *__restrict__ H, const double *__restric
 
 // dst[row][t] = scale[t] * (base[row][t] + sign * sum_i coef[i][t] * b_i[row][boff + t])
 // (scale == nullptr: 1; base may alias dst).
-template <int NB>
-__global__ void __launch_bounds__(kCols * 8)
+template <int NB, int kCols>
+__global__ void __launch_bounds__(kThr)
     combine_kernel(double *dst, const double *base, const double *const *__restrict__ b, int boff,
                    const double *__restrict__ coef, double sign, const double *__restrict__ scale, int64_t rows,
                    int64_t pitch, int n_tl) {
@@ -148,10 +171,14 @@ cudaError_t gmres_lsq(const double *H, const double *beta, int k, int n_tl, doub
     return cudaGetLastError();
 }
 
+int cols_for(int n_tl) { return n_tl > 16 ? 64 : n_tl > 2 ? 8 : 2; }
+
 int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *chunks) {
-    // ~512 row chunks: enough blocks for the GPU at any n_tl
-    int64_t ch = (rows + 511) / 512;
-    if (ch < 256) ch = 256;
+    // ~2048 row chunks whatever the window width (the summation order depends on it only):
+    // enough independent rows in flight for the narrow windows of the wavefront
+    (void)n_tl;
+    int64_t ch = (rows + 2047) / 2048;
+    if (ch < 64) ch = 64;
     *chunk = ch;
     *chunks = (int)((rows + ch - 1) / ch);
     return (int64_t)(*chunks) * nb * n_tl;
@@ -164,16 +191,19 @@ cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, in
     int64_t chunk;
     int chunks;
     gmres_dots_scratch(rows, n_tl, nb, &chunk, &chunks);
-    const dim3 g1((n_tl + kCols - 1) / kCols, chunks), b1(kCols, kRowsY);
-    const size_t sh = (size_t)kRowsY * nb * kCols * sizeof(double);
-    switch (nb) {
-#define BIOT_D(N) case N: dots_stage1<N><<<g1, b1, sh, st>>>(a, b_dev, boff, rows, pitch, n_tl, chunk, scratch); break;
+    const int cols = cols_for(n_tl), cpb = kThr / (cols * kLanes);
+    const dim3 g1((n_tl + cols - 1) / cols, (chunks + cpb - 1) / cpb), b1(cols, kThr / cols);
+    const size_t sh = (size_t)kThr * nb * sizeof(double);
+    switch (nb * 100 + cols) {
+#define BIOT_D1(N, C) case N * 100 + C: dots_stage1<N, C><<<g1, b1, sh, st>>>(a, b_dev, boff, rows, pitch, n_tl, chunk, chunks, scratch); break;
+#define BIOT_D(N) BIOT_D1(N, 64) BIOT_D1(N, 8) BIOT_D1(N, 2)
         BIOT_D(1) BIOT_D(2) BIOT_D(3) BIOT_D(4) BIOT_D(5) BIOT_D(6) BIOT_D(7) BIOT_D(8) BIOT_D(9)
         BIOT_D(10) BIOT_D(11) BIOT_D(12) BIOT_D(13) BIOT_D(14) BIOT_D(15) BIOT_D(16) BIOT_D(17)
 #undef BIOT_D
+#undef BIOT_D1
     }
     const int64_t n = (int64_t)nb * n_tl;
-    dots_stage2<<<(int)((n + 255) / 256), 256, 0, st>>>(scratch, chunks, nb, n_tl, out, hacc, norm ? 1 : 0);
+    dots_stage2<<<(int)n, kS2, 0, st>>>(scratch, chunks, nb, n_tl, out, hacc, norm ? 1 : 0);
     return cudaGetLastError();
 }
 
@@ -181,13 +211,16 @@ cudaError_t gmres_combine(double *dst, const double *base, const double *const *
                           int nb, double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl,
                           cudaStream_t st) {
     if (nb < 0 || nb > kMaxVec) return cudaErrorInvalidValue;
-    const int gy = (int)((rows + 7) / 8 < 4096 ? (rows + 7) / 8 : 4096);
-    const dim3 g2((n_tl + kCols - 1) / kCols, gy), b2(kCols, 8);
-    switch (nb) {
-#define BIOT_C(N) case N: combine_kernel<N><<<g2, b2, 0, st>>>(dst, base, b_dev, boff, coef, sign, scale, rows, pitch, n_tl); break;
+    const int cols = cols_for(n_tl), ry = kThr / cols;
+    const int gy = (int)((rows + ry - 1) / ry < 4096 ? (rows + ry - 1) / ry : 4096);
+    const dim3 g2((n_tl + cols - 1) / cols, gy), b2(cols, ry);
+    switch (nb * 100 + cols) {
+#define BIOT_C1(N, C) case N * 100 + C: combine_kernel<N, C><<<g2, b2, 0, st>>>(dst, base, b_dev, boff, coef, sign, scale, rows, pitch, n_tl); break;
+#define BIOT_C(N) BIOT_C1(N, 64) BIOT_C1(N, 8) BIOT_C1(N, 2)
         BIOT_C(0) BIOT_C(1) BIOT_C(2) BIOT_C(3) BIOT_C(4) BIOT_C(5) BIOT_C(6) BIOT_C(7) BIOT_C(8) BIOT_C(9)
         BIOT_C(10) BIOT_C(11) BIOT_C(12) BIOT_C(13) BIOT_C(14) BIOT_C(15) BIOT_C(16) BIOT_C(17)
 #undef BIOT_C
+#undef BIOT_C1
     }
     return cudaGetLastError();
 }
