@@ -46,12 +46,14 @@ def parse():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
-    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs", "gmres", "gs_gmres"],
+    ap.add_argument("--method", default="jacobi", choices=["jacobi", "gs", "gmres", "gs_gmres", "cheb"],
                     help="jacobi: all steps at once (BASELINE metric); gs: Gauss-Seidel in time "
                          "(PAPER.md Alg. 2 literal) as a wavefront; gmres: Alg. 3 with one GMRES(k) "
                          "cycle per step and outer iteration (left P~2); gs_gmres: Alg. 3 literally "
                          "(Gauss-Seidel in time + GMRES(k)) on the wavefront")
     ap.add_argument("--gmres-k", type=int, default=10)
+    ap.add_argument("--cheb-m", type=int, default=2, help="Chebyshev steps per inner inverse (--method cheb)")
+    ap.add_argument("--cheb-alpha", type=float, default=30.0)
     return ap.parse_args()
 
 
@@ -204,7 +206,9 @@ def workload_config(args, prob, world):
                         + (", Gauss-Seidel in time (wavefront)" if args.method == "gs" else "")
                         + (f", per-step GMRES({args.gmres_k})" if args.method == "gmres" else "")
                         + (f", Alg. 3: Gauss-Seidel in time + GMRES({args.gmres_k})" if args.method == "gs_gmres"
-                           else ""),
+                           else "")
+                        + (f", P~2 with Chebyshev({args.cheb_m}) inner inverses (alpha {args.cheb_alpha})"
+                           if args.method == "cheb" else ""),
             "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
             "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
             "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
@@ -284,6 +288,8 @@ def main():
         step = lambda K: g.iterate_gmres(K, args.gmres_k)
     elif args.method == "gs_gmres":
         step = lambda K: g.iterate_gs_gmres(K, args.gmres_k)
+    elif args.method == "cheb":
+        step = lambda K: g.iterate_cheb(K, args.cheb_m, args.cheb_alpha)
     else:
         step = g.iterate_gs if args.method == "gs" else g.iterate
     clk = ClockSampler(local)
@@ -339,6 +345,13 @@ def main():
             # one GMRES(k) cycle = 7 + 14k + 2k^2 passes over a space-time panel
             kk = args.gmres_k
             algo_bytes = (7 + 14 * kk + 2 * kk * kk) * 8.0 * prob.n_dof * info.n_t_local
+        if args.method == "cheb":
+            # panel passes per outer iteration: residual 2, start 2 + 1/nc
+            # (m = 1: 3 with the update), step k: 5 (+1 from k = 2 on), the last one 4 (+1)
+            mm, nc = args.cheb_m, prob.dim + 1
+            passes = 5.0 if mm == 1 else 2 + 2 + 1.0 / nc + sum(
+                (4 if k == mm - 1 else 5) + (1 if k >= 2 else 0) for k in range(1, mm))
+            algo_bytes = passes * 8.0 * prob.n_dof * info.n_t_local
         achieved_gbs = algo_bytes / (sweep_ms / 1e3) / 1e9
         sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
         fp64_meas_tf, fp64_nom_tf = fp64_peak(sm_max)
@@ -357,6 +370,10 @@ def main():
                                    f"{fp64_nom_tf:.1f} TFLOP/s",
                     "hbm_gbs": achieved_gbs, "hbm_peak": hbm}
         roof["kernel"] = KERNELS.get(info.kernel_path, f"kernel path {info.kernel_path}")
+        if args.method in ("gmres", "gs_gmres", "cheb", "gs"):
+            roof["kernel"] = ("whole outer iteration (events around all its kernels): " + roof["kernel"]
+                              + {"gmres": " + GMRES panel kernels", "gs_gmres": " + GMRES panel kernels",
+                                 "cheb": " + cheb_init/cheb_step kernels", "gs": " on the wavefront windows"}[args.method])
         roof["kernel_ms"] = sweep_ms
         roof["algorithmic"] = {"bytes_per_launch": algo_bytes, "flops_per_launch": info.flops_per_iter,
                                "per_unit": "16 B and 2*(nnz(AA)+nnz(A'))/n_dof flop per space-time DoF "
@@ -365,6 +382,8 @@ def main():
         launches = per_step * args.steps
         if args.method == "gs":   # n_t + K - 1 waves and two checkerboard copies per call
             launches = 2 + (info.n_t_local + args.steps - 1) * per_step
+        if args.method == "cheb":   # residual sweep + finalize (1-2) + start + m - 1 steps
+            launches = args.steps * (info.launches_per_iter + args.cheb_m)
         if args.method in ("gmres", "gs_gmres"):   # residual + finalize, 2 + k (1 + 2 x 3 + 3) + 1 panel kernels
             launches = args.steps * (2 + 2 + 2 + args.gmres_k * (1 + 6 + 3) + 1)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

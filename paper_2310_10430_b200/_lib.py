@@ -66,7 +66,7 @@ class BiotInfo(ctypes.Structure):
 
 
 # every symbol include/biot_pit.h declares (checked by tests/test_abi.py)
-EXPORTS = ["biot_setup", "biot_set_iterate", "biot_set_load_scale", "biot_iterate", "biot_iterate_gs", "biot_iterate_gmres",
+EXPORTS = ["biot_setup", "biot_set_iterate", "biot_set_load_scale", "biot_iterate", "biot_iterate_gs", "biot_iterate_gmres", "biot_iterate_cheb",
            "biot_iterate_gs_gmres", "biot_gs_begin_gmres",
            "biot_gs_begin", "biot_gs_waves", "biot_gs_wave", "biot_gs_end",
            "biot_residual_norms", "biot_residual_history", "biot_solution", "biot_last_slice",
@@ -97,6 +97,7 @@ def load():
     L.biot_iterate_gs.argtypes = [ctx_p, ctypes.c_int32]
     L.biot_iterate_gmres.argtypes = [ctx_p, ctypes.c_int32, ctypes.c_int32]
     L.biot_iterate_gs_gmres.argtypes = [ctx_p, ctypes.c_int32, ctypes.c_int32]
+    L.biot_iterate_cheb.argtypes = [ctx_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_double]
     L.biot_gs_begin_gmres.argtypes = [ctx_p, ctypes.c_int32, ctypes.c_int32]
     L.biot_gs_begin.argtypes = [ctx_p, ctypes.c_int32]
     L.biot_gs_waves.argtypes = [ctx_p, ctypes.POINTER(ctypes.c_int32)]

@@ -170,6 +170,11 @@ struct biot_ctx {
     std::vector<CUtensorMap> gm_tmap;
     double **gm_Vdev = nullptr;
     double *gm_scratch = nullptr, *gm_small = nullptr;
+    // Chebyshev inner inverses (biot_iterate_cheb): Gershgorin bounds of D^{-1} A and
+    // D_S^{-1} S~p, the scaled-residual panel, d ping-pong and y panels
+    double lmax_u = 0.0, lmax_p = 0.0;
+    double *cb_base[4] = {nullptr, nullptr, nullptr, nullptr};
+    double *cb[4] = {nullptr, nullptr, nullptr, nullptr};   // s, d0, d1, y (at node 0)
     // Gauss-Seidel wavefront state (biot_gs_begin / biot_gs_wave / biot_gs_end)
     int32_t gs_K = 0, gs_w = 0, gs_k = 0;   // gs_k > 0: each window update is a GMRES(gs_k) cycle
     int64_t gs_k0 = 0;
@@ -229,6 +234,8 @@ void free_all(biot_ctx *c) {
                     (void *)c->gm_small})
         if (p) cudaFree(p);
     for (double *p : c->gm_Vbase) cudaFree(p);
+    for (double *p : c->cb_base)
+        if (p) cudaFree(p);
     for (cudaEvent_t e : {c->ev_a, c->ev_b})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_s) cudaEventDestroy(e);
@@ -594,7 +601,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
 // (Jacobi in time).  The N_t Krylov bases live in k+1 space-time panels; Arnoldi by
 // classical Gram-Schmidt with one reorthogonalisation (CGS2), every dot product and
 // update column-wise (one value per time step); the (k+1) x k least-squares problems
-// are solved on the host by Givens rotations.
+// are solved on the device by Givens rotations (one thread per step).
 namespace {
 
 biot_status gmres_alloc(biot_ctx *ctx, int k) {
@@ -929,6 +936,29 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->beta = op->beta;
     ctx->nnz_AA = op->nnz_AA;
     ctx->nnz_AP = op->nnz_AP;
+    {
+        // Gershgorin bounds of the diagonally scaled inner blocks (R22): max over free rows of
+        // sum_j |M_ij| / M_ii, M = A (displacement rows) or S~p = -AA_pp (pressure rows)
+        const int ncc = op->nc, dd = op->d, WB = biot::block_width(ncc);
+        double lu = 0.0, lp = 0.0;
+        for (int64_t i = 0; i < op->n_nodes; ++i)
+            for (int c = 0; c < ncc; ++c) {
+                const double dv = op->dinv[(size_t)i * ncc + c];
+                if (dv == 0.0) continue;
+                double sum = 0.0;
+                for (int sl = 0; sl < op->n_slots; ++sl) {
+                    const double *b = op->blk.data() + ((size_t)i * op->n_slots + sl) * WB;
+                    if (c < dd)
+                        for (int cc = 0; cc < dd; ++cc) sum += std::fabs(b[c * ncc + cc]);
+                    else
+                        sum += std::fabs(b[dd * ncc + dd]);
+                }
+                if (c < dd) lu = std::max(lu, sum * std::fabs(dv));
+                else lp = std::max(lp, sum * std::fabs(dv));
+            }
+        ctx->lmax_u = lu;
+        ctx->lmax_p = lp;
+    }
     ctx->hist_cap = opts->history > 0 ? opts->history : 1024;
     ctx->pitch = ((int64_t)ctx->n_tl + biot::kChunk - 1) / biot::kChunk * biot::kChunk;
     ctx->node_block = 8;
@@ -1551,6 +1581,100 @@ biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
                                  ctx->stream));
         ctx->send_dirty = true;
         ctx->iterations++;
+    }
+    CU(cudaEventRecord(ctx->ev_b, ctx->stream));
+    CU(cudaEventSynchronize(ctx->ev_b));
+    float tot = 0.f;
+    CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
+    ctx->last_ms_iter = tot / K;
+    ctx->last_ms_sweep = tot / K;
+    int nf = 0;
+    CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (nf) return fail(ctx, BIOT_E_NONFINITE, "a residual norm became non-finite");
+    return BIOT_OK;
+}
+
+// Chebyshev inner inverses inside P~2: per outer iteration the
+// residual with its norms (main kernel, P~1 first-pass mode: Z = (D_A^{-1} r_u, r_p)),
+// then m Chebyshev steps for A and S~p on all steps at once (cheb_kernels.cu), and the
+// damped update.  Jacobi in time; any mesh (generic kernels for the inner steps).
+biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha) {
+    if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
+    if (K < 0 || m < 1 || m > 64 || !(alpha > 1.0) || !std::isfinite(alpha))
+        return fail(ctx, BIOT_E_INVALID, "need K >= 0, 1 <= m <= 64 and alpha > 1");
+    if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "Chebyshev inner inverses are built for P~2 (precond = 2)");
+    if (K == 0) return BIOT_OK;
+    CU(cudaSetDevice(ctx->device));
+    const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
+    const int need = m == 1 ? 2 : m == 2 ? 3 : 4;   // s, d0 [, d1 [, y]]
+    for (int q = 0; q < need; ++q)
+        if (!ctx->cb_base[q]) {
+            ALLOC(ctx->cb_base[q], panel_bytes);
+            CU(cudaMemsetAsync(ctx->cb_base[q], 0, panel_bytes, ctx->stream));
+            ctx->cb[q] = ctx->cb_base[q] + ctx->pad * ctx->nc * ctx->pitch;
+        }
+    auto bounds = [&](double lmax, double &theta, double &delta) {
+        theta = 0.5 * (lmax + lmax / alpha);
+        delta = 0.5 * (lmax - lmax / alpha);
+    };
+    double th_u, de_u, th_p, de_p;
+    bounds(ctx->lmax_u, th_u, de_u);
+    bounds(ctx->lmax_p, th_p, de_p);
+    biot::ChebArgs c{};
+    c.blk = ctx->blk;
+    c.cols = ctx->cols;
+    for (int q = 0; q < 32; ++q) c.off[q] = q < (int)ctx->offsets.size() ? ctx->offsets[q] : 0;
+    c.dinv = ctx->dinv;
+    c.n_nodes = ctx->N;
+    c.pitch = ctx->pitch;
+    c.nc = ctx->nc;
+    c.n_tl = ctx->n_tl;
+    c.omega = ctx->omega;
+    c.inv_theta_u = th_u > 0.0 ? 1.0 / th_u : 0.0;
+    c.inv_theta_p = th_p > 0.0 ? 1.0 / th_p : 0.0;
+    CU(cudaEventRecord(ctx->ev_a, ctx->stream));
+    double *const zsave = ctx->z;
+    for (int32_t it = 0; it < K; ++it) {
+        biot_status st = halo_exchange(ctx);
+        if (st != BIOT_OK) { ctx->z = zsave; return st; }
+        const double *xin = ctx->x[ctx->cur];
+        double *xout = ctx->x[1 - ctx->cur];
+        // r and its norms; Z = (D_A^{-1} r_u, r_p) into the s panel (x_u into xout is
+        // overwritten by the last Chebyshev pass)
+        ctx->z = ctx->cb[0];
+        cudaError_t e = launch_main(ctx, biot::MODE_P1_PASS1, xin, xout);
+        ctx->z = zsave;
+        CU(e);
+        double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
+        CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
+                                 ctx->fin_scratch, ctx->stream));
+        c.s = ctx->cb[0];
+        c.x = xin;
+        c.xn = xout;
+        c.sendbuf = ctx->world > 1 ? ctx->sendbuf : nullptr;
+        c.last = m == 1;
+        c.dn = ctx->cb[1];
+        CU(biot::launch_cheb_init(c, ctx->stream));
+        double rho_u = de_u / th_u, rho_p = de_p / th_p;   // rho_0 = 1 / sigma
+        for (int k = 1; k < m; ++k) {
+            const double ru = 1.0 / (2.0 * th_u / de_u - rho_u), rp = 1.0 / (2.0 * th_p / de_p - rho_p);
+            c.c1_u = ru * rho_u;
+            c.c2_u = 2.0 * ru / de_u;
+            c.c1_p = rp * rho_p;
+            c.c2_p = 2.0 * rp / de_p;
+            rho_u = ru;
+            rho_p = rp;
+            c.d = ctx->cb[1 + (k - 1) % 2];
+            c.dn = ctx->cb[1 + k % 2];
+            c.y = k == 1 ? nullptr : ctx->cb[3];
+            c.yn = ctx->cb[3];
+            c.last = k == m - 1;
+            CU(biot::launch_cheb_step(ctx->d, ctx->path, ctx->S, c, ctx->stream));
+        }
+        ctx->cur = 1 - ctx->cur;
+        ctx->iterations++;
+        if (ctx->world > 1) ctx->send_dirty = false;
     }
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
     CU(cudaEventSynchronize(ctx->ev_b));

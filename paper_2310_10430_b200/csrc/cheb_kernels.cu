@@ -1,0 +1,167 @@
+// Chebyshev inner inverses for the block preconditioner P~2 (SURVEY §8(f) NEXT-1,
+// reading R22): z = P~2^{-1} r with A^{-1} and S~p^{-1} (PAPER.md eq. p2)
+// each replaced by m steps of Chebyshev iteration preconditioned by the diagonal, on
+// [lambda_max / alpha, lambda_max] of D^{-1} M (Gershgorin lambda_max per block).
+//
+// The outer iteration's residual r (with the previous-step coupling and the norms) comes
+// from the main kernel in its P~1 first-pass mode, which leaves Z = (D_A^{-1} r_u, r_p)
+// in a panel.  The Chebyshev recurrence then runs on the scaled residual s = D^{-1} r
+// (s_u = Z_u, s_p = D_S^{-1} Z_p), all time steps at once (the inner operators have no
+// time coupling):
+//     d_0 = s_0 / theta,  y_1 = d_0,
+//     s_k = s_{k-1} - D^{-1} M d_{k-1},
+//     d_k = rho_k rho_{k-1} d_{k-1} + (2 rho_k / delta) s_k,   y_{k+1} = y_k + d_k,
+// per block (M = A for the displacement rows, M = S~p = -AA_pp for the pressure rows,
+// each with its own theta, delta, rho), and finally x^{k+1} = x^k + omega (y_u, -y_p).
+// Panels are time-contiguous rows as everywhere: p[(node*nc + c)*pitch + t].
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "node_update.cuh"
+#include "sweep_kernels.cuh"
+
+namespace biot {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kCThreads = 256;
+
+// Elementwise start: s = D^{-1} r (in place on the Z panel: only the pressure rows
+// change), d_0 = s / theta; with m = 1 directly x^{k+1} = x + omega (d_u, -d_p).
+__global__ void __launch_bounds__(kCThreads) cheb_init_kernel(const ChebArgs a) {
+    const int nc = a.nc, d = nc - 1;
+    const int64_t n_rows = a.n_nodes * nc;
+    const int64_t tot = n_rows * a.n_tl;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < tot;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t row = k / a.n_tl;
+        const int t = (int)(k % a.n_tl);
+        const int c = (int)(row % nc);
+        const int64_t o = row * a.pitch + t;
+        const bool p = c == d;
+        const double sv = p ? __ldg(a.dinv + row) * a.s[o] : a.s[o];
+        const double dv = sv * (p ? a.inv_theta_p : a.inv_theta_u);
+        if (a.last) {
+            const double xv = a.x[o] + a.omega * (p ? -dv : dv);
+            a.xn[o] = xv;
+            if (a.sendbuf && t == a.n_tl - 1) a.sendbuf[row] = xv;
+        } else {
+            if (p) a.s[o] = sv;
+            a.dn[o] = dv;
+        }
+    }
+}
+
+// One Chebyshev step for node i over the lane's kT steps: M d from the operator blocks
+// (displacement-displacement entries and -AA_pp only: the inner operators are the
+// diagonal blocks of P~2), then the recurrence above.
+template <int D, int S, bool ELL>
+__global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) {
+    constexpr int NC = D + 1;
+    constexpr int W = (NC * NC + 2) / 2 * 2;
+    const int lane = threadIdx.x & 31;
+    const int n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    const int64_t P = a.pitch;
+    const int64_t n_warps = a.n_nodes * n_chunks;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t i = w / n_chunks;
+        const int t0 = (int)(w % n_chunks) * kChunk + lane * kT;
+        if (t0 >= a.n_tl) continue;
+        const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
+        double acc[NC][kT];
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) acc[c][tt] = 0.0;
+        for (int s = 0; s < S; ++s) {
+            const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
+            const double *__restrict__ dj = a.d + j * NC * P + t0;
+            double v[NC][kT];
+#pragma unroll
+            for (int cc = 0; cc < NC; ++cc) {
+                const double2 v01 = __ldg(reinterpret_cast<const double2 *>(dj + cc * P));
+                const double2 v23 = __ldg(reinterpret_cast<const double2 *>(dj + cc * P + 2));
+                v[cc][0] = v01.x;
+                v[cc][1] = v01.y;
+                v[cc][2] = v23.x;
+                v[cc][3] = v23.y;
+            }
+#pragma unroll
+            for (int c = 0; c < D; ++c)
+#pragma unroll
+                for (int cc = 0; cc < D; ++cc) {
+                    const double cf = __ldg(bp + s * W + c * NC + cc);
+#pragma unroll
+                    for (int tt = 0; tt < kT; ++tt) acc[c][tt] = fma(cf, v[cc][tt], acc[c][tt]);
+                }
+            const double cpp = -__ldg(bp + s * W + D * NC + D);   // S~p = -AA_pp
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) acc[D][tt] = fma(cpp, v[D][tt], acc[D][tt]);
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            const int64_t o = (i * NC + c) * P + t0;
+            const bool p = c == D;
+            const double dv = __ldg(a.dinv + i * NC + c);
+            const double c1 = p ? a.c1_p : a.c1_u, c2 = p ? a.c2_p : a.c2_u;
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) {
+                if (t0 + tt >= a.n_tl) break;
+                const double sn = a.s[o + tt] - dv * acc[c][tt];
+                const double dn = fma(c1, a.d[o + tt], c2 * sn);
+                const double yn = (a.y ? a.y[o + tt] : a.d[o + tt]) + dn;   // y_1 = d_0
+                if (a.last) {
+                    const double xv = fma(a.omega, p ? -yn : yn, a.x[o + tt]);
+                    a.xn[o + tt] = xv;
+                    if (a.sendbuf && t0 + tt == a.n_tl - 1) a.sendbuf[i * NC + c] = xv;
+                } else {
+                    a.s[o + tt] = sn;
+                    a.dn[o + tt] = dn;
+                    a.yn[o + tt] = yn;
+                }
+            }
+        }
+    }
+}
+
+using StepFn = void (*)(const ChebArgs);
+
+StepFn pick_step(int dim, int path, int S) {
+#define BIOT_CS(D_, S_, ELL_) \
+    if (dim == D_ && S == S_ && (path == 2) == ELL_) return cheb_step_kernel<D_, S_, ELL_>;
+    BIOT_CS(2, 7, false)
+    BIOT_CS(3, 15, false)
+    BIOT_CS(2, 8, true)
+    BIOT_CS(2, 16, true)
+    BIOT_CS(2, 32, true)
+    BIOT_CS(3, 8, true)
+    BIOT_CS(3, 16, true)
+    BIOT_CS(3, 32, true)
+#undef BIOT_CS
+    return nullptr;
+}
+
+int grid_for(int64_t work, int per_block) {
+    const int64_t g = (work + per_block - 1) / per_block;
+    return (int)(g < 148 * 16 ? (g < 1 ? 1 : g) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t launch_cheb_init(const ChebArgs &a, cudaStream_t st) {
+    cheb_init_kernel<<<grid_for(a.n_nodes * a.nc * a.n_tl, kCThreads), kCThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st) {
+    StepFn f = pick_step(dim, path, n_slots);
+    if (!f) return cudaErrorInvalidValue;
+    const int64_t n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    f<<<grid_for(a.n_nodes * n_chunks * 32, kCThreads), kCThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace biot

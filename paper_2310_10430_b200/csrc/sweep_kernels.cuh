@@ -164,6 +164,31 @@ cudaError_t gmres_combine(double *dst, const double *base, const double *const *
 // H[(i + j (k+1)) n_tl + t] (Givens rotations on the device, one thread per step)
 cudaError_t gmres_lsq(const double *H, const double *beta, int k, int n_tl, double *y, cudaStream_t st);
 
+// Chebyshev inner inverses of P~2 (cheb_kernels.cu): panels at node 0
+// with the context's padding and pitch.
+struct ChebArgs {
+    const double *blk;      // operator blocks [i][slot][W]
+    const int32_t *cols;    // ELL columns (null for BDIA)
+    int64_t off[32];        // BDIA offsets
+    const double *dinv;     // D_A^{-1} / D_S^{-1} per (node, comp)
+    int64_t n_nodes, pitch;
+    int32_t nc, n_tl;
+    double *s;              // scaled residual s = D^{-1} r (in place)
+    const double *d;        // d_{k-1}
+    double *dn;             // d_k
+    const double *y;        // y_{k-1} (null: y_1 = d_0)
+    double *yn;             // y_k
+    const double *x;        // x^k (last pass)
+    double *xn;             // x^{k+1} (last pass)
+    double *sendbuf;        // last step of x^{k+1} (multi-slab), or null
+    double c1_u, c2_u, c1_p, c2_p;          // rho_k rho_{k-1}, 2 rho_k / delta per block
+    double inv_theta_u, inv_theta_p;        // 1 / theta per block (the start)
+    double omega;
+    int32_t last;           // 1: write x^{k+1} instead of s, d, y
+};
+cudaError_t launch_cheb_init(const ChebArgs &a, cudaStream_t st);
+cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st);
+
 bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);
 cudaError_t launch_stencil(int dim, int R, int T, const StencilArgs &a, const LaunchShape &sh,

@@ -102,6 +102,9 @@ class BiotSolver:
     def iterate_gmres(self, K, k):
         check(self.lib.biot_iterate_gmres(self.ctx, K, k), self.ctx)
 
+    def iterate_cheb(self, K, m, alpha=30.0):
+        check(self.lib.biot_iterate_cheb(self.ctx, int(K), int(m), float(alpha)), self.ctx)
+
     def iterate_gs_gmres(self, K, k):
         check(self.lib.biot_iterate_gs_gmres(self.ctx, K, k), self.ctx)
 

@@ -1,0 +1,84 @@
+"""Chebyshev inner inverses of P~2 on the GPU (reading R22) -- needs
+a B200.  Parity at 1e-9 per field (R17) of x^K and the residual history against
+oracle/chebyshev.py (its own pins: closed-form polynomial, direct-solve limit, BE fixed
+point): 2D tile path (config 1, several m), the generic kernel, a 3D tile mesh and the
+§4.1 multi-load problem."""
+import numpy as np
+import pytest
+
+import oracle
+from oracle import chebyshev as ocheb
+from paper_2310_10430_b200 import BiotSolver
+from workloads import config_problem, make_problem, initial_iterate, load_scales, trig_problem
+
+from _parity import TOL, field_errors, norm_errors
+
+pytestmark = pytest.mark.gpu
+
+
+def _pair(prob, nt, K, m, omega=0.5, alpha=30.0, trig=False):
+    x0 = initial_iterate(prob.dirichlet, np.arange(1, nt + 1), 17)
+    S = oracle.OracleSystem(prob)
+    if trig:
+        s_or = S.coefs(np.zeros(nt), 1, nt)
+        g = BiotSolver(prob, n_t=nt, precond=2, omega=omega)
+    else:
+        s = load_scales(nt, parity=True)
+        s_or = s
+        g = BiotSolver(prob, n_t=nt, precond=2, omega=omega, load_scale=s)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate_cheb(K, m, alpha)
+        xg = g.solution()
+        hg = np.stack([g.residual_history(k) for k in range(K)])
+        path = g.info.kernel_path
+    finally:
+        g.close()
+    X = np.zeros((nt + 1, S.ndof))
+    if trig:
+        X[0] = S.to_paper(prob.x_initial) * S.free
+    X[1:] = S.to_paper(x0)
+    Xo, ho = ocheb.iterate(S, X, s_or, K, m, precond=2, omega=omega, alpha=alpha)
+    return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho), path
+
+
+@pytest.mark.parametrize("m", [1, 2, 4])
+def test_cheb_parity_config1(m):
+    prob = config_problem(1)
+    (xg, hg), (xo, ho), path = _pair(prob, 32, 10, m)
+    assert path == 5
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_cheb_parity_generic_kernel(monkeypatch):
+    monkeypatch.setenv("BIOT_KERNEL", "generic")
+    prob = config_problem(2)
+    (xg, hg), (xo, ho), path = _pair(prob, 40, 4, 3)
+    assert path == 1
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_cheb_parity_3d():
+    prob = make_problem(3, 6, 24, 1.0 / 24, 1, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0, kappa_seed=2)
+    (xg, hg), (xo, ho), path = _pair(prob, 24, 5, 2, omega=0.4)
+    assert path == 7
+    assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_cheb_parity_trig_multiload():
+    prob = trig_problem(4, 40, 1.0 / 64)
+    (xg, hg), (xo, ho), path = _pair(prob, 40, 6, 2, trig=True)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_cheb_m1_is_scaled_diagonal():
+    """m = 1 is the diagonal P~2 step with omega / theta per block: with a single block
+    bound this is biot_iterate at a rescaled omega -- here checked against the oracle's
+    closed form directly on the first iterate."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho), _ = _pair(prob, 8, 1, 1)
+    assert field_errors(xg, xo, 2).max() < TOL
