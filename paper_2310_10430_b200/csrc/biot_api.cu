@@ -1158,7 +1158,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             }
             r[13] = same ? 1.0 : 2.0;   // path flag: 1 interior template, 2 geometric-class stencil
             for (int j = 1; j < ctx->n_load; ++j)   // further load vectors (kMaxLoads kernels)
-                for (int c = 0; c < 3; ++c) r[16 + 3 * (j - 1) + c] = lterm_f[j][(size_t)i * 3 + c];
+                for (int c = 0; c < 3; ++c) r[14 + 3 * (j - 1) + c] = lterm_f[j][(size_t)i * 3 + c];
             n_int += same;
         }
         ctx->n_interior = n_int;

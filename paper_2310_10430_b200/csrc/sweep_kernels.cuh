@@ -76,7 +76,7 @@ struct StencilArgs : SweepArgs {
 // Arguments of the TMA-pipelined 2D tile kernel (tile2d_kernels.cu).
 struct Tile2dArgs : SweepArgs {
     static constexpr int kAux = 16;   // per-node record: AA_pp per slot [7], f [3], dinv [3], path flag
-    static constexpr int kAuxML = 32; // kMaxLoads kernels: + the further load vectors F_j at [16 + 3 (j-1) + c]
+    static constexpr int kAuxML = 24; // kMaxLoads kernels: + the further load vectors F_j at [14 + 3 (j-1) + c]
     double tmpl[7][10];               // interior stencil blocks (slot order), pp entry unused
     const double *aux;                // [n_alloc][kAux]
     const double *cls;                // geometric-class stencils [9][7][kClsW], column-major blocks

@@ -53,20 +53,23 @@ constexpr int kCW = Tile2dArgs::kClsW;      // doubles per class-stencil slot
 constexpr uint32_t kXBytes = kStrip * 3 * kCT * 8;                                 // 43008
 
 // Shared-memory layout by load-term count: single-load kernels stream 16-double aux
-// records through a 5-stage ring; the kMaxLoads kernels carry the further load vectors
-// in 32-double records (F_j at [16 + 3 (j-1) + c]) through 4 stages.
+// records through a 5-stage ring and stage the class stencils in shared memory; the
+// kMaxLoads kernels carry the further load vectors in 24-double records (F_j at
+// [14 + 3 (j-1) + c]) through 5 stages and read the class stencils (boundary nodes only)
+// from global memory, which frees the room for the longer records.
 template <int NL>
 struct Lay {
-    static constexpr int kStages = NL == 1 ? 5 : 4;
+    static constexpr int kStages = 5;
     static constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
     static constexpr uint32_t kAuxBytes = kSeg * kAuxRec * 8;
     static constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;
     static constexpr uint32_t kClsOff = kStages * kStageBytes;
-    static constexpr uint32_t kCarryOff = kClsOff + 9 * 7 * kCW * 8;
+    static constexpr uint32_t kCarryOff = kClsOff + (NL == 1 ? 9 * 7 * kCW * 8 : 0);
     static constexpr uint32_t kSmemBytes = kCarryOff + kMaxRR * kSeg * 8;
 };
 constexpr uint32_t kSmemBytes = Lay<1>::kSmemBytes > Lay<kMaxLoads>::kSmemBytes ? Lay<1>::kSmemBytes
                                                                                : Lay<kMaxLoads>::kSmemBytes;
+static_assert(kSmemBytes <= 232448, "tile2d shared memory exceeds 227 KB");
 
 // (row delta, column delta) of the 7 BDIA slots in storage order
 __host__ __device__ constexpr int sdr(int s) { return (s == 1 || s == 2) ? -1 : (s >= 5) ? 1 : 0; }
@@ -221,7 +224,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
                                                                            h * (kCT / 2)));
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const double fj = aux[16 + 3 * (j - 1) + c];
+                    const double fj = aux[14 + 3 * (j - 1) + c];
                     acc[c][2 * h] = fma(-s2.x, fj, acc[c][2 * h]);
                     acc[c][2 * h + 1] = fma(-s2.y, fj, acc[c][2 * h + 1]);
                 }
@@ -457,7 +460,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         fence_barrier_init();
     }
-    for (int k = threadIdx.x; k < 9 * 7 * kCW; k += blockDim.x) cls_sm[k] = a.cls[k];
+    if constexpr (NL == 1)
+        for (int k = threadIdx.x; k < 9 * 7 * kCW; k += blockDim.x) cls_sm[k] = a.cls[k];
     __syncthreads();
 
     if (warp >= kSeg) {
@@ -524,7 +528,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
             }
             double acc[3][kT2], q[kT2];
             int kindP = 0;                       // pending node (row m-1): 0 none, 1 interior, 2 class
-            const double *T = cls_sm;
+            const double *const cls_base = NL == 1 ? static_cast<const double *>(cls_sm) : a.cls;
+            const double *T = cls_base;
             int sd = it % kStages;               // stage of row m-1
             uint32_t phd = (it / kStages) & 1;
             mbar_wait_suspend(&full[sd], phd);
@@ -560,7 +565,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const double *aux = reinterpret_cast<const double *>(
                                                 reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
                         kindP = aux[13] == 1.0 ? 1 : 2;
-                        if (kindP == 2) T = cls_sm + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
+                        if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
                         if constexpr (MODE == MODE_PASS2) {   // bt rides in q
                             if (kindP == 1) start_bt<false, S0, Tile2dArgs>(a, pd, pm, p, lane, T, q);
                             else start_bt<true, S0, Tile2dArgs>(a, pd, pm, p, lane, T, q);
