@@ -153,9 +153,12 @@ def fp64_peak(sm_mhz):
 
 
 def load_traffic(cid):
+    """DRAM bytes (read + write) per launch of the dominant kernel from one ncu --set full
+    capture (profiles/traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        return json.load(open(p)).get(cid if isinstance(cid, str) else f"config{cid}")
+        t = json.load(open(p)).get(cid if isinstance(cid, str) else f"config{cid}")
+        return None if t is None else float(t["bytes"])
     except Exception:
         return None
 
@@ -359,12 +362,18 @@ def main():
         if prob.dim == 2:
             roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                     "frac": achieved_gbs / hbm,
-                    "traffic": load_traffic("trig" if args.workload == "trig" else args.config),
+                    "traffic": (load_traffic("trig" if args.workload == "trig" else args.config)
+                                if args.method == "jacobi" and args.precond == 2 else None),
+                    "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                    "profiles/traffic.json)",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
                     "fp64_tflops": achieved_tf, "fp64_peak_tflops_measured": fp64_meas_tf}
         else:
             roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_meas_tf, "unit": "TFLOP/s",
-                    "frac": achieved_tf / fp64_meas_tf, "traffic": load_traffic(args.config),
+                    "frac": achieved_tf / fp64_meas_tf,
+                    "traffic": load_traffic(args.config) if args.method == "jacobi" and args.precond == 2 else None,
+                    "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                                    "profiles/traffic.json)",
                     "peak_source": "DFMA microbenchmark 58.8 FMA/clk/SM x 148 SMs x 2 x sm_max_mhz "
                                    "(profiles/r01_ubench_dfma.txt); nominal 64 FMA/clk/SM = "
                                    f"{fp64_nom_tf:.1f} TFLOP/s",
