@@ -359,7 +359,7 @@ def main():
         sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
         fp64_meas_tf, fp64_nom_tf = fp64_peak(sm_max)
         achieved_tf = info.flops_per_iter / (sweep_ms / 1e3) / 1e12
-        if prob.dim == 2:
+        if prob.dim == 2 or args.method in ("gmres", "gs_gmres", "cheb"):   # panel-pass bound
             roof = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                     "frac": achieved_gbs / hbm,
                     "traffic": (load_traffic("trig" if args.workload == "trig" else args.config)

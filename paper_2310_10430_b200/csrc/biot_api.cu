@@ -490,7 +490,10 @@ struct Window {
     double *send = nullptr;             // send slice (only when the window ends at the slab's last step)
 };
 
-cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, const Window *win = nullptr) {
+// tmo / zb (tile kernels only): the tensor map of xin and the Z panel, when they are not
+// the context's own (the GMRES Krylov panels).
+cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, const Window *win = nullptr,
+                        const CUtensorMap *tmo = nullptr, double *zb = nullptr) {
     if (c->kern == 2) {
         biot::StencilArgs a = stencil_args(c, mode, xin, xout);
         return biot::launch_stencil(c->d, c->sR, c->sT, a, c->shape, c->stream);
@@ -516,6 +519,8 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost_stride = win->stride;
             a.sendbuf = win->send;
         }
+        if (zb) a.zbuf = zb;
+        if (tmo) return biot::launch_tile3d(*tmo, a, c->shape, c->stream);
         if (mode == biot::MODE_PASS2) return biot::launch_tile3d(c->tmapz, a, c->shape, c->stream);
         return biot::launch_tile3d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
@@ -539,6 +544,8 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         }
         a.s0 = c->s0;
         a.dry = c->tile_dry;
+        if (zb) a.zbuf = zb;
+        if (tmo) return biot::launch_tile2d(*tmo, a, c->shape, c->stream);
         if (mode == biot::MODE_PASS2) return biot::launch_tile2d(c->tmapz, a, c->shape, c->stream);
         return biot::launch_tile2d(c->tmap[xin == c->x[0] ? 0 : 1], a, c->shape, c->stream);
     }
@@ -613,22 +620,38 @@ biot_status gmres_alloc(biot_ctx *ctx, int k) {
     if (!fn || qres != cudaDriverEntryPointSuccess)
         return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled not available");
     auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    uint32_t box[2];
-    biot::tile2d_box(box);
     while ((int)ctx->gm_V.size() < k + 1) {
         double *base = nullptr;
         ALLOC(base, panel_bytes);
         CU(cudaMemsetAsync(base, 0, panel_bytes, ctx->stream));
         ctx->gm_Vbase.push_back(base);
-        ctx->gm_V.push_back(base + ctx->pad * ctx->nc * ctx->pitch);
+        double *v0 = base + ctx->pad * ctx->nc * ctx->pitch;
+        ctx->gm_V.push_back(v0);
         CUtensorMap m;
-        cuuint64_t dims[2] = {(cuuint64_t)ctx->pitch, (cuuint64_t)ctx->rows_alloc};
-        cuuint64_t strides[1] = {(cuuint64_t)ctx->pitch * sizeof(double)};
-        cuuint32_t bx[2] = {box[0], box[1]};
-        cuuint32_t es[2] = {1, 1};
-        CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, bx, es,
-                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        CUresult r;
+        if (ctx->kern == 4) {   // as the 2D x panels: {time, panel rows}
+            uint32_t box[2];
+            biot::tile2d_box(box);
+            cuuint64_t dims[2] = {(cuuint64_t)ctx->pitch, (cuuint64_t)ctx->rows_alloc};
+            cuuint64_t strides[1] = {(cuuint64_t)ctx->pitch * sizeof(double)};
+            cuuint32_t bx[2] = {box[0], box[1]};
+            cuuint32_t es[2] = {1, 1};
+            r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, bx, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        } else {                // as the 3D x panels: {time, x*4 + c, y, z} at node 0
+            uint32_t box[4];
+            biot::tile3d_box(box);
+            const int64_t n1 = ctx->n1;
+            cuuint64_t dims[4] = {(cuuint64_t)ctx->pitch, (cuuint64_t)(n1 * 4), (cuuint64_t)n1, (cuuint64_t)n1};
+            const cuuint64_t rb = (cuuint64_t)ctx->pitch * sizeof(double);
+            cuuint64_t strides[3] = {rb, rb * (cuuint64_t)(n1 * 4), rb * (cuuint64_t)(n1 * n1 * 4)};
+            cuuint32_t bx[4] = {box[0], box[1], box[2], box[3]};
+            cuuint32_t es[4] = {1, 1, 1, 1};
+            r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, v0, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        }
         if (r != CUDA_SUCCESS) return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (V) failed");
         ctx->gm_tmap.push_back(m);
     }
@@ -682,35 +705,16 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
         return biot::gmres_combine(dst + c0, base + c0, Vd, c0, coef, nb, sign, scale, rows, ctx->pitch, nt,
                                    ctx->stream);
     };
-    auto tile_args = [&](int mode, const double *x, double *xn) {
-        biot::Tile2dArgs a{};
-        static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, x, xn);
-        std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
-        a.aux = ctx->aux;
-        a.cls = ctx->cls;
-        a.pad_nodes = ctx->pad;
-        a.s0 = ctx->s0;
-        a.sendbuf = nullptr;
-        a.t_off = win.t_off;
-        a.t_lo = win.t_lo;
-        a.n_tl = win.len;
-        a.ghost = win.ghost;
-        a.ghost_stride = win.stride;
-        return a;
-    };
+    Window w = win;          // tile passes of the cycle never write the send slice
+    w.send = nullptr;
     CU(cudaMemsetAsync(d_H, 0, (size_t)(k + 1) * k * nt * sizeof(double), ctx->stream));
     // v_0 = P~2^{-1} (b - AA x_in) with b = A' x_prev + f, and the norms of b - AA x_in
-    {
-        biot::Tile2dArgs a = tile_args(biot::MODE_ZOUT, xin, nullptr);
-        a.zbuf = ctx->gm_V[0];
-        CU(biot::launch_tile2d(tm, a, ctx->shape, ctx->stream));
-    }
+    CU(launch_main(ctx, biot::MODE_ZOUT, xin, nullptr, &w, &tm, ctx->gm_V[0]));
     CU(dots(ctx->gm_V[0], Vd, 1, d_scale, d_beta, true));              // beta_t, 1 / beta_t
     CU(combine(ctx->gm_V[0], ctx->gm_V[0], nullptr, 0, 1.0, d_scale));
     for (int j = 0; j < k; ++j) {
         // w = P~2^{-1} AA v_j into v_{j+1}
-        biot::Tile2dArgs a = tile_args(biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1]);
-        CU(biot::launch_tile2d(ctx->gm_tmap[j], a, ctx->shape, ctx->stream));
+        CU(launch_main(ctx, biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1], &w, &ctx->gm_tmap[j]));
         // CGS2: two passes of h = V^T w (accumulated into column j of H), w -= V h
         for (int pass = 0; pass < 2; ++pass) {
             CU(dots(ctx->gm_V[j + 1], Vd, j + 1, d_h, hcol(0, j), false));
@@ -728,7 +732,8 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
 biot_status gmres_check(biot_ctx *ctx, int32_t K, int32_t k) {
     if (K < 0 || k < 1 || k > biot::gmres_max_vectors() - 1)
         return fail(ctx, BIOT_E_INVALID, "need K >= 0 and 1 <= k <= " + std::to_string(biot::gmres_max_vectors() - 1));
-    if (ctx->kern != 4) return fail(ctx, BIOT_E_STATE, "per-step GMRES needs the 2D tile kernel (structured 2D mesh)");
+    if (ctx->kern != 4 && ctx->kern != 6)
+        return fail(ctx, BIOT_E_STATE, "per-step GMRES needs a tile kernel (structured 2D / 3D mesh)");
     if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "per-step GMRES is left-preconditioned by P~2 (precond = 2)");
     return BIOT_OK;
 }

@@ -205,6 +205,23 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
                                        double sv, const double *TA, const double *TB, double (&acc)[2][4],
                                        double (&q)[2], double &nu, double &npn) {
     accum_plane<1, NN, CLS, S0>(a, pu, sx, sy, lane, aux, TA, TB, acc, q);
+    if constexpr (MODE == MODE_MATVEC) {
+        // GMRES Arnoldi (R23): w = P~2^{-1} AA v, no time coupling, no load, no norms
+        if (t < a.n_tl && t >= a.t_lo) {
+            const int64_t P = a.pitch;
+#pragma unroll
+            for (int n = 0; n < NN; ++n) {
+                const double *ax = aux + n * kAuxRec;
+                const int64_t row = (iA + n) * 4 * P + a.t_off + t;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const double dv = ax[19 + c];
+                    a.xn[row + c * P] = c < 3 ? dv * acc[n][c] : -(dv * acc[n][c]);
+                }
+            }
+        }
+        return;
+    }
     double qp[2];
 #pragma unroll
     for (int n = 0; n < NN; ++n) qp[n] = __shfl_up_sync(0xffffffffu, q[n], 1);
@@ -237,10 +254,17 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
             acc1[c][0] = acc[n][c];
         }
         double outx[4][1], outz[4][1];
-        epilogue_math<3, 1, CLS>(a.omega, acc1, q1, qp[n], single_load(F, sv1), Dv, xs, nu1, np1, outx, outz);
+        epilogue_math<3, 1, CLS, MODE == MODE_ZOUT>(a.omega, acc1, q1, qp[n], single_load(F, sv1), Dv, xs, nu1, np1,
+                                                    outx, outz);
         nu += nu1[0];
         npn += np1[0];
-        if constexpr (MODE != MODE_RESIDUAL) {   // stores through one row pointer per node
+        if constexpr (MODE == MODE_ZOUT) {       // GMRES start: z = P~2^{-1} r, x untouched
+            if (t < a.n_tl && t >= a.t_lo) {
+                const int64_t P = a.pitch, row = (iA + n) * 4 * P + a.t_off + t;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) a.zbuf[row + c * P] = outz[c][0];
+            }
+        } else if constexpr (MODE != MODE_RESIDUAL) {   // stores through one row pointer per node
             constexpr int ncw = MODE == MODE_UPDATE_P2 ? 4 : 3;   // P~1: pressure written by pass 2
             if (t < a.n_tl && t >= a.t_lo) {
                 const int64_t P = a.pitch, row = (iA + n) * 4 * P + a.t_off + t;
@@ -510,7 +534,7 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
             if (lane == 0) mbar_arrive(&empty[sd]);       // plane zb
             it += (uint32_t)(zb - za + 2);
             // per-step norm partials of this (tile, chunk), fixed reduction order over warps
-            if constexpr (MODE == MODE_PASS2) continue;   // the norms come from pass 1
+            if constexpr (MODE == MODE_PASS2 || MODE == MODE_MATVEC) continue;   // no norms in these passes
             red[warp][lane][0] = t >= a.t_lo ? nu : 0.0;
             red[warp][lane][1] = t >= a.t_lo ? npn : 0.0;
             asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
@@ -558,7 +582,9 @@ cudaError_t tile3d_shape(int device, LaunchShape *out) {
     for (auto fn : {tile3d_kernel<false, kR, MODE_UPDATE_P2>, tile3d_kernel<true, kR, MODE_UPDATE_P2>,
                     tile3d_kernel<false, kR, MODE_P1_PASS1>, tile3d_kernel<true, kR, MODE_P1_PASS1>,
                     tile3d_kernel<false, kR, MODE_RESIDUAL>, tile3d_kernel<true, kR, MODE_RESIDUAL>,
-                    tile3d_kernel<false, kR, MODE_PASS2>, tile3d_kernel<true, kR, MODE_PASS2>}) {
+                    tile3d_kernel<false, kR, MODE_PASS2>, tile3d_kernel<true, kR, MODE_PASS2>,
+                    tile3d_kernel<false, kR, MODE_ZOUT>, tile3d_kernel<true, kR, MODE_ZOUT>,
+                    tile3d_kernel<false, kR, MODE_MATVEC>, tile3d_kernel<true, kR, MODE_MATVEC>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytesOf<kR>);
         if (e != cudaSuccess) return e;
     }
@@ -582,6 +608,8 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T3(true, MODE_UPDATE_P2); else BIOT_T3(false, MODE_UPDATE_P2); }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T3(true, MODE_P1_PASS1); else BIOT_T3(false, MODE_P1_PASS1); }
     else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T3(true, MODE_PASS2); else BIOT_T3(false, MODE_PASS2); }
+    else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T3(true, MODE_ZOUT); else BIOT_T3(false, MODE_ZOUT); }
+    else if (a.mode == MODE_MATVEC) { if (a.s0) BIOT_T3(true, MODE_MATVEC); else BIOT_T3(false, MODE_MATVEC); }
     else { if (a.s0) BIOT_T3(true, MODE_RESIDUAL); else BIOT_T3(false, MODE_RESIDUAL); }
 #undef BIOT_T3
     return cudaGetLastError();

@@ -354,3 +354,13 @@ def test_gs_gmres_exact_solves_are_backward_euler_in_one_sweep():
     Xbe = extras.sequential_be(S, np.zeros(S.ndof), s, 6)
     xbe = np.stack([S.from_paper(v) for v in Xbe[1:]])
     assert field_errors(xg, xbe, 2).max() < 1e-9
+
+
+@pytest.mark.parametrize("gs", [False, True])
+def test_gmres_parity_3d(gs):
+    """Per-step GMRES on the 3D tile kernel (ZOUT / MATVEC plane-march modes, 4D tensor
+    maps of the Krylov panels): Jacobi and Gauss-Seidel in time vs the oracle's Alg. 3."""
+    prob = make_problem(3, 6, 20, 1.0 / 20, 1, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0, kappa_seed=2)
+    (xg, hg), (xo, ho) = (_gs_gmres_pair if gs else _gmres_pair)(prob, 20, 2, 4)
+    assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
