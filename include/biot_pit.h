@@ -256,6 +256,28 @@ biot_status biot_last_timing(const biot_ctx *ctx, double *out_ms);
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 only; dlopens libnccl.so.2). */
 biot_status biot_nccl_unique_id(void *out);
 
+/* Host helpers for the paper's structured workloads (no device needed).
+ *
+ * biot_mesh_structured: the unit square (dim 2, n x n cells, each split by the
+ * lower-left -> upper-right diagonal into (n00, n10, n11) and (n00, n11, n01)) or the unit
+ * cube (dim 3, n^3 cells, 6 Kuhn tetrahedra {v, v+e_a, v+e_a+e_b, v+e_a+e_b+e_c} per cell,
+ * positively oriented); node id = j(n+1)+i (2D), (k(n+1)+j)(n+1)+i (3D) at (i,j[,k])/n
+ * ("uniform mesh, h = 1/2^k").  *coords (nn*dim) and
+ * *cells (nc*(dim+1)) are allocated by the library; release them with biot_free.
+ *
+ * biot_bc_column: the Terzaghi-type column of the BASELINE configs on such a mesh
+ * (PAPER.md L70-84): dirichlet[n_nodes*(dim+1)] = 1 for u_x on x in {0,1}, (3D: u_y on
+ * y in {0,1}), u on the bottom, p on the top; F[n_nodes*(dim+1)] = the load of the
+ * traction (0,..,-load) on the top face (exact P1 facet integral, |f|/dim per vertex;
+ * pressure entries 0); facets (may be NULL) receives the top facets, dim node ids each,
+ * *n_facets their number (query with facets = NULL).  Coordinates within 1e-12 of a face
+ * count as on it. */
+biot_status biot_mesh_structured(int32_t dim, int32_t n, double **coords, int32_t **cells, int64_t *n_nodes,
+                                 int64_t *n_cells);
+biot_status biot_bc_column(const biot_mesh *mesh, double load, uint8_t *dirichlet, double *F,
+                           int64_t *n_facets, int32_t *facets);
+void biot_free(void *p);
+
 void biot_destroy(biot_ctx *ctx);
 const char *biot_last_error(const biot_ctx *ctx);
 const char *biot_status_string(biot_status s);

@@ -72,7 +72,7 @@ EXPORTS = ["biot_setup", "biot_set_iterate", "biot_set_load_scale", "biot_iterat
            "biot_residual_norms", "biot_residual_history", "biot_solution", "biot_last_slice",
            "biot_set_ghost", "biot_assemble_host", "biot_assemble_loads_host", "biot_get_info", "biot_last_timing",
            "biot_nccl_unique_id", "biot_destroy", "biot_last_error", "biot_status_string",
-           "biot_abi_version"]
+           "biot_abi_version", "biot_mesh_structured", "biot_bc_column", "biot_free"]
 
 _lib = None
 
@@ -112,6 +112,10 @@ def load():
                                      _i64, _i64, _i64, _d, _i64, _i64, _i64, _d, _d, _d]
     L.biot_assemble_loads_host.argtypes = [P(BiotMesh), P(BiotMaterial), P(BiotBC), ctypes.c_double,
                                            P(ctypes.c_int32), _d, P(ctypes.c_int32), P(ctypes.c_int32)]
+    L.biot_mesh_structured.argtypes = [ctypes.c_int32, ctypes.c_int32, P(_d), P(_i32), _i64, _i64]
+    L.biot_bc_column.argtypes = [P(BiotMesh), ctypes.c_double, _u8, _d, _i64, _i32]
+    L.biot_free.argtypes = [ctypes.c_void_p]
+    L.biot_free.restype = None
     L.biot_get_info.argtypes = [ctx_p, P(BiotInfo)]
     L.biot_last_timing.argtypes = [ctx_p, _d]
     L.biot_nccl_unique_id.argtypes = [ctypes.c_void_p]

@@ -744,6 +744,135 @@ extern "C" {
 
 int32_t biot_abi_version(void) { return BIOT_PIT_ABI_VERSION; }
 
+void biot_free(void *p) { std::free(p); }
+
+biot_status biot_mesh_structured(int32_t dim, int32_t n, double **coords, int32_t **cells, int64_t *n_nodes,
+                                 int64_t *n_cells) {
+    if (!coords || !cells || !n_nodes || !n_cells) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    if ((dim != 2 && dim != 3) || n < 1 || (dim == 3 ? (int64_t)n * n * n > 100000000LL : (int64_t)n * n > 1000000000LL))
+        return fail(nullptr, BIOT_E_INVALID, "need dim in {2, 3} and a positive n of a supported size");
+    const int64_t w = (int64_t)n + 1;
+    const int64_t nn = dim == 2 ? w * w : w * w * w;
+    const int64_t nc = dim == 2 ? 2LL * n * n : 6LL * n * n * n;
+    double *X = static_cast<double *>(std::malloc((size_t)nn * dim * sizeof(double)));
+    int32_t *C = static_cast<int32_t *>(std::malloc((size_t)nc * (dim + 1) * sizeof(int32_t)));
+    if (!X || !C) {
+        std::free(X);
+        std::free(C);
+        return fail(nullptr, BIOT_E_NOMEM, "host allocation failed");
+    }
+    if (dim == 2) {
+        for (int64_t j = 0; j < w; ++j)
+            for (int64_t i = 0; i < w; ++i) {
+                X[(j * w + i) * 2 + 0] = (double)i / n;
+                X[(j * w + i) * 2 + 1] = (double)j / n;
+            }
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) {
+                const int32_t n00 = (int32_t)(j * w + i), n10 = n00 + 1, n11 = (int32_t)(n00 + w + 1),
+                              n01 = (int32_t)(n00 + w);
+                int32_t *c = C + ((j * n + i) * 2) * 3;
+                c[0] = n00; c[1] = n10; c[2] = n11;   // counter-clockwise
+                c[3] = n00; c[4] = n11; c[5] = n01;
+            }
+    } else {
+        for (int64_t k = 0; k < w; ++k)
+            for (int64_t j = 0; j < w; ++j)
+                for (int64_t i = 0; i < w; ++i) {
+                    double *x = X + ((k * w + j) * w + i) * 3;
+                    x[0] = (double)i / n;
+                    x[1] = (double)j / n;
+                    x[2] = (double)k / n;
+                }
+        const int perms[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+        const int64_t stride[3] = {1, w, w * w};
+        int64_t off[6][4];
+        for (int p = 0; p < 6; ++p) {
+            // vertices v, v+e_a, v+e_a+e_b, v+e_a+e_b+e_c; orientation from det[e_a; e_a+e_b; e_a+e_b+e_c]
+            int e[3][3] = {{0}};
+            e[0][perms[p][0]] = 1;
+            for (int q = 0; q < 3; ++q) e[1][q] = e[0][q];
+            e[1][perms[p][1]] = 1;
+            for (int q = 0; q < 3; ++q) e[2][q] = 1;
+            const int det = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                            e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                            e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+            off[p][0] = 0;
+            for (int v = 0; v < 3; ++v) off[p][v + 1] = e[v][0] * stride[0] + e[v][1] * stride[1] + e[v][2] * stride[2];
+            if (det < 0) std::swap(off[p][2], off[p][3]);
+        }
+        for (int64_t k = 0; k < n; ++k)
+            for (int64_t j = 0; j < n; ++j)
+                for (int64_t i = 0; i < n; ++i) {
+                    const int64_t v = (k * w + j) * w + i, cube = (k * n + j) * n + i;
+                    for (int p = 0; p < 6; ++p)
+                        for (int q = 0; q < 4; ++q) C[(cube * 6 + p) * 4 + q] = (int32_t)(v + off[p][q]);
+                }
+    }
+    *coords = X;
+    *cells = C;
+    *n_nodes = nn;
+    *n_cells = nc;
+    return BIOT_OK;
+}
+
+biot_status biot_bc_column(const biot_mesh *mesh, double load, uint8_t *dirichlet, double *F, int64_t *n_facets,
+                           int32_t *facets) {
+    if (!mesh || !n_facets || !mesh->coords || !mesh->cells) return fail(nullptr, BIOT_E_INVALID, "NULL argument");
+    const int d = mesh->dim, nc = d + 1;
+    if (d != 2 && d != 3) return fail(nullptr, BIOT_E_INVALID, "mesh.dim must be 2 or 3");
+    if (!std::isfinite(load)) return fail(nullptr, BIOT_E_INVALID, "load must be finite");
+    const double eps = 1e-12;
+    const int64_t N = mesh->n_nodes;
+    auto on_top = [&](int64_t v) { return mesh->coords[v * d + (d - 1)] > 1.0 - eps; };
+    if (dirichlet) {
+        for (int64_t v = 0; v < N; ++v) {
+            const double *x = mesh->coords + v * d;
+            uint8_t *m = dirichlet + v * nc;
+            for (int c = 0; c < nc; ++c) m[c] = 0;
+            for (int ax = 0; ax < d - 1; ++ax)
+                if (x[ax] < eps || x[ax] > 1.0 - eps) m[ax] = 1;   // rollers on the sides
+            if (x[d - 1] < eps)
+                for (int c = 0; c < d; ++c) m[c] = 1;               // fixed bottom
+            if (x[d - 1] > 1.0 - eps) m[d] = 1;                     // drained top
+        }
+    }
+    if (F)
+        for (int64_t q = 0; q < N * nc; ++q) F[q] = 0.0;
+    int64_t nf = 0;
+    for (int64_t e = 0; e < mesh->n_cells; ++e) {
+        const int32_t *cv = mesh->cells + e * nc;
+        int32_t f[3];
+        int cnt = 0;
+        for (int a = 0; a < nc; ++a) {
+            if (cv[a] < 0 || cv[a] >= N) return fail(nullptr, BIOT_E_INVALID, "cell references a node out of range");
+            if (on_top(cv[a]) && cnt < 3) f[cnt++] = cv[a];
+            else if (on_top(cv[a])) ++cnt;
+        }
+        if (cnt != d) continue;   // a facet on the top face: exactly d of the cell's vertices on it
+        if (facets)
+            for (int a = 0; a < d; ++a) facets[nf * d + a] = f[a];
+        if (F) {
+            const double *P0 = mesh->coords + (int64_t)f[0] * d, *P1 = mesh->coords + (int64_t)f[1] * d;
+            double meas;
+            if (d == 2) {
+                meas = std::hypot(P1[0] - P0[0], P1[1] - P0[1]);
+            } else {
+                const double *P2 = mesh->coords + (int64_t)f[2] * d;
+                const double u[3] = {P1[0] - P0[0], P1[1] - P0[1], P1[2] - P0[2]};
+                const double v[3] = {P2[0] - P0[0], P2[1] - P0[1], P2[2] - P0[2]};
+                const double cx = u[1] * v[2] - u[2] * v[1], cy = u[2] * v[0] - u[0] * v[2],
+                             cz = u[0] * v[1] - u[1] * v[0];
+                meas = 0.5 * std::sqrt(cx * cx + cy * cy + cz * cz);
+            }
+            for (int a = 0; a < d; ++a) F[(int64_t)f[a] * nc + (d - 1)] += -load * meas / d;
+        }
+        ++nf;
+    }
+    *n_facets = nf;
+    return BIOT_OK;
+}
+
 const char *biot_status_string(biot_status s) {
     switch (s) {
         case BIOT_OK: return "ok";

@@ -38,6 +38,41 @@ def assemble_host(prob, dt, beta=None):
     return (Ai, Aj, Av), (Pi, Pj, Pv), f, dinv
 
 
+def mesh_structured(dim, n):
+    """biot_mesh_structured: (coords [N, dim], cells [nc, dim+1]) of the library's
+    structured unit square / Kuhn cube (copied out, library buffers released)."""
+    L = _lib.load()
+    X = ctypes.POINTER(ctypes.c_double)()
+    C = ctypes.POINTER(ctypes.c_int32)()
+    nn, nc = ctypes.c_int64(), ctypes.c_int64()
+    check(L.biot_mesh_structured(dim, n, ctypes.byref(X), ctypes.byref(C), ctypes.byref(nn), ctypes.byref(nc)))
+    try:
+        coords = np.ctypeslib.as_array(X, shape=(nn.value, dim)).copy()
+        cells = np.ctypeslib.as_array(C, shape=(nc.value, dim + 1)).copy()
+    finally:
+        L.biot_free(ctypes.cast(X, ctypes.c_void_p))
+        L.biot_free(ctypes.cast(C, ctypes.c_void_p))
+    return coords, cells
+
+
+def bc_column(coords, cells, load=1.0):
+    """biot_bc_column: (dirichlet mask, load vector F, top facets) of the column problem."""
+    from ._lib import BiotMesh
+    L = _lib.load()
+    coords = np.ascontiguousarray(coords, dtype=np.float64)
+    cells = np.ascontiguousarray(cells, dtype=np.int32)
+    dim = coords.shape[1]
+    mesh = BiotMesh(dim, coords.shape[0], ptr(coords), cells.shape[0], ptr(cells, ctypes.POINTER(ctypes.c_int32)))
+    nf = ctypes.c_int64()
+    check(L.biot_bc_column(ctypes.byref(mesh), load, None, None, ctypes.byref(nf), None))
+    mask = np.zeros(coords.shape[0] * (dim + 1), np.uint8)
+    F = np.zeros(coords.shape[0] * (dim + 1))
+    facets = np.zeros((nf.value, dim), np.int32)
+    check(L.biot_bc_column(ctypes.byref(mesh), load, ptr(mask, ctypes.POINTER(ctypes.c_uint8)), ptr(F),
+                           ctypes.byref(nf), ptr(facets, ctypes.POINTER(ctypes.c_int32))))
+    return mask, F, facets
+
+
 def assemble_loads_host(prob, dt, beta=None):
     """biot_assemble_loads_host: the library's further load terms (R24), node-interleaved
     [n_terms, n_dof], with their kinds (0 source, 1 lifting at c_n, 2 at c_{n-1}) and

@@ -193,3 +193,36 @@ def test_host_load_terms_match_oracle(which):
         ref = S.from_paper(want[key])
         scale = np.abs(ref).max()
         assert np.abs(F[j] - ref).max() <= 1e-13 * scale, (key, np.abs(F[j] - ref).max(), scale)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 1), (2, 5), (3, 1), (3, 3)])
+def test_structured_mesh_helper_matches_workloads(dim, n):
+    """biot_mesh_structured reproduces the workload meshes (node numbering, cell vertex
+    order, orientation) exactly; SURVEY §8(b) helpers."""
+    from paper_2310_10430_b200.solver import mesh_structured
+    from workloads import mesh
+    X, C = mesh_structured(dim, n)
+    Xw, Cw = mesh(dim, n)
+    assert np.array_equal(X, Xw)
+    assert np.array_equal(C, Cw)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 4), (3, 2)])
+def test_bc_column_helper(dim, n):
+    """biot_bc_column: the column Dirichlet mask and top facets of the workloads, and the
+    traction load equal to the oracle's (total = -load * |top| = -load)."""
+    from paper_2310_10430_b200.solver import mesh_structured, bc_column
+    from workloads import column_dirichlet, top_facets
+    X, C = mesh_structured(dim, n)
+    mask, F, facets = bc_column(X, C, load=2.5)
+    assert np.array_equal(mask, column_dirichlet(X))
+    tf = top_facets(X, C)
+    assert sorted(map(tuple, np.sort(facets, axis=1))) == sorted(map(tuple, np.sort(tf, axis=1)))
+    tr = np.zeros(dim)
+    tr[dim - 1] = -2.5
+    Fu = oracle.traction_load(dim, X, tf, tr)                  # node-major U, d per node
+    nn = X.shape[0]
+    Fi = F.reshape(nn, dim + 1)
+    assert np.abs(Fi[:, :dim].ravel() - Fu).max() < 1e-15
+    assert np.all(Fi[:, dim] == 0.0)
+    assert abs(Fi[:, dim - 1].sum() + 2.5) < 1e-13
