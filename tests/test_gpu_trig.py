@@ -184,3 +184,31 @@ def test_trig_time_slabs_bitwise(precond):
         ref.close()
         for g in ranks:
             g.close()
+
+
+@pytest.mark.parametrize("precond,omega", [(2, 0.5), (1, 0.3)])
+def test_trig_parity_bench_size_windows(precond, omega):
+    """The benchmark's §4.1 configuration (h = 1/512, N_t = 1024, the launch configuration
+    bench.py --workload trig times): x^K on sampled step windows against the oracle run on a
+    window that starts K steps earlier (light cone: x_n^K depends on x^0 of steps n-K..n
+    only), with the load coefficients of the global steps."""
+    nt, K = 1024, 4
+    prob = trig_problem(9, nt, 1.0 / 1024)
+    x0 = _x0(prob, nt)
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega)
+    try:
+        g.set_iterate(1, x0)
+        g.iterate(K)
+        S = oracle.OracleSystem(prob)
+        for n_lo, n_hi in [(1, 3), (517, 520), (1021, 1024)]:
+            a = max(1, n_lo - K)
+            L = n_hi - a + 1
+            X = np.zeros((L + 1, S.ndof))
+            X[0] = S.to_paper(x0[a - 2]) if a > 1 else S.to_paper(prob.x_initial) * S.free
+            X[1:] = S.to_paper(x0[a - 1:n_hi])
+            Xo, _ = S.iterate(X, S.coefs(np.zeros(L), a, L), K, precond, omega, history=False)
+            xo = np.stack([S.from_paper(v) for v in Xo[1 + n_lo - a:]])
+            xg = g.solution(n_lo, n_hi - n_lo + 1)
+            assert field_errors(xg, xo, 2).max() < TOL, (n_lo, field_errors(xg, xo, 2))
+    finally:
+        g.close()
