@@ -234,7 +234,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     // half takes lane 31's first-half step 63, lane 0 of the first half the carry
     double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
     double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
-    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
+    if (lane == 0) qp0 = *carry;   // chunk 0: prefilled from the ghost column (see the chunk loop)
     __syncwarp();
     if (lane == 31) *carry = q[3];
     double Dv[3], xs[3][kT2];
@@ -530,6 +530,23 @@ __global__ void __launch_bounds__(kThreads2, 1)
             int kindP = 0;                       // pending node (row m-1): 0 none, 1 interior, 2 class
             const double *const cls_base = NL == 1 ? static_cast<const double *>(cls_sm) : a.cls;
             const double *T = cls_base;
+            if constexpr (MODE != MODE_PASS2 && MODE != MODE_MATVEC) {
+                if (ghost && valid && a.dry != 1) {
+                    // q(t0-1) of chunk 0 from the ghost column, for every row of the tile at
+                    // once (one row per lane, each in the march's FMA order), into the q
+                    // carry that later chunks use: its global loads overlap instead of
+                    // stalling lane 0 at every node (Gauss-Seidel windows are all chunk 0)
+                    for (int mm = ja + lane; mm < jb; mm += 32) {
+                        const int64_t i = (int64_t)mm * g.W + col;
+                        const bool intr = __ldg(a.aux + i * kAuxRec + 13) == 1.0;
+                        qcarry[(mm - ja) * kSeg + warp] =
+                            intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
+                                 : ghost_q<true, S0, Tile2dArgs>(
+                                       a, i, cls_base + (ccx + 3 * axis_class(mm, g.nrows)) * 7 * kCW);
+                    }
+                    __syncwarp();
+                }
+            }
             int sd = it % kStages;               // stage of row m-1
             uint32_t phd = (it / kStages) & 1;
             mbar_wait_suspend(&full[sd], phd);
