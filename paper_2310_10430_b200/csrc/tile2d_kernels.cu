@@ -234,7 +234,9 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     // half takes lane 31's first-half step 63, lane 0 of the first half the carry
     double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
     double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
-    if (lane == 0) qp0 = *carry;   // chunk 0: prefilled from the ghost column (see the chunk loop)
+    // ghost: q(t0-1) from the ghost column now (single-chunk windows); otherwise from the
+    // carry, which the chunk loop prefilled from the ghost column for chunk 0
+    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
     double Dv[3], xs[3][kT2];
@@ -531,11 +533,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const double *const cls_base = NL == 1 ? static_cast<const double *>(cls_sm) : a.cls;
             const double *T = cls_base;
             if constexpr (MODE != MODE_PASS2 && MODE != MODE_MATVEC) {
-                if (ghost && valid && a.dry != 1) {
+                if (ghost && g.nchunks > 1 && valid && a.dry != 1) {
                     // q(t0-1) of chunk 0 from the ghost column, for every row of the tile at
                     // once (one row per lane, each in the march's FMA order), into the q
                     // carry that later chunks use: its global loads overlap instead of
-                    // stalling lane 0 at every node (Gauss-Seidel windows are all chunk 0)
+                    // stalling lane 0 at every node.  Single-chunk passes (the Gauss-Seidel
+                    // windows) keep the per-node path: there the prefill would stall every
+                    // tile start while the ring is full
                     for (int mm = ja + lane; mm < jb; mm += 32) {
                         const int64_t i = (int64_t)mm * g.W + col;
                         const bool intr = __ldg(a.aux + i * kAuxRec + 13) == 1.0;
@@ -570,10 +574,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                             else finish_mv<true, S0, Tile2dArgs>(a, pm, p, lane, aux, T, i, t0, whole, acc, q);
                         } else {
                             if (kindP == 1)
-                                finish<false, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                finish<false, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && g.nchunks == 1, whole,
                                                                     carry, sv, acc, q, nu, npn);
                             else
-                                finish<true, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost, whole,
+                                finish<true, S0, MODE, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && g.nchunks == 1, whole,
                                                                    carry, sv, acc, q, nu, npn);
                         }
                     }
