@@ -181,13 +181,14 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
  * the cycle's start.  Collective for world > 1 (one slice per outer iteration). */
 biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k);
 
-/* K outer iterations as biot_iterate with P~2 whose inner inverses A^{-1} and S~p^{-1}
- * (PAPER.md eq. p2) are m steps of Chebyshev iteration preconditioned by the
- * diagonal, on [lambda_max / alpha, lambda_max] of D^{-1} M with lambda_max the Gershgorin
- * bound of each block (reading R22; m = 1 is the diagonal inverse divided by theta).
- * 1 <= m <= 64, alpha > 1 (30 in R22); needs precond = 2 (BIOT_E_STATE otherwise); any
- * mesh; allocates up to 4 extra space-time panels on first use.  The residual history
- * records r(x^k) as biot_iterate does.  Collective for world > 1. */
+/* K outer iterations as biot_iterate with the context's P~ (P~2, eq. p2, or P~1, eq. p1;
+ * P:L238-262) whose inner inverses A^{-1} and S~p^{-1} are m steps of Chebyshev
+ * iteration preconditioned by the diagonal, on [lambda_max / alpha, lambda_max] of
+ * D^{-1} M with lambda_max the Gershgorin bound of each block (reading R22; m = 1 is the
+ * diagonal inverse divided by theta).  P~1 runs the displacement block first, then the
+ * pressure block on B^T z_u - r_p.  1 <= m <= 64, alpha > 1 (30 in R22); any mesh;
+ * allocates up to 4 extra space-time panels on first use.  The residual history records
+ * r(x^k) as biot_iterate does.  Collective for world > 1. */
 biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha);
 
 /* PAPER.md Algorithm 3 literally: Gauss-Seidel in time (b^{n,m} = A' X^{n-1,m} + f^n)

@@ -1737,11 +1737,11 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (K < 0 || m < 1 || m > 64 || !(alpha > 1.0) || !std::isfinite(alpha))
         return fail(ctx, BIOT_E_INVALID, "need K >= 0, 1 <= m <= 64 and alpha > 1");
-    if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "Chebyshev inner inverses are built for P~2 (precond = 2)");
     if (K == 0) return BIOT_OK;
+    const bool p1 = ctx->precond == 1;
     CU(cudaSetDevice(ctx->device));
     const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
-    const int need = m == 1 ? 2 : m == 2 ? 3 : 4;   // s, d0 [, d1 [, y]]
+    const int need = m == 1 ? 2 : (m == 2 && !p1) ? 3 : 4;   // s, d0 [, d1 [, y]]
     for (int q = 0; q < need; ++q)
         if (!ctx->cb_base[q]) {
             ALLOC(ctx->cb_base[q], panel_bytes);
@@ -1767,6 +1767,8 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
     c.omega = ctx->omega;
     c.inv_theta_u = th_u > 0.0 ? 1.0 / th_u : 0.0;
     c.inv_theta_p = th_p > 0.0 ? 1.0 / th_p : 0.0;
+    c.rows = p1 ? 1 : 3;
+    c.p_sign = p1 ? 1.0 : -1.0;
     CU(cudaEventRecord(ctx->ev_a, ctx->stream));
     double *const zsave = ctx->z;
     for (int32_t it = 0; it < K; ++it) {
@@ -1787,24 +1789,45 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
         c.x = xin;
         c.xn = xout;
         c.sendbuf = ctx->world > 1 ? ctx->sendbuf : nullptr;
-        c.last = m == 1;
-        c.dn = ctx->cb[1];
-        CU(biot::launch_cheb_init(c, ctx->stream));
-        double rho_u = de_u / th_u, rho_p = de_p / th_p;   // rho_0 = 1 / sigma
-        for (int k = 1; k < m; ++k) {
-            const double ru = 1.0 / (2.0 * th_u / de_u - rho_u), rp = 1.0 / (2.0 * th_p / de_p - rho_p);
-            c.c1_u = ru * rho_u;
-            c.c2_u = 2.0 * ru / de_u;
-            c.c1_p = rp * rho_p;
-            c.c2_p = 2.0 * rp / de_p;
-            rho_u = ru;
-            rho_p = rp;
-            c.d = ctx->cb[1 + (k - 1) % 2];
-            c.dn = ctx->cb[1 + k % 2];
-            c.y = k == 1 ? nullptr : ctx->cb[3];
-            c.yn = ctx->cb[3];
-            c.last = k == m - 1;
-            CU(biot::launch_cheb_step(ctx->d, ctx->path, ctx->S, c, ctx->stream));
+        // P~2: both blocks at once.  P~1 (eq. p1): the displacement block first (it cannot
+        // write x yet), then r~_p = B^T z_u - r_p and the pressure block on it.
+        auto run_block = [&](int rows, bool final_block) -> cudaError_t {
+            c.rows = rows;
+            c.last = final_block && m == 1;
+            c.dn = ctx->cb[1];
+            cudaError_t e2 = cudaSuccess;
+            if (rows != 2) e2 = biot::launch_cheb_init(c, ctx->stream);
+            if (e2 != cudaSuccess) return e2;
+            if (rows == 2) {        // P~1 pressure start from z_u
+                c.zu = m == 1 ? ctx->cb[1] : ctx->cb[3];
+                c.last = m == 1;
+                e2 = biot::launch_cheb_p1_rhs(ctx->d, ctx->path, ctx->S, c, ctx->stream);
+                if (e2 != cudaSuccess) return e2;
+            }
+            double rho_u = de_u / th_u, rho_p = de_p / th_p;   // rho_0 = 1 / sigma
+            for (int k = 1; k < m; ++k) {
+                const double ru = 1.0 / (2.0 * th_u / de_u - rho_u), rp = 1.0 / (2.0 * th_p / de_p - rho_p);
+                c.c1_u = ru * rho_u;
+                c.c2_u = 2.0 * ru / de_u;
+                c.c1_p = rp * rho_p;
+                c.c2_p = 2.0 * rp / de_p;
+                rho_u = ru;
+                rho_p = rp;
+                c.d = ctx->cb[1 + (k - 1) % 2];
+                c.dn = ctx->cb[1 + k % 2];
+                c.y = k == 1 ? nullptr : ctx->cb[3];
+                c.yn = ctx->cb[3];
+                c.last = final_block && k == m - 1;
+                e2 = biot::launch_cheb_step(ctx->d, ctx->path, ctx->S, c, ctx->stream);
+                if (e2 != cudaSuccess) return e2;
+            }
+            return cudaSuccess;
+        };
+        if (p1) {
+            CU(run_block(1, false));
+            CU(run_block(2, true));
+        } else {
+            CU(run_block(3, true));
         }
         ctx->cur = 1 - ctx->cur;
         ctx->iterations++;

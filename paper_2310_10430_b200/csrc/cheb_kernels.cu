@@ -41,10 +41,11 @@ __global__ void __launch_bounds__(kCThreads) cheb_init_kernel(const ChebArgs a) 
         const int c = (int)(row % nc);
         const int64_t o = row * a.pitch + t;
         const bool p = c == d;
+        if (!(a.rows & (p ? 2 : 1))) continue;
         const double sv = p ? __ldg(a.dinv + row) * a.s[o] : a.s[o];
         const double dv = sv * (p ? a.inv_theta_p : a.inv_theta_u);
         if (a.last) {
-            const double xv = a.x[o] + a.omega * (p ? -dv : dv);
+            const double xv = a.x[o] + a.omega * (p ? a.p_sign * dv : dv);
             a.xn[o] = xv;
             if (a.sendbuf && t == a.n_tl - 1) a.sendbuf[row] = xv;
         } else {
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
         for (int c = 0; c < NC; ++c) {
             const int64_t o = (i * NC + c) * P + t0;
             const bool p = c == D;
+            if (!(a.rows & (p ? 2 : 1))) continue;
             const double dv = __ldg(a.dinv + i * NC + c);
             const double c1 = p ? a.c1_p : a.c1_u, c2 = p ? a.c2_p : a.c2_u;
 #pragma unroll
@@ -114,7 +116,7 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
                 const double dn = fma(c1, a.d[o + tt], c2 * sn);
                 const double yn = (a.y ? a.y[o + tt] : a.d[o + tt]) + dn;   // y_1 = d_0
                 if (a.last) {
-                    const double xv = fma(a.omega, p ? -yn : yn, a.x[o + tt]);
+                    const double xv = fma(a.omega, p ? a.p_sign * yn : yn, a.x[o + tt]);
                     a.xn[o + tt] = xv;
                     if (a.sendbuf && t0 + tt == a.n_tl - 1) a.sendbuf[i * NC + c] = xv;
                 } else {
@@ -127,11 +129,74 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
     }
 }
 
+// P~1 between the blocks (PAPER.md eq. p1: z_p = S~p^{-1} (B^T z_u - r_p)): the right-hand
+// side of the pressure block from z_u (all neighbours), its Chebyshev start, and the
+// displacement update x_u + omega z_u of the node.
+template <int D, int S, bool ELL>
+__global__ void __launch_bounds__(kCThreads) cheb_p1_rhs_kernel(const ChebArgs a) {
+    constexpr int NC = D + 1;
+    constexpr int W = (NC * NC + 2) / 2 * 2;
+    const int lane = threadIdx.x & 31;
+    const int n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    const int64_t P = a.pitch;
+    const int64_t n_warps = a.n_nodes * n_chunks;
+    for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_warps;
+         w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t i = w / n_chunks;
+        const int t0 = (int)(w % n_chunks) * kChunk + lane * kT;
+        if (t0 >= a.n_tl) continue;
+        const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
+        double bt[kT] = {0.0, 0.0, 0.0, 0.0};
+        for (int s = 0; s < S; ++s) {
+            const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
+#pragma unroll
+            for (int cc = 0; cc < D; ++cc) {
+                const double cf = __ldg(bp + s * W + D * NC + cc);
+                const double *src = a.zu + (j * NC + cc) * P + t0;
+                const double2 v01 = __ldg(reinterpret_cast<const double2 *>(src));
+                const double2 v23 = __ldg(reinterpret_cast<const double2 *>(src + 2));
+                bt[0] = fma(cf, v01.x, bt[0]);
+                bt[1] = fma(cf, v01.y, bt[1]);
+                bt[2] = fma(cf, v23.x, bt[2]);
+                bt[3] = fma(cf, v23.y, bt[3]);
+            }
+        }
+        const double dvp = __ldg(a.dinv + i * NC + D);
+        const int64_t op = (i * NC + D) * P + t0;
+#pragma unroll
+        for (int tt = 0; tt < kT; ++tt) {
+            if (t0 + tt >= a.n_tl) break;
+            const double sp = dvp * (bt[tt] - a.s[op + tt]);   // s holds r_p here
+            const double dp = sp * a.inv_theta_p;
+            if (a.last) {
+                const double xv = fma(a.omega, dp, a.x[op + tt]);
+                a.xn[op + tt] = xv;
+                if (a.sendbuf && t0 + tt == a.n_tl - 1) a.sendbuf[i * NC + D] = xv;
+            } else {
+                a.s[op + tt] = sp;
+                a.dn[op + tt] = dp;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const int64_t o = (i * NC + c) * P + t0;
+#pragma unroll
+            for (int tt = 0; tt < kT; ++tt) {
+                if (t0 + tt >= a.n_tl) break;
+                const double xv = fma(a.omega, a.zu[o + tt], a.x[o + tt]);
+                a.xn[o + tt] = xv;
+                if (a.sendbuf && t0 + tt == a.n_tl - 1) a.sendbuf[i * NC + c] = xv;
+            }
+        }
+    }
+}
+
 using StepFn = void (*)(const ChebArgs);
 
-StepFn pick_step(int dim, int path, int S) {
+StepFn pick_step(int dim, int path, int S, bool rhs = false) {
 #define BIOT_CS(D_, S_, ELL_) \
-    if (dim == D_ && S == S_ && (path == 2) == ELL_) return cheb_step_kernel<D_, S_, ELL_>;
+    if (dim == D_ && S == S_ && (path == 2) == ELL_) \
+        return rhs ? cheb_p1_rhs_kernel<D_, S_, ELL_> : cheb_step_kernel<D_, S_, ELL_>;
     BIOT_CS(2, 7, false)
     BIOT_CS(3, 15, false)
     BIOT_CS(2, 8, true)
@@ -158,6 +223,14 @@ cudaError_t launch_cheb_init(const ChebArgs &a, cudaStream_t st) {
 
 cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st) {
     StepFn f = pick_step(dim, path, n_slots);
+    if (!f) return cudaErrorInvalidValue;
+    const int64_t n_chunks = (a.n_tl + kChunk - 1) / kChunk;
+    f<<<grid_for(a.n_nodes * n_chunks * 32, kCThreads), kCThreads, 0, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cheb_p1_rhs(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st) {
+    StepFn f = pick_step(dim, path, n_slots, true);
     if (!f) return cudaErrorInvalidValue;
     const int64_t n_chunks = (a.n_tl + kChunk - 1) / kChunk;
     f<<<grid_for(a.n_nodes * n_chunks * 32, kCThreads), kCThreads, 0, st>>>(a);

@@ -185,9 +185,15 @@ struct ChebArgs {
     double inv_theta_u, inv_theta_p;        // 1 / theta per block (the start)
     double omega;
     int32_t last;           // 1: write x^{k+1} instead of s, d, y
+    int32_t rows;           // rows updated: 1 displacement, 2 pressure, 3 both (P~1 runs the blocks in turn)
+    double p_sign;          // z_p = p_sign y_p: -1 for P~2 (S~p y = r_p, z_p = -y), +1 for P~1
+    const double *zu;       // P~1 pressure start: the panel holding z_u
 };
 cudaError_t launch_cheb_init(const ChebArgs &a, cudaStream_t st);
 cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st);
+// P~1: r~_p = B^T z_u - r_p, s_p = D_S^{-1} r~_p, d_p = s_p / theta_p (or, m = 1, the
+// update), and x_u^{k+1} = x_u + omega z_u
+cudaError_t launch_cheb_p1_rhs(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st);
 
 bool stencil_supported(int dim, int R, int T);
 cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);

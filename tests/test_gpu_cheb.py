@@ -16,16 +16,16 @@ from _parity import TOL, field_errors, norm_errors
 pytestmark = pytest.mark.gpu
 
 
-def _pair(prob, nt, K, m, omega=0.5, alpha=30.0, trig=False):
+def _pair(prob, nt, K, m, omega=0.5, alpha=30.0, trig=False, precond=2):
     x0 = initial_iterate(prob.dirichlet, np.arange(1, nt + 1), 17)
     S = oracle.OracleSystem(prob)
     if trig:
         s_or = S.coefs(np.zeros(nt), 1, nt)
-        g = BiotSolver(prob, n_t=nt, precond=2, omega=omega)
+        g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega)
     else:
         s = load_scales(nt, parity=True)
         s_or = s
-        g = BiotSolver(prob, n_t=nt, precond=2, omega=omega, load_scale=s)
+        g = BiotSolver(prob, n_t=nt, precond=precond, omega=omega, load_scale=s)
     try:
         g.set_iterate(1, x0)
         g.iterate_cheb(K, m, alpha)
@@ -38,7 +38,7 @@ def _pair(prob, nt, K, m, omega=0.5, alpha=30.0, trig=False):
     if trig:
         X[0] = S.to_paper(prob.x_initial) * S.free
     X[1:] = S.to_paper(x0)
-    Xo, ho = ocheb.iterate(S, X, s_or, K, m, precond=2, omega=omega, alpha=alpha)
+    Xo, ho = ocheb.iterate(S, X, s_or, K, m, precond=precond, omega=omega, alpha=alpha)
     return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho), path
 
 
@@ -82,3 +82,20 @@ def test_cheb_m1_is_scaled_diagonal():
     prob = config_problem(1)
     (xg, hg), (xo, ho), _ = _pair(prob, 8, 1, 1)
     assert field_errors(xg, xo, 2).max() < TOL
+
+
+@pytest.mark.parametrize("m", [1, 2, 3])
+def test_cheb_parity_p1(m):
+    """P~1 (eq. p1) with Chebyshev inner inverses: displacement block, then the pressure
+    block on B^T z_u - r_p (config 1 tile path and a 3D mesh)."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho), _ = _pair(prob, 32, 8, m, omega=0.3, precond=1)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_cheb_parity_p1_3d():
+    prob = make_problem(3, 6, 16, 1.0 / 16, 1, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0, kappa_seed=2)
+    (xg, hg), (xo, ho), _ = _pair(prob, 16, 4, 2, omega=0.3, precond=1)
+    assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
