@@ -352,8 +352,16 @@ def main():
             # panel passes per outer iteration: residual 2, start 2 + 1/nc
             # (m = 1: 3 with the update), step k: 5 (+1 from k = 2 on), the last one 4 (+1)
             mm, nc = args.cheb_m, prob.dim + 1
-            passes = 5.0 if mm == 1 else 2 + 2 + 1.0 / nc + sum(
-                (4 if k == mm - 1 else 5) + (1 if k >= 2 else 0) for k in range(1, mm))
+            if args.precond == 2:
+                passes = 5.0 if mm == 1 else 2 + 2 + 1.0 / nc + sum(
+                    (4 if k == mm - 1 else 5) + (1 if k >= 2 else 0) for k in range(1, mm))
+            else:   # P~1: displacement block, B^T z_u - r_p, pressure block (fractions fu, fp)
+                fu, fp = (nc - 1) / nc, 1.0 / nc
+                steps = lambda f, last_x: sum(((3 if k == mm - 1 and last_x else 5) + (1 if k >= 2 else 0)) * f
+                                               + (2 * f if k == mm - 1 and last_x else 0) for k in range(1, mm))
+                passes = (2 + 2 * fu + steps(fu, False)              # residual, u start, u steps
+                          + fu + fp + 2 * fu + (2 * fp if mm == 1 else 2 * fp)   # r~_p, x_u update, p start
+                          + steps(fp, True))
             algo_bytes = passes * 8.0 * prob.n_dof * info.n_t_local
         achieved_gbs = algo_bytes / (sweep_ms / 1e3) / 1e9
         sm_max = (pk or {}).get("sm_max_mhz", 1965.0)
