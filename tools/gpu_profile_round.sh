@@ -12,7 +12,7 @@ timeout 300 python bench.py --config 2 --steps 100 --no-cpu-baseline > gpurun_ou
 timeout 300 python bench.py --config 1 --steps 100 --no-cpu-baseline > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err
 timeout 600 python bench.py --config 5 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 timeout 900 python bench.py --method gmres --gmres-k 10 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c3_gmres.json 2> gpurun_out/bench_c3_gmres.err
-timeout 900 python bench.py --method gs_gmres --gmres-k 10 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c3_gs_gmres.json 2> gpurun_out/bench_c3_gs_gmres.err
+timeout 1200 python bench.py --method gs_gmres --gmres-k 10 --steps 16 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c3_gs_gmres.json 2> gpurun_out/bench_c3_gs_gmres.err
 timeout 600 python bench.py --method cheb --cheb-m 2 --steps 20 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench_c3_cheb2.json 2> gpurun_out/bench_c3_cheb2.err
 timeout 900 python bench.py --config 4 --method gmres --gmres-k 10 --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_c4_gmres.json 2> gpurun_out/bench_c4_gmres.err
 timeout 600 python bench.py --workload trig > gpurun_out/bench_trig.json 2> gpurun_out/bench_trig.err
