@@ -352,9 +352,9 @@ def main():
             # panel passes per outer iteration: residual 2, start 2 + 1/nc
             # (m = 1: 3 with the update), step k: 5 (+1 from k = 2 on), the last one 4 (+1)
             mm, nc = args.cheb_m, prob.dim + 1
-            if args.precond == 2:
-                passes = 5.0 if mm == 1 else 2 + 2 + 1.0 / nc + sum(
-                    (4 if k == mm - 1 else 5) + (1 if k >= 2 else 0) for k in range(1, mm))
+            if args.precond == 2:   # the start is fused into the first step (reads Z directly)
+                passes = 5.0 if mm == 1 else 2 + sum(
+                    (3 if k == mm - 1 else 4) + (2 if k >= 2 else 0) for k in range(1, mm))
             else:   # P~1: displacement block, B^T z_u - r_p, pressure block (fractions fu, fp)
                 fu, fp = (nc - 1) / nc, 1.0 / nc
                 steps = lambda f, last_x: sum(((3 if k == mm - 1 and last_x else 5) + (1 if k >= 2 else 0)) * f

@@ -1741,7 +1741,7 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
     const bool p1 = ctx->precond == 1;
     CU(cudaSetDevice(ctx->device));
     const size_t panel_bytes = (size_t)ctx->rows_alloc * ctx->pitch * sizeof(double);
-    const int need = m == 1 ? 2 : (m == 2 && !p1) ? 3 : 4;   // s, d0 [, d1 [, y]]
+    const int need = m == 1 ? 2 : 4;   // s (Z), d0 [, d1, y]
     for (int q = 0; q < need; ++q)
         if (!ctx->cb_base[q]) {
             ALLOC(ctx->cb_base[q], panel_bytes);
@@ -1795,7 +1795,37 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
             c.rows = rows;
             c.last = final_block && m == 1;
             c.dn = ctx->cb[1];
+            c.first = 0;
+            c.sn = nullptr;
             cudaError_t e2 = cudaSuccess;
+            if (rows == 3 && m >= 2) {
+                // P~2: the start is fused into the first step, which reads the Z panel (cb[0])
+                // and writes s to cb[1]; d alternates cb[2] (odd k) / cb[0] (even k)
+                double rho_u = de_u / th_u, rho_p = de_p / th_p;
+                for (int k = 1; k < m; ++k) {
+                    const double ru = 1.0 / (2.0 * th_u / de_u - rho_u), rp = 1.0 / (2.0 * th_p / de_p - rho_p);
+                    c.c1_u = ru * rho_u;
+                    c.c2_u = 2.0 * ru / de_u;
+                    c.c1_p = rp * rho_p;
+                    c.c2_p = 2.0 * rp / de_p;
+                    rho_u = ru;
+                    rho_p = rp;
+                    c.first = k == 1;
+                    c.s = k == 1 ? ctx->cb[0] : ctx->cb[1];
+                    c.sn = k == 1 ? ctx->cb[1] : nullptr;
+                    c.d = k == 1 ? nullptr : (k % 2 == 0 ? ctx->cb[2] : ctx->cb[0]);
+                    c.dn = k % 2 == 1 ? ctx->cb[2] : ctx->cb[0];
+                    c.y = k == 1 ? nullptr : ctx->cb[3];
+                    c.yn = ctx->cb[3];
+                    c.last = final_block && k == m - 1;
+                    e2 = biot::launch_cheb_step(ctx->d, ctx->path, ctx->S, c, ctx->stream);
+                    if (e2 != cudaSuccess) return e2;
+                }
+                c.first = 0;
+                c.sn = nullptr;
+                c.s = ctx->cb[0];
+                return cudaSuccess;
+            }
             if (rows != 2) e2 = biot::launch_cheb_init(c, ctx->stream);
             if (e2 != cudaSuccess) return e2;
             if (rows == 2) {        // P~1 pressure start from z_u

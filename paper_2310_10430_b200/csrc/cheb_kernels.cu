@@ -77,9 +77,11 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
         for (int c = 0; c < NC; ++c)
 #pragma unroll
             for (int tt = 0; tt < kT; ++tt) acc[c][tt] = 0.0;
+        const bool first = a.first != 0;
+        const double *__restrict__ dsrc = first ? a.s : a.d;
         for (int s = 0; s < S; ++s) {
             const int64_t j = column<S, ELL>(a.cols, a.off, i, s);
-            const double *__restrict__ dj = a.d + j * NC * P + t0;
+            const double *__restrict__ dj = dsrc + j * NC * P + t0;
             double v[NC][kT];
 #pragma unroll
             for (int cc = 0; cc < NC; ++cc) {
@@ -89,6 +91,15 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
                 v[cc][1] = v01.y;
                 v[cc][2] = v23.x;
                 v[cc][3] = v23.y;
+            }
+            if (first) {   // d_0 = s_0 / theta, s_0 = (Z_u, D_S^{-1} Z_p), as cheb_init_kernel
+                const double dsj = __ldg(a.dinv + j * NC + D);
+#pragma unroll
+                for (int tt = 0; tt < kT; ++tt) {
+#pragma unroll
+                    for (int cc = 0; cc < D; ++cc) v[cc][tt] = v[cc][tt] * a.inv_theta_u;
+                    v[D][tt] = (dsj * v[D][tt]) * a.inv_theta_p;
+                }
             }
 #pragma unroll
             for (int c = 0; c < D; ++c)
@@ -112,15 +123,23 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
 #pragma unroll
             for (int tt = 0; tt < kT; ++tt) {
                 if (t0 + tt >= a.n_tl) break;
-                const double sn = a.s[o + tt] - dv * acc[c][tt];
-                const double dn = fma(c1, a.d[o + tt], c2 * sn);
-                const double yn = (a.y ? a.y[o + tt] : a.d[o + tt]) + dn;   // y_1 = d_0
+                double so, dold;
+                if (first) {   // the start of this node, as cheb_init_kernel computes it
+                    so = p ? dv * a.s[o + tt] : a.s[o + tt];
+                    dold = so * (p ? a.inv_theta_p : a.inv_theta_u);
+                } else {
+                    so = a.s[o + tt];
+                    dold = a.d[o + tt];
+                }
+                const double sn = so - dv * acc[c][tt];
+                const double dn = fma(c1, dold, c2 * sn);
+                const double yn = (a.y ? a.y[o + tt] : dold) + dn;   // y_1 = d_0
                 if (a.last) {
                     const double xv = fma(a.omega, p ? a.p_sign * yn : yn, a.x[o + tt]);
                     a.xn[o + tt] = xv;
                     if (a.sendbuf && t0 + tt == a.n_tl - 1) a.sendbuf[i * NC + c] = xv;
                 } else {
-                    a.s[o + tt] = sn;
+                    (a.sn ? a.sn : a.s)[o + tt] = sn;
                     a.dn[o + tt] = dn;
                     a.yn[o + tt] = yn;
                 }

@@ -188,6 +188,9 @@ struct ChebArgs {
     int32_t rows;           // rows updated: 1 displacement, 2 pressure, 3 both (P~1 runs the blocks in turn)
     double p_sign;          // z_p = p_sign y_p: -1 for P~2 (S~p y = r_p, z_p = -y), +1 for P~1
     const double *zu;       // P~1 pressure start: the panel holding z_u
+    int32_t first;          // 1: d_0 = D^{-1} r / theta computed on the fly from the Z panel in s
+                            //    (no start pass); the new s goes to sn
+    double *sn;
 };
 cudaError_t launch_cheb_init(const ChebArgs &a, cudaStream_t st);
 cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st);
