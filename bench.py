@@ -359,7 +359,7 @@ def main():
                 fu, fp = (nc - 1) / nc, 1.0 / nc
                 steps = lambda f, last_x: sum(((3 if k == mm - 1 and last_x else 5) + (1 if k >= 2 else 0)) * f
                                                + (2 * f if k == mm - 1 and last_x else 0) for k in range(1, mm))
-                passes = (2 + 2 * fu + steps(fu, False)              # residual, u start, u steps
+                passes = (2 + (2 * fu if mm == 1 else -fu) + steps(fu, False)   # residual, u start (fused: d_0 not read)
                           + fu + fp + 2 * fu + (2 * fp if mm == 1 else 2 * fp)   # r~_p, x_u update, p start
                           + steps(fp, True))
             algo_bytes = passes * 8.0 * prob.n_dof * info.n_t_local

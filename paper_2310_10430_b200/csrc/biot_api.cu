@@ -1798,8 +1798,9 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
             c.first = 0;
             c.sn = nullptr;
             cudaError_t e2 = cudaSuccess;
-            if (rows == 3 && m >= 2) {
-                // P~2: the start is fused into the first step, which reads the Z panel (cb[0])
+            if (rows != 2 && m >= 2) {
+                // P~2 (and the P~1 displacement block): the start is fused into the first step,
+                // which reads the Z panel (cb[0])
                 // and writes s to cb[1]; d alternates cb[2] (odd k) / cb[0] (even k)
                 double rho_u = de_u / th_u, rho_p = de_p / th_p;
                 for (int k = 1; k < m; ++k) {
