@@ -155,6 +155,11 @@ struct biot_ctx {
     int64_t row_w = 0;
     int32_t n_rows = 0, rows_per_tile = 0;
     int64_t groups = 0;               // norm-partial groups of the active kernel
+    // fused single-pass P~1 (tile2d MODE_P1_FUSED): its own tile shape and partial groups
+    bool p1_fused = false;
+    int32_t rows_per_tile_p1 = 0;
+    int64_t groups_p1 = 0;
+    double *aux_base = nullptr;       // aux records with front padding (tile2d halo columns)
     // 4: TMA-pipelined 2D tile kernel
     double *aux = nullptr;
     double tmpl[7][10] = {{0}};
@@ -229,7 +234,7 @@ void free_all(biot_ctx *c) {
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->loadx, (void *)c->dinv, (void *)c->s,
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
-                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux,
+                    (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
                     (void *)c->gm_small})
         if (p) cudaFree(p);
@@ -531,6 +536,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         a.aux = c->aux;
         a.cls = c->cls;
         a.pad_nodes = c->pad;
+        if (mode == biot::MODE_P1_FUSED) a.rows_per_tile = c->rows_per_tile_p1;
         a.ghost_stride = 1;
         a.t_off = 0;
         a.t_lo = 0;
@@ -578,20 +584,29 @@ cudaError_t launch_pass2_any(biot_ctx *ctx, const double *xin, double *xout, dou
     return biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream);
 }
 
+// norm-partial groups written by a pass of `mode`
+int64_t groups_of(const biot_ctx *c, int mode) { return mode == biot::MODE_P1_FUSED ? c->groups_p1 : c->groups; }
+
+// the preconditioner pass of one outer iteration: P~2, fused P~1, or P~1's first pass
+int main_mode(const biot_ctx *c) {
+    return c->precond == 2 ? biot::MODE_UPDATE_P2 : c->p1_fused ? biot::MODE_P1_FUSED : biot::MODE_P1_PASS1;
+}
+
 biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     const bool timing = e0 != nullptr;
     biot_status st = halo_exchange(ctx);
     if (st != BIOT_OK) return st;
     const double *xin = ctx->x[ctx->cur];
     double *xout = ctx->x[1 - ctx->cur];
-    const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+    const int mode = main_mode(ctx);
     biot::SweepArgs a = sweep_args(ctx, mode, xin, xout);
+    // timed span: every pass of the preconditioner (P~1 two-pass: both)
     if (timing) CU(cudaEventRecord(e0, ctx->stream));
     CU(launch_main(ctx, mode, xin, xout));
+    if (mode == biot::MODE_P1_PASS1) CU(launch_pass2_any(ctx, xin, xout, a.sendbuf, nullptr));
     if (timing) CU(cudaEventRecord(e1, ctx->stream));
-    if (ctx->precond == 1) CU(launch_pass2_any(ctx, xin, xout, a.sendbuf, nullptr));
     double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
-    CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
+    CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, hslot, ctx->nonfinite,
                              ctx->fin_scratch, ctx->stream));
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
@@ -1134,6 +1149,13 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         }
     }
     if (ctx->n_load > 1 && ctx->kern != 1 && ctx->kern != 4) ctx->kern = 1;   // kMaxLoads kernels: generic, tile2d
+    if (ctx->kern == 4) {
+        // the fused P~1 tile reads x two grid rows above its first row (panel padding), and
+        // P~1 runs in one pass unless BIOT_P1_TWOPASS=1 (the two-pass form, kept for comparison)
+        ctx->pad = std::max<int64_t>(ctx->pad, 2 * ctx->row_w + 2);
+        const char *tp = std::getenv("BIOT_P1_TWOPASS");
+        ctx->p1_fused = ctx->precond == 1 && !(tp && std::atoi(tp) == 1);
+    }
     const int64_t chunk = ctx->kern == 2 ? 32 * ctx->sT
                         : ctx->kern == 3 ? 32 * ctx->mT
                         : ctx->kern == 4 ? biot::tile2d_chunk()
@@ -1163,7 +1185,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         CU(cudaMemsetAsync(ctx->xbase[k], 0, panel_bytes, ctx->stream));
         ctx->x[k] = ctx->xbase[k] + ctx->pad * nc * ctx->pitch;
     }
-    if (ctx->precond == 1) {
+    if (ctx->precond == 1 && !ctx->p1_fused) {   // the Z panel of the two-pass P~1
         ALLOC(ctx->zbase, panel_bytes);
         CU(cudaMemsetAsync(ctx->zbase, 0, panel_bytes, ctx->stream));
         ctx->z = ctx->zbase + ctx->pad * nc * ctx->pitch;
@@ -1255,6 +1277,22 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         tmp.n_rows = ctx->n_rows;
         tmp.rows_per_tile = ctx->rows_per_tile;
         ctx->groups = biot::tile2d_groups(tmp, ctx->shape.grid);
+        {
+            // fused P~1: 10 owned columns per tile, 2 extra z_u rows and 4 extra x rows per tile
+            const int64_t n_seg1 = (ctx->row_w + biot::tile2d_seg_p1() - 1) / biot::tile2d_seg_p1();
+            int64_t r1 = 1;
+            double best1 = 1e300;
+            for (int64_t rr = 1; rr <= biot::tile2d_max_rows(); ++rr) {
+                const int64_t waves = (n_seg1 * ((ctx->n_rows + rr - 1) / rr) + ctx->shape.grid - 1) / ctx->shape.grid;
+                const double cost = (double)waves * ((double)std::min<int64_t>(rr, ctx->n_rows) + 2.5);
+                if (cost < best1 - 1e-9) { best1 = cost; r1 = rr; }
+            }
+            if (const char *e = std::getenv("BIOT_P1_ROWS")) r1 = std::max(1, std::min(biot::tile2d_max_rows(), std::atoi(e)));
+            ctx->rows_per_tile_p1 = (int32_t)r1;
+            tmp.rows_per_tile = ctx->rows_per_tile_p1;
+            tmp.mode = biot::MODE_P1_FUSED;
+            ctx->groups_p1 = biot::tile2d_groups(tmp, ctx->shape.grid);
+        }
         // interior template + per-node aux records
         const int S = 7, WB = 10, KA = ctx->n_load > 1 ? biot::Tile2dArgs::kAuxML : biot::Tile2dArgs::kAux;
         const int64_t tnode = (int64_t)(ctx->n_rows / 2) * ctx->row_w + ctx->row_w / 2;
@@ -1278,13 +1316,13 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         CU(h2d(ctx, ctx->cls, cls2.data(), cls2.size() * sizeof(double)));
         // records for every node a tile's bulk copy can touch: the last row's segment may
         // extend up to one segment past node N-1
-        const int64_t aux_nodes = ctx->N + 2 * biot::tile2d_seg() + 8;
-        std::vector<double> aux((size_t)aux_nodes * KA, 0.0);
+        const int64_t aux_nodes = ctx->N + 2 * biot::tile2d_seg() + 8, aux_front = 16;   // front: halo column -1
+        std::vector<double> aux((size_t)(aux_front + aux_nodes) * KA, 0.0);
         int64_t n_int = 0;
         for (int64_t i = 0; i < ctx->N; ++i) {
             const double *b = op->blk.data() + (size_t)i * S * WB;
             const bool same = base_ok && template_node(*op, i, tb, [&](int q, int k) { return tz(q, k, z0); });
-            double *r = aux.data() + (size_t)i * KA;
+            double *r = aux.data() + (size_t)(aux_front + i) * KA;
             for (int q = 0; q < S; ++q) r[q] = b[q * WB + 8];
             for (int c = 0; c < 3; ++c) {
                 r[7 + c] = op->load[(size_t)i * 3 + c];
@@ -1300,8 +1338,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             std::fprintf(stderr, "[biot] tile2d: W=%lld rows/tile=%d groups=%lld interior=%lld/%lld s0=%d\n",
                          (long long)ctx->row_w, ctx->rows_per_tile, (long long)ctx->groups, (long long)n_int,
                          (long long)ctx->N, ctx->s0);
-        ALLOC(ctx->aux, aux.size() * sizeof(double));
-        CU(h2d(ctx, ctx->aux, aux.data(), aux.size() * sizeof(double)));
+        ALLOC(ctx->aux_base, aux.size() * sizeof(double));
+        CU(h2d(ctx, ctx->aux_base, aux.data(), aux.size() * sizeof(double)));
+        ctx->aux = ctx->aux_base + aux_front * KA;
         // TMA tensor maps of the two panels: {time (pitch), panel rows}
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult qres;
@@ -1404,8 +1443,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             std::fprintf(stderr, "[biot] tile3d: n1=%d z_rows=%d tiles=%lld interior=%lld/%lld s0=%d grid=%d\n",
                          ctx->n1, ctx->z_rows, (long long)ctx->groups, (long long)n_int, (long long)ctx->N, ctx->s0,
                          ctx->shape.grid);
-        ALLOC(ctx->aux, aux.size() * sizeof(double));
-        CU(h2d(ctx, ctx->aux, aux.data(), aux.size() * sizeof(double)));
+        ALLOC(ctx->aux_base, aux.size() * sizeof(double));
+        CU(h2d(ctx, ctx->aux_base, aux.data(), aux.size() * sizeof(double)));
+        ctx->aux = ctx->aux_base;
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult qres;
         CU(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qres));
@@ -1444,8 +1484,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         CU(biot::sweep_shape(ctx->d, ctx->path, ctx->S, false, ctx->device, &p2));
         ctx->pass2_grid = p2.grid;
     }
-    ALLOC(ctx->partial, (size_t)ctx->groups * ctx->n_tl * 2 * sizeof(double));
-    ALLOC(ctx->fin_scratch, (size_t)std::max<int64_t>(1, biot::finalize_scratch_doubles((int)ctx->groups, ctx->n_tl)) *
+    const int64_t gmax = std::max(ctx->groups, ctx->groups_p1);
+    ALLOC(ctx->partial, (size_t)gmax * ctx->n_tl * 2 * sizeof(double));
+    ALLOC(ctx->fin_scratch, (size_t)std::max<int64_t>(1, biot::finalize_scratch_doubles((int)gmax, ctx->n_tl)) *
                                 sizeof(double));
     ALLOC(ctx->hist, (size_t)ctx->hist_cap * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double));
@@ -1582,6 +1623,7 @@ biot_status gs_run_wave(biot_ctx *ctx) {
         win.stride = ctx->pitch;
     }
     win.send = (ctx->world > 1 && hi == L - 1) ? ctx->sendbuf : nullptr;
+    int64_t wave_groups = ctx->groups;
     if (ctx->gs_k > 0) {   // Alg. 3 literal: a GMRES(k) cycle per step of the window
         biot_status st = gmres_cycle(ctx, ctx->gs_k, ctx->tmap[r], ctx->x[r], ctx->x[1 - r], win);
         if (st != BIOT_OK) return st;
@@ -1589,11 +1631,12 @@ biot_status gs_run_wave(biot_ctx *ctx) {
             CU(cudaMemcpy2DAsync(win.send, sizeof(double), ctx->x[1 - r] + (L - 1), ctx->pitch * sizeof(double),
                                  sizeof(double), (size_t)ctx->N * ctx->nc, cudaMemcpyDeviceToDevice, ctx->stream));
     } else {
-        const int mode = ctx->precond == 2 ? biot::MODE_UPDATE_P2 : biot::MODE_P1_PASS1;
+        const int mode = main_mode(ctx);
         CU(launch_main(ctx, mode, ctx->x[r], ctx->x[1 - r], &win));
-        if (ctx->precond == 1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
+        if (mode == biot::MODE_P1_PASS1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
+        wave_groups = groups_of(ctx, mode);
     }
-    CU(biot::launch_finalize_wave(ctx->partial, (int)ctx->groups, win.len, win.t_off, lo, ctx->gs_k0 + w - g0,
+    CU(biot::launch_finalize_wave(ctx->partial, (int)wave_groups, win.len, win.t_off, lo, ctx->gs_k0 + w - g0,
                                   ctx->hist_cap, L, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
     if (win.send) ctx->send_dirty = false;
     return BIOT_OK;
@@ -1975,8 +2018,9 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->bytes_per_iter = 16.0 * st + 8.0 * (double)(ctx->nnz_AA + ctx->nnz_AP);
     o->flops_per_iter = 2.0 * (double)(ctx->nnz_AA + ctx->nnz_AP) * ctx->n_tl;
     o->device_bytes = (double)ctx->device_bytes;
-    o->launches_per_iter = 1 + (ctx->precond == 1 ? 1 : 0) +
-                           (biot::finalize_scratch_doubles((int)ctx->groups, ctx->n_tl) > 0 ? 2 : 1);
+    const int mm = main_mode(ctx);
+    o->launches_per_iter = 1 + (mm == biot::MODE_P1_PASS1 ? 1 : 0) +
+                           (biot::finalize_scratch_doubles((int)groups_of(ctx, mm), ctx->n_tl) > 0 ? 2 : 1);
     o->interior_nodes = (int32_t)ctx->n_interior;
     return BIOT_OK;
 }

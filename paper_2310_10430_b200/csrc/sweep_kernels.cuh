@@ -19,6 +19,8 @@ enum SweepMode : int {
     MODE_PASS2 = 3,       // P~1 second pass (tile kernels): x_p += omega DSinv (B^T z_u - r_p)
     MODE_ZOUT = 4,        // GMRES start (2D tile): zbuf = P~2^{-1} r, norms of r, x untouched
     MODE_MATVEC = 5,      // GMRES Arnoldi (2D tile): xn = P~2^{-1} AA x, no time coupling
+    MODE_P1_FUSED = 6,    // P~1 in one pass (2D tile): residual, z_u, z_p = D_S^{-1}(B^T z_u - r_p) from
+                          // the neighbours' z_u (recomputed on the tile's halo), update, norms
 };
 
 struct SweepArgs {
@@ -134,6 +136,7 @@ int64_t tile2d_groups(const Tile2dArgs &a, int grid);   // norm-partial groups: 
 int tile2d_chunk();
 int tile2d_seg();         // grid columns per tile
 int tile2d_max_rows();    // rows per tile (q carry capacity)
+int tile2d_seg_p1();      // own grid columns per tile of the fused P~1 mode
 void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,

@@ -67,9 +67,6 @@ struct Lay {
     static constexpr uint32_t kCarryOff = kClsOff + (NL == 1 ? 9 * 7 * kCW * 8 : 0);
     static constexpr uint32_t kSmemBytes = kCarryOff + kMaxRR * kSeg * 8;
 };
-constexpr uint32_t kSmemBytes = Lay<1>::kSmemBytes > Lay<kMaxLoads>::kSmemBytes ? Lay<1>::kSmemBytes
-                                                                               : Lay<kMaxLoads>::kSmemBytes;
-static_assert(kSmemBytes <= 232448, "tile2d shared memory exceeds 227 KB");
 
 // (row delta, column delta) of the 7 BDIA slots in storage order
 __host__ __device__ constexpr int sdr(int s) { return (s == 1 || s == 2) ? -1 : (s >= 5) ? 1 : 0; }
@@ -620,14 +617,411 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
 }
 
+
+// ============================================================================
+// P~1 in one pass (PAPER.md eq. p1: P~1 = [[A, 0], [B^T, -S~p]], so
+// z_u = A^{-1} r_u and z_p = S~p^{-1} (B^T z_u - r_p); inner inverses by their
+// diagonals, reading R2).  z_p of a node needs z_u of its 7 neighbours, and z_u of a
+// neighbour needs that neighbour's residual, so a tile computes z_u on a one-node
+// halo around the nodes it owns: of the 12 consumer columns (strip positions 1..12)
+// positions 2..11 are owned and 1, 12 only produce z_u; the rows march from ja-1 to
+// jb (ja-1 and jb produce z_u only), reading x rows ja-2..jb+1.  The pressure update
+// is lagged one row: at row step m a warp finishes node m-1 (residual, norms, x_u,
+// z_u published in shared memory), then -- after a CTA-wide named barrier -- adds
+// the B^T contributions of row m-1's z_u to the nodes of rows m-2, m-1 and m of its
+// column (push form: the node's own coefficients, slot order (row, column) as the
+// two-pass kernel's pull), which completes node m-2: x_p += omega D_S^{-1} (bt - r_p).
+// The Z panel round trip of the two-pass form (8 + 5 panel accesses per DoF instead
+// of 6) is gone; the halo costs 14/10 x reads and 12/10 x residual work.
+// ============================================================================
+constexpr int kSegP1 = kSeg - 2;            // owned grid columns per tile
+
+template <int NL>
+struct LayP1 {
+    static constexpr int kStages = NL == 1 ? 4 : 3;
+    static constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
+    static constexpr uint32_t kAuxBytes = kSeg * kAuxRec * 8;
+    static constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;
+    static constexpr uint32_t kZBytes = kSeg * 2 * kCT * 8;                 // z_u of one row: 12 positions x 2 comps
+    static constexpr uint32_t kZOff = kStages * kStageBytes;
+    static constexpr uint32_t kCarryOff = kZOff + 2 * kZBytes;              // z_u double-buffered by row parity
+    static constexpr uint32_t kSmemBytes = kCarryOff + (kMaxRR + 1) * kSeg * 8;   // + dummy carry row (halo rows)
+};
+static_assert(LayP1<1>::kSmemBytes <= 232448 - 128 && LayP1<kMaxLoads>::kSmemBytes <= 232448 - 128,
+              "fused P~1 tile exceeds 227 KB");
+
+constexpr uint32_t cmax(uint32_t x, uint32_t y) { return x > y ? x : y; }
+// one dynamic shared-memory size for every tile2d kernel (the largest layout)
+constexpr uint32_t kSmemBytes = cmax(cmax(Lay<1>::kSmemBytes, Lay<kMaxLoads>::kSmemBytes),
+                                     cmax(LayP1<1>::kSmemBytes, LayP1<kMaxLoads>::kSmemBytes));
+static_assert(kSmemBytes <= 232448 - 128, "tile2d shared memory exceeds 227 KB");
+
+// B^T contributions of one published z_u row to the node at row delta -DR from it: the
+// node's slots of row delta DR, in column order (dc = -1, 0, +1), components u_x, u_y.
+template <int DR, bool CLS, bool S0, class A>
+__device__ __forceinline__ void bt_row(const A &a, const double *zrow, int p, int lane, const double *T,
+                                       double (&bt)[kT2]) {
+#pragma unroll
+    for (int dc = -1; dc <= 1; ++dc) {
+        const int s = slot2(DR, dc);
+        if (s < 0) continue;
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+            if constexpr (!CLS) {
+                if (tmpl_zero(s, 6 + cc, S0)) continue;
+            }
+            const double cf = CLS ? T[s * kCW + cc * 3 + 2] : a.tmpl[s][6 + cc];
+            const double *src = zrow + ((p + dc - 1) * 2 + cc) * kCT + lane * 2;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 w = *reinterpret_cast<const double2 *>(src + h * (kCT / 2));
+                bt[2 * h] = fma(cf, w.x, bt[2 * h]);
+                bt[2 * h + 1] = fma(cf, w.y, bt[2 * h + 1]);
+            }
+        }
+    }
+}
+
+template <int DR, bool S0, class A>
+__device__ __forceinline__ void bt_row_any(const A &a, const double *zrow, int p, int lane, int kind,
+                                           const double *T, double (&bt)[kT2]) {
+    if (kind == 1) bt_row<DR, false, S0, A>(a, zrow, p, lane, T, bt);
+    else bt_row<DR, true, S0, A>(a, zrow, p, lane, T, bt);
+}
+
+// Finish node (m-1) of the fused pass: the +W slots, the residual epilogue (norms of
+// owned nodes), x_u^{k+1} of owned nodes; returns z_u (published by the caller),
+// r_p and x_p^k of the lane's steps.
+template <bool CLS, bool S0, int NL, class A>
+__device__ __forceinline__ void finish_p1(const A &a, const double *po, const double *pu, int p, int lane,
+                                          const double *aux, const double *T, int64_t i, int t0, bool ghost,
+                                          bool whole, bool own, double *carry, const double (&sv)[kT2],
+                                          double (&acc)[3][kT2], double (&q)[kT2], double (&nu)[kT2],
+                                          double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2]) {
+    accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
+    if constexpr (NL > 1) {
+#pragma unroll
+        for (int j = 1; j < NL; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + j * a.s_pitch + a.t_off + t0 +
+                                                                           h * (kCT / 2)));
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const double fj = aux[14 + 3 * (j - 1) + c];
+                    acc[c][2 * h] = fma(-s2.x, fj, acc[c][2 * h]);
+                    acc[c][2 * h + 1] = fma(-s2.y, fj, acc[c][2 * h + 1]);
+                }
+            }
+    }
+    double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
+    double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
+    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
+    __syncwarp();
+    if (lane == 31) *carry = q[3];
+    double Dv[3], xs[3][kT2];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) Dv[c] = aux[10 + c];
+    load_v(xs, po, p, lane);
+    const int64_t P = a.pitch;
+    const int n_tl = a.n_tl;
+    const int64_t row = i * 3 * P + a.t_off + t0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        double acc2[3][2], q2[2], xs2[3][2], nu2[2] = {0.0, 0.0}, np2[2] = {0.0, 0.0}, outx[3][2], outz[3][2];
+        Loads<3, 2, 1> ld;
+        ld.sv[0][0] = sv[2 * h];
+        ld.sv[0][1] = sv[2 * h + 1];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ld.F[0][c] = aux[7 + c];
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) {
+            q2[tt] = q[2 * h + tt];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                acc2[c][tt] = acc[c][2 * h + tt];
+                xs2[c][tt] = xs[c][2 * h + tt];
+            }
+        }
+        epilogue_math<2, 2, CLS, false>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2, outx, outz);
+        const int th = t0 + h * (kCT / 2);
+        // z_u published for the neighbours; the pressure part waits for B^T z_u:
+        // x_p^{k+1} = x_p + omega D_S^{-1} (bt - r_p) = y + (omega D_S^{-1}) bt
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            *reinterpret_cast<double2 *>(zd + c * kCT + h * (kCT / 2)) = make_double2(outz[c][0], outz[c][1]);
+#pragma unroll
+        for (int tt = 0; tt < 2; ++tt) y[2 * h + tt] = fma(-wdv, outz[2][tt], xs2[2][tt]);
+        if (own) {
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+                nu[2 * h + tt] += nu2[tt];       // = the in-place accumulation: nu + (0 + su)
+                npn[2 * h + tt] += np2[tt];
+            }
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                double *dst = a.xn + row + c * P + h * (kCT / 2);
+                if (whole) {
+                    *reinterpret_cast<double2 *>(dst) = make_double2(outx[c][0], outx[c][1]);
+                } else {
+                    if (st0) dst[0] = outx[c][0];
+                    if (st1) dst[1] = outx[c][1];
+                }
+            }
+            if (a.sendbuf) {
+                const int tl = n_tl - 1 - th;
+                if (tl == 0 || tl == 1)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) a.sendbuf[i * 3 + c] = tl == 0 ? outx[c][0] : outx[c][1];
+            }
+        }
+    }
+}
+
+// x_p^{k+1} of an owned node whose B^T z_u is complete (as finish_bt of the two-pass form)
+template <class A>
+__device__ __forceinline__ void finish_zp(const A &a, int64_t i, int t0, bool whole, double wdv,
+                                          const double (&bt)[kT2], const double (&y)[kT2]) {
+    const int64_t P = a.pitch, row = i * 3 * P + 2 * P + a.t_off + t0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const double v0 = fma(wdv, bt[2 * h], y[2 * h]);
+        const double v1 = fma(wdv, bt[2 * h + 1], y[2 * h + 1]);
+        double *dst = a.xn + row + h * (kCT / 2);
+        const int th = t0 + h * (kCT / 2);
+        if (whole) {
+            *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
+        } else {
+            if (th < a.n_tl && th >= a.t_lo) dst[0] = v0;
+            if (th + 1 < a.n_tl) dst[1] = v1;
+        }
+        if (a.sendbuf) {
+            if (th == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v0;
+            if (th + 1 == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v1;
+        }
+    }
+}
+
+__device__ __forceinline__ void named_barrier_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+template <bool S0, int NL>
+__global__ void __launch_bounds__(kThreads2, 1)
+    tile2d_p1_kernel(const __grid_constant__ CUtensorMap tmx, const Tile2dArgs a) {
+    using L = LayP1<NL>;
+    constexpr int kStages = L::kStages, kAuxRec = L::kAuxRec;
+    constexpr uint32_t kAuxBytes = L::kAuxBytes, kStageBytes = L::kStageBytes;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ uint64_t full[kStages], empty[kStages];
+    double *zbuf = reinterpret_cast<double *>(smem + L::kZOff);          // [2][12][2][kCT]
+    double *qcarry = reinterpret_cast<double *>(smem + L::kCarryOff);    // [kMaxRR + 1][kSeg]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int W = (int)a.row_w, nrows = a.n_rows, rr = a.rows_per_tile;
+    const int nseg = (W + kSegP1 - 1) / kSegP1, nrr = (nrows + rr - 1) / rr;
+    const int ntiles = nseg * nrr, nchunks = (a.n_tl + kCT - 1) / kCT;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kSeg);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp >= kSeg) {
+        // ------------------------------- producer -------------------------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
+        if (warp == kSeg && lane == 0) {
+            uint32_t it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int i0 = (tile % nseg) * kSegP1, ja = (tile / nseg) * rr, jb = min(nrows, ja + rr);
+                for (int chunk = 0; chunk < nchunks; ++chunk)
+                    for (int r = ja - 2; r <= jb + 1; ++r, ++it) {
+                        const int st = it % kStages;
+                        if (it >= (uint32_t)kStages) mbar_wait_suspend(&empty[st], ((it / kStages) - 1) & 1);
+                        unsigned char *base = smem + (size_t)st * kStageBytes;
+                        const bool real = (r >= 0 && r < nrows);
+                        mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
+                        const int64_t node0 = (int64_t)r * W + i0 - 2;
+                        load_2d(base, &tmx, a.t_off + chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
+                        if (real)
+                            bulk_g2s(base + kXBytes, a.aux + ((int64_t)r * W + i0 - 1) * kAuxRec, kAuxBytes,
+                                     &full[st]);
+                    }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------- consumers ------------------------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kConsumerRegs));
+    const int p = warp + 1;                   // strip position: 1..12, owned 2..11
+    const double *const cls_base = a.cls;     // class stencils (boundary nodes) from global memory
+    uint32_t it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int i0 = (tile % nseg) * kSegP1, ja = (tile / nseg) * rr, jb = min(nrows, ja + rr);
+        const int col = i0 + p - 2;
+        const bool valid = col >= 0 && col < W;
+        const bool ocol = valid && p >= 2 && p <= kSegP1 + 1;
+        const int ccx = axis_class(min(max(col, 0), W - 1), W);
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const int t0 = chunk * kCT + lane * 2;
+            const bool ghost = chunk == 0;
+            const bool whole = (chunk + 1) * kCT <= a.n_tl && (chunk > 0 || a.t_lo == 0);
+            double nu[kT2], npn[kT2], sv[kT2];
+            const bool first = tile == (int)blockIdx.x;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
+                sv[2 * h] = s2.x;
+                sv[2 * h + 1] = s2.y;
+            }
+#pragma unroll
+            for (int tt = 0; tt < kT2; ++tt) nu[tt] = npn[tt] = 0.0;
+            if (ghost && nchunks > 1 && ocol) {
+                // q(t0-1) of chunk 0 for the tile's owned rows, as the P~2 kernel does
+                for (int mm = ja + lane; mm < jb; mm += 32) {
+                    const int64_t i = (int64_t)mm * W + col;
+                    const bool intr = __ldg(a.aux + i * kAuxRec + 13) == 1.0;
+                    qcarry[(mm - ja) * kSeg + warp] =
+                        intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
+                             : ghost_q<true, S0, Tile2dArgs>(a, i, cls_base + (ccx + 3 * axis_class(mm, nrows)) * 7 * kCW);
+                }
+                __syncwarp();
+            }
+            double acc[3][kT2], q[kT2];
+            double btA[kT2], btB[kT2], btC[kT2];          // B^T z_u of the nodes of rows m-2, m-1, m
+            double yA[kT2], yB[kT2];                      // x_p - omega D_S^{-1} r_p of rows m-2, m-1
+            double wA = 0.0, wB = 0.0;                    // omega D_S^{-1} of rows m-2, m-1
+            int kindP = 0, kindA = 0, kindB = 0;          // node m-1 (pending finish); rows m-2, m-1 (pending z_p)
+            const double *T = cls_base;
+#pragma unroll
+            for (int tt = 0; tt < kT2; ++tt) btA[tt] = btB[tt] = btC[tt] = yA[tt] = yB[tt] = 0.0;
+            int sd = it % kStages;                        // stage of row m-1
+            uint32_t phd = (it / kStages) & 1;
+            mbar_wait_suspend(&full[sd], phd);
+            for (int m = ja - 1; m <= jb + 1; ++m) {
+                const int sm_ = sd + 1 == kStages ? 0 : sd + 1;
+                const uint32_t phm = sm_ == 0 ? phd ^ 1u : phd;
+                mbar_wait_suspend(&full[sm_], phm);
+                const double *pd = reinterpret_cast<const double *>(smem + (size_t)sd * kStageBytes);
+                const double *pm = reinterpret_cast<const double *>(smem + (size_t)sm_ * kStageBytes);
+                double *zrow = zbuf + (size_t)((m - 1) & 1) * (kSeg * 2 * kCT);
+                const bool orow1 = m - 1 >= ja && m - 1 < jb;       // node m-1 owned (row)
+                // (1) finish node m-1 and publish its z_u (zero off the mesh)
+                if (m >= ja) {
+                    double *zd = zrow + (p - 1) * 2 * kCT + lane * 2;
+                    if (kindP != 0) {
+                        const double *aux = reinterpret_cast<const double *>(
+                                                reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
+                        const int64_t i = (int64_t)(m - 1) * W + col;
+                        double *carry = qcarry + (orow1 ? (m - 1 - ja) : kMaxRR) * kSeg + warp;
+                        const bool own = orow1 && ocol;
+                        wB = a.omega * aux[12];
+                        if (kindP == 1)
+                            finish_p1<false, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
+                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                        else
+                            finish_p1<true, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
+                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 2; ++c)
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+                                *reinterpret_cast<double2 *>(zd + c * kCT + h * (kCT / 2)) = make_double2(0.0, 0.0);
+                    }
+                }
+                kindB = (orow1 && ocol) ? kindP : 0;
+                kindP = 0;
+                // (2) every z_u of row m-1 is published
+                named_barrier_sync(1, kSeg * 32);
+                // (3) B^T contributions of row m-1's z_u: node m-2 (its +W slots; then complete),
+                // node m-1 (0 slots), node m (-W slots)
+                int kindC = 0;
+                if (m <= jb && valid) {
+                    const double *auxm = reinterpret_cast<const double *>(
+                                             reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                    if (m >= 0 && m < nrows) kindC = auxm[13] == 1.0 ? 1 : 2;
+                }
+                if (m >= ja) {
+                    if (kindA != 0) {
+                        const double *TA = cls_base + (ccx + 3 * axis_class(m - 2, nrows)) * 7 * kCW;
+                        bt_row_any<1, S0, Tile2dArgs>(a, zrow, p, lane, kindA, TA, btA);
+                        finish_zp<Tile2dArgs>(a, (int64_t)(m - 2) * W + col, t0, whole, wA, btA, yA);
+                    }
+                    if (kindB != 0) {
+                        const double *TB = cls_base + (ccx + 3 * axis_class(m - 1, nrows)) * 7 * kCW;
+                        bt_row_any<0, S0, Tile2dArgs>(a, zrow, p, lane, kindB, TB, btB);
+                    }
+                    if (kindC != 0 && m >= ja && m < jb && ocol) {
+                        const double *TC = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
+#pragma unroll
+                        for (int tt = 0; tt < kT2; ++tt) btC[tt] = 0.0;
+                        bt_row_any<-1, S0, Tile2dArgs>(a, zrow, p, lane, kindC, TC, btC);
+                    }
+                }
+                // rotate the pending rows: m-1 -> A, m -> B
+                kindA = kindB;
+                wA = wB;
+#pragma unroll
+                for (int tt = 0; tt < kT2; ++tt) {
+                    btA[tt] = btB[tt];
+                    yA[tt] = yB[tt];
+                    btB[tt] = btC[tt];
+                    btC[tt] = 0.0;
+                }
+                // (4) start node m (z rows ja-1..jb on the mesh)
+                if (m <= jb && kindC != 0) {
+                    const double *aux = reinterpret_cast<const double *>(
+                                            reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                    kindP = kindC;
+                    if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
+                    if (kindP == 1) start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                    else start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[sd]);   // row m-1 no longer needed
+                sd = sm_;
+                phd = phm;
+            }
+            if (lane == 0) mbar_arrive(&empty[sd]);       // row jb+1
+            it += (uint32_t)(jb - ja + 4);
+            // per-(CTA, column) norm partials, summed over this CTA's tiles in order (the
+            // halo columns contribute zeros)
+#pragma unroll
+            for (int tt = 0; tt < kT2; ++tt) {
+                const int t = t0 + (tt >> 1) * (kCT / 2) + (tt & 1);
+                if (t < a.n_tl) {
+                    double *dst = a.partial + (((int64_t)blockIdx.x * kSeg + warp) * a.n_tl + t) * 2;
+                    const double u = t >= a.t_lo ? nu[tt] : 0.0, v = t >= a.t_lo ? npn[tt] : 0.0;
+                    if (first) {
+                        dst[0] = u;
+                        dst[1] = v;
+                    } else {
+                        dst[0] = dst[0] + u;
+                        dst[1] = dst[1] + v;
+                    }
+                }
+            }
+        }
+    }
+}
+
 }  // namespace
 
 int tile2d_seg() { return kSeg; }
+int tile2d_seg_p1() { return kSegP1; }
 int tile2d_chunk() { return kCT; }
 int tile2d_max_rows() { return kMaxRR; }
 
 int64_t tile2d_tiles(const Tile2dArgs &a) {
-    const int64_t n_seg = (a.row_w + kSeg - 1) / kSeg;
+    const int seg = a.mode == MODE_P1_FUSED ? kSegP1 : kSeg;
+    const int64_t n_seg = (a.row_w + seg - 1) / seg;
     const int64_t n_rr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
     return n_seg * n_rr;
 }
@@ -653,7 +1047,9 @@ cudaError_t tile2d_shape(int device, LaunchShape *out) {
                     tile2d_kernel<false, MODE_RESIDUAL, ML>, tile2d_kernel<true, MODE_RESIDUAL, ML>,
                     tile2d_kernel<false, MODE_ZOUT, ML>, tile2d_kernel<true, MODE_ZOUT, ML>,
                     tile2d_kernel<false, MODE_PASS2, ML>, tile2d_kernel<true, MODE_PASS2, ML>,
-                    tile2d_kernel<false, MODE_MATVEC, ML>, tile2d_kernel<true, MODE_MATVEC, ML>}) {
+                    tile2d_kernel<false, MODE_MATVEC, ML>, tile2d_kernel<true, MODE_MATVEC, ML>,
+                    tile2d_p1_kernel<false, 1>, tile2d_p1_kernel<true, 1>, tile2d_p1_kernel<false, ML>,
+                    tile2d_p1_kernel<true, ML>}) {
         e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemBytes);
         if (e != cudaSuccess) return e;
     }
@@ -676,7 +1072,12 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
 #define BIOT_T2(S0_, M_, NL_) tile2d_kernel<S0_, M_, NL_><<<grid, block, sh.smem, st>>>(tmx, a)
 // NL = kMaxLoads also selects the aux-record layout (Lay), so every mode follows n_load
 #define BIOT_T2L(S0_, M_) { if (a.n_load > 1) BIOT_T2(S0_, M_, kMaxLoads); else BIOT_T2(S0_, M_, 1); }
-    if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2L(true, MODE_UPDATE_P2) else BIOT_T2L(false, MODE_UPDATE_P2) }
+    if (a.mode == MODE_P1_FUSED) {
+#define BIOT_T2P(S0_, NL_) tile2d_p1_kernel<S0_, NL_><<<grid, block, sh.smem, st>>>(tmx, a)
+        if (a.n_load > 1) { if (a.s0) BIOT_T2P(true, kMaxLoads); else BIOT_T2P(false, kMaxLoads); }
+        else { if (a.s0) BIOT_T2P(true, 1); else BIOT_T2P(false, 1); }
+#undef BIOT_T2P
+    } else if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T2L(true, MODE_UPDATE_P2) else BIOT_T2L(false, MODE_UPDATE_P2) }
     else if (a.mode == MODE_P1_PASS1) { if (a.s0) BIOT_T2L(true, MODE_P1_PASS1) else BIOT_T2L(false, MODE_P1_PASS1) }
     else if (a.mode == MODE_PASS2) { if (a.s0) BIOT_T2L(true, MODE_PASS2) else BIOT_T2L(false, MODE_PASS2) }
     else if (a.mode == MODE_ZOUT) { if (a.s0) BIOT_T2L(true, MODE_ZOUT) else BIOT_T2L(false, MODE_ZOUT) }

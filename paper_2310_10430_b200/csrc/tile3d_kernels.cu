@@ -452,6 +452,11 @@ __global__ void __launch_bounds__(kThreadsOf<R>, 1)
         // class stencils this tile can touch: x class in {cxl, cxl+1}, y in {cyl, cyl+1}, z in
         // {interior, the one z face the tile's plane range reaches (z_rows < n1)}
         const int cxl = x0 == 0 ? 0 : 1, cyl = y0 == 0 ? 0 : 1, czf = za == 0 ? 0 : 2;
+        // every consumer is done with the previous tile's class stencils before they are
+        // overwritten (the norm-reduction barriers order this in the residual modes, but
+        // the PASS2 / MATVEC modes have none: without this barrier a fast warp reloaded
+        // the stencils under a slow one -- found by the full-K parity test of P~1, config 4)
+        if (tile != (int)blockIdx.x) asm volatile("bar.sync 1, %0;" ::"r"(kConsumers * 32) : "memory");
         for (int k = threadIdx.x; k < kClsLocal * kClsD; k += kConsumers * 32) {
             const int L = k / kClsD, w = k - L * kClsD;
             const int cz = (L >> 2) ? czf : 1, cy = cyl + ((L >> 1) & 1), cx = cxl + (L & 1);

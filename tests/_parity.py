@@ -81,3 +81,23 @@ def oracle_window(sysm, x0_fn, s, n_lo, n_hi, K, precond, omega, ghost=None, nth
     X[1:] = sysm.to_paper(x0_fn(steps))
     X, _ = sysm.iterate(X, s[steps - 1], K, precond, omega, history=False, nthreads=nthreads)
     return sysm.from_paper(X[1 + (n_lo - a):])
+
+
+def oracle_window_full(sysm, x0_fn, s, n_lo, n_hi, K, precond, omega, nthreads=0):
+    """As oracle_window, plus the residual history and the norms at x^K.
+
+    Returns (x [L, ndof], hist [K, L, 2], norms [L, 2], exact_from) for the global steps
+    n_lo..n_hi (L = n_hi - n_lo + 1).  The oracle starts at a = max(1, n_lo - K) with a
+    zero ghost; x^k_n is exact for n >= a + k (one step of the light cone per iteration),
+    so x^K and every history entry r(x^k)_n (k < K) are exact on the window, and the norms
+    at x^K from step exact_from on (n_lo + 1 when a > 1: r(x^K)_{n_lo} reads x^K_{n_lo-1};
+    every step when a = 1, whose ghost is the true x_0).
+    """
+    a = max(1, n_lo - K)
+    steps = np.arange(a, n_hi + 1)
+    X = np.zeros((steps.size + 1, sysm.ndof))
+    X[1:] = sysm.to_paper(x0_fn(steps))
+    X, hist = sysm.iterate(X, s[steps - 1], K, precond, omega, history=True, nthreads=nthreads)
+    rn = sysm.residual_norms(X, s[steps - 1], nthreads=nthreads)
+    o = n_lo - a
+    return (sysm.from_paper(X[1 + o:]), hist[:, o:], rn[o:], n_lo if a == 1 else n_lo + 1)
