@@ -7,8 +7,14 @@ time step of the workload (residual with previous-step coupling, block
 preconditioner, damped update, per-step residual norms).  Default workload:
 config 3 (2D 512x512 P1-P1, N_t = 1024, kappa=1e-6, S=0), the configuration the
 metric's roofline and 8-GPU efficiency targets are quoted on that fits one GPU
-(DESIGN.md "Measurement").  N > 1: torchrun, one rank per GPU, time slabs of
-N_t/N steps, NCCL send/recv of one slice per step (strong scaling).
+(DESIGN.md "Measurement").  N > 1: one rank per GPU (under torchrun, or
+self-spawned through torch.distributed.run when WORLD_SIZE is unset), time slabs
+of N_t/N steps, NCCL send/recv of one slice per outer iteration (strong scaling).
+
+Timing: W warm-up iterations, then --repeats (default 5) timed runs of exactly K
+outer iterations, each bracketed by a barrier + device synchronize and timed with
+CUDA events on the launching stream, max over ranks; the line reports the median
+run, nvidia-smi clocks sampled across the timed runs.
 
 Prints ONE JSON line on rank 0.
 """
@@ -54,7 +60,24 @@ def parse():
     ap.add_argument("--gmres-k", type=int, default=10)
     ap.add_argument("--cheb-m", type=int, default=2, help="Chebyshev steps per inner inverse (--method cheb)")
     ap.add_argument("--cheb-alpha", type=float, default=30.0)
+    ap.add_argument("--repeats", type=int, default=5, help="timed runs of K iterations; the median is reported")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel directly (BIOT_FLAG_NO_GRAPH)")
     return ap.parse_args()
+
+
+def spawn_ranks(n):
+    """--gpus N without a launcher: re-run this command under torch.distributed.run with N
+    local ranks (127.0.0.1 rendezvous); rank 0 prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # communicator size visible in the NCCL INIT lines
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 def peaks():
@@ -139,7 +162,7 @@ class ClockSampler:
 
 KERNELS = {1: "sweep_kernel<BDIA> (generic, fused residual + P~ + update + norms)",
            2: "sweep_kernel<ELL> (generic, fused residual + P~ + update + norms)",
-           3: "stencil_kernel", 4: "march2d_kernel",
+           4: "march2d_kernel",
            5: "tile2d_kernel (TMA row march, fused residual + P~ + update + norms)",
            7: "tile3d_kernel (TMA plane march, fused residual + P~ + update + norms)"}
 
@@ -255,6 +278,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     import torch
@@ -263,23 +288,26 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus and world > 1:
+    if world != args.gpus:
         raise SystemExit(f"WORLD_SIZE={world} but --gpus {args.gpus}")
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
 
-    from paper_2310_10430_b200 import BiotSolver, nccl_unique_id
+    from paper_2310_10430_b200 import BiotSolver, nccl_unique_id, FLAG_NO_GRAPH
 
     prob = make_problem_for(args)
     nccl_id = None
     if world > 1:
         from paper_2310_10430_b200.dist import broadcast_nccl_id
-        nccl_id = broadcast_nccl_id(nccl_unique_id)
+        nccl_id = broadcast_nccl_id(nccl_unique_id, device=dev)
     stream = torch.cuda.current_stream()
+    reps = max(1, args.repeats)
     g = BiotSolver(prob, precond=args.precond, omega=args.omega, device=local, rank=rank, world=world,
-                   nccl_id=nccl_id, stream=stream.cuda_stream, history=max(1024, args.steps + args.warmup + 8))
+                   nccl_id=nccl_id, stream=stream.cuda_stream, flags=FLAG_NO_GRAPH if args.no_graph else 0,
+                   history=max(1024, reps * args.steps + args.warmup + args.e2e_steps + 8))
     info = g.info
 
     def barrier():
@@ -301,19 +329,21 @@ def main():
     step(max(args.warmup, 3))
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
+    runs = []
     clk.mark()
-    ev0.record(stream)
-    step(args.steps)                   # K outer iterations, one library call, no host sync inside
-    ev1.record(stream)
-    barrier()
+    for _ in range(reps):
+        barrier()
+        ev0.record(stream)
+        step(args.steps)               # K outer iterations, one library call
+        ev1.record(stream)
+        barrier()
+        # preconditioner pass(es) of the dominant kernel, CUDA events on the launching stream
+        t = torch.tensor([ev0.elapsed_time(ev1), float(g.last_timing()[1])], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        runs.append((float(t[0]), float(t[1])))
     clocks = clk.stop()
-    ms = ev0.elapsed_time(ev1)
-    sweep_ms = float(g.last_timing()[1])   # dominant kernel, CUDA events on the launching stream
-    t = torch.tensor([ms, sweep_ms], dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, sweep_ms = float(t[0]), float(t[1])
+    ms, sweep_ms = sorted(runs)[len(runs) // 2]             # the median run and its kernel time
     ms_per_step = ms / args.steps
     value = prob.n_dof * prob.n_t * args.steps / (ms / 1e3)
 
@@ -335,7 +365,7 @@ def main():
         _lib.check(g.lib.biot_residual_history(g.ctx, g.get_info().iterations - 1, _lib.ptr(out_np)), g.ctx)
     e1.record(stream)
     barrier()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64)
+    e2e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     e2e_value = prob.n_dof * prob.n_t * args.e2e_steps / (float(e2e_ms[0]) / 1e3)
@@ -397,6 +427,8 @@ def main():
                                            "update + operator values once (DESIGN.md roofline)"}
         per_step = info.launches_per_iter
         launches = per_step * args.steps
+        if info.graph and args.method == "jacobi" and args.steps >= 2:
+            launches += 1 + args.steps // 2      # history counter: one set per call + one advance per replay
         if args.method == "gs":   # n_t + K - 1 waves and two checkerboard copies per call
             launches = 2 + (info.n_t_local + args.steps - 1) * per_step
         if args.method == "cheb":   # residual sweep + finalize (1-2) + start + m - 1 steps
@@ -414,6 +446,9 @@ def main():
                                  "per step: biot_set_load_scale (host s_n) + biot_iterate(1) + "
                                  "biot_residual_history readback, host sync each step")},
                 "gpu_launches": launches,
+                "timing": {"repeats": reps, "runs_ms": [r[0] for r in runs], "reported": "median run",
+                           "cuda_graph": bool(info.graph) and args.method == "jacobi",
+                           "comm_nranks": int(info.comm_nranks) if world > 1 else None},
                 "clocks": clocks}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(prob, args.precond, args.omega)

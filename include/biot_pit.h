@@ -31,8 +31,15 @@
  *  - Every call returns a biot_status; nothing aborts or throws across the
  *    ABI.  On error, biot_last_error(ctx) (or biot_last_error(NULL) for
  *    errors before a context exists) holds a message.
- *  - A context is not thread-safe.  With world > 1, biot_setup, biot_iterate
- *    and biot_destroy are collective: every rank calls them in the same order.
+ *  - A context is not thread-safe.  With world > 1 (NCCL), these calls are
+ *    collective -- every rank makes them in the same order, or the call blocks
+ *    until BIOT_NCCL_TIMEOUT_S (default 600 s) and returns BIOT_E_NCCL:
+ *    biot_setup, biot_iterate, biot_iterate_gs, biot_iterate_gmres,
+ *    biot_iterate_cheb, biot_iterate_gs_gmres, biot_residual_norms (it refreshes
+ *    the ghost slice before its residual pass) and biot_destroy.  A failed or
+ *    silent peer surfaces as BIOT_E_NCCL (ncclCommGetAsyncError is polled while
+ *    waiting; the communicator is then aborted and the context unusable for
+ *    further collective calls).
  *  - biot_iterate is additive: iterate(a); iterate(b) == iterate(a+b), bitwise.
  *  - Results are bitwise reproducible run to run, and the iterates x^k are
  *    bitwise independent of world (time-slab count).
@@ -47,7 +54,7 @@
 extern "C" {
 #endif
 
-#define BIOT_PIT_ABI_VERSION 3
+#define BIOT_PIT_ABI_VERSION 4
 
 typedef struct biot_ctx biot_ctx;   /* opaque; owned by the library until biot_destroy */
 
@@ -114,7 +121,9 @@ typedef struct {
 
 #define BIOT_FLAG_MANUAL_HALO 1u     /* world > 1 without NCCL: caller moves the halo with
                                         biot_last_slice / biot_set_ghost (tests, emulation) */
-#define BIOT_FLAG_NO_GRAPH    2u     /* launch kernels directly instead of a CUDA graph     */
+#define BIOT_FLAG_NO_GRAPH    2u     /* biot_iterate launches kernels directly; default: pairs
+                                        of iterations replay one captured CUDA graph (world == 1
+                                        or MANUAL_HALO; NCCL iterations always launch directly) */
 
 typedef struct {
     int32_t precond;         /* 1 = P~1, 2 = P~2                                          */
@@ -135,7 +144,6 @@ typedef struct {
     int32_t n_t, n_t_local, first_step; /* global N_t; owned steps first_step..+n_t_local-1 */
     int64_t iterations;              /* outer iterations done since setup               */
     int32_t kernel_path;             /* 1 = BDIA offsets, 2 = ELL explicit columns,
-                                        3 = register-blocked structured stencil,
                                         4 = 2D row-march (L1-reuse) kernel,
                                         5 = 2D TMA-pipelined tile kernel,
                                         7 = 3D TMA-pipelined tile kernel             */
@@ -146,6 +154,8 @@ typedef struct {
     double device_bytes;             /* device memory held by the context               */
     int32_t launches_per_iter;       /* kernels biot_iterate launches per outer iteration */
     int32_t interior_nodes;          /* nodes on the shared interior stencil (tile kernels; 0 otherwise) */
+    int32_t comm_nranks;             /* ranks of the context's NCCL communicator (0: none)         */
+    int32_t graph;                   /* 1: biot_iterate replays a CUDA graph per pair of iterations */
 } biot_info;
 
 /* Build the operators on the host, upload, allocate the space-time panels
@@ -208,7 +218,8 @@ biot_status biot_gs_wave(biot_ctx *ctx);
 biot_status biot_gs_end(biot_ctx *ctx);
 
 /* Residual norms at the current iterate: out[n_t_local][2] = ||r_u||, ||r_p||
- * of the owned steps (a residual-only pass, no update). */
+ * of the owned steps (a residual-only pass, no update).  Collective for world > 1:
+ * the pass needs the predecessor rank's current last slice (one halo exchange). */
 biot_status biot_residual_norms(biot_ctx *ctx, double *out);
 
 /* Norms of r(x^k) computed inside iteration k (k = 0-based count since setup):
@@ -251,7 +262,9 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *out);
 
 /* Device time of the kernels of the last biot_iterate call, per iteration,
  * measured with CUDA events on the compute stream: out[0] = whole iteration,
- * out[1] = the fused sweep kernel alone (ms). */
+ * out[1] = the preconditioner pass(es) alone (ms): the fused sweep kernel (P~2,
+ * single-pass P~1) or both passes of the two-pass P~1; with the CUDA graph the
+ * mean over the two iterations of the last replay plus any direct launches. */
 biot_status biot_last_timing(const biot_ctx *ctx, double *out_ms);
 
 /* Fill out[128] with a fresh ncclUniqueId (rank 0 only; dlopens libnccl.so.2). */

@@ -62,7 +62,7 @@ class BiotInfo(ctypes.Structure):
                 ("kernel_path", ctypes.c_int32), ("n_slots", ctypes.c_int32), ("beta", ctypes.c_double),
                 ("bytes_per_iter", ctypes.c_double), ("flops_per_iter", ctypes.c_double),
                 ("device_bytes", ctypes.c_double), ("launches_per_iter", ctypes.c_int32),
-                ("interior_nodes", ctypes.c_int32)]
+                ("interior_nodes", ctypes.c_int32), ("comm_nranks", ctypes.c_int32), ("graph", ctypes.c_int32)]
 
 
 # every symbol include/biot_pit.h declares (checked by tests/test_abi.py)

@@ -17,7 +17,7 @@ OUT = os.path.join(HERE, "libbiot_pit.so")
 BUILD = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["host_assembly.cpp", "sweep_kernels.cu", "stencil_kernels.cu", "march_kernels.cu", "tile2d_kernels.cu", "tile3d_kernels.cu", "gmres_kernels.cu", "cheb_kernels.cu", "biot_api.cu"]
+SOURCES = ["host_assembly.cpp", "sweep_kernels.cu", "march_kernels.cu", "tile2d_kernels.cu", "tile3d_kernels.cu", "gmres_kernels.cu", "cheb_kernels.cu", "biot_api.cu"]
 HEADERS = ["host_assembly.h", "sweep_kernels.cuh", "node_update.cuh", "tma_util.cuh"]
 
 

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 #include <limits>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/biot_pit.h"
@@ -39,6 +41,9 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;   // optional
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                           // optional
+    ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;              // optional
 };
 
 NcclApi *nccl() {
@@ -60,6 +65,9 @@ NcclApi *nccl() {
             api.GroupStart = (decltype(api.GroupStart))dlsym(api.h, "ncclGroupStart");
             api.GroupEnd = (decltype(api.GroupEnd))dlsym(api.h, "ncclGroupEnd");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(api.h, "ncclGetErrorString");
+            api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(api.h, "ncclCommGetAsyncError");
+            api.CommAbort = (decltype(api.CommAbort))dlsym(api.h, "ncclCommAbort");
+            api.CommCount = (decltype(api.CommCount))dlsym(api.h, "ncclCommCount");
             if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.GroupStart ||
                 !api.GroupEnd || !api.CommDestroy)
                 api.h = nullptr;
@@ -148,7 +156,7 @@ struct biot_ctx {
     int hist_cap = 1024;
     biot::LaunchShape shape{0, 0};
     int tw = 8, node_block = 8;
-    // kernel choice: 1 generic BDIA/ELL sweep, 2 register-blocked stencil, 3 2D march
+    // kernel choice: 1 generic BDIA/ELL sweep, 3 2D march, 4 2D TMA tile, 6 3D TMA tile
     int kern = 1;
     bool stencil = false;             // detect_stencil() succeeded (structured offsets)
     int mT = 2;                       // march: time steps per lane
@@ -185,13 +193,20 @@ struct biot_ctx {
     int64_t gs_k0 = 0;
     int32_t n1 = 0, z_rows = 0;
     int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
-    int sR = 4, sT = 2;
     int64_t gbase[8] = {0};
     int32_t slot[8][3] = {{0}};
     int64_t n_alloc = 0;              // nodes allocated in operator arrays (>= N, multiple of 8)
     int pass2_grid = 0;
     size_t device_bytes = 0;
     ncclComm_t comm = nullptr;
+    double nccl_timeout_s = 600.0;    // BIOT_NCCL_TIMEOUT_S: a peer silent this long -> BIOT_E_NCCL
+    // CUDA graph of two outer iterations per starting panel (biot_iterate, world == 1 or
+    // manual halo, unless BIOT_FLAG_NO_GRAPH): the history slot comes from d_iter
+    bool use_graph = false;
+    int64_t *d_iter = nullptr;        // device copy of `iterations`
+    cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+    cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};   // sweep spans inside the graph
+    cudaStream_t cap_stream = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     std::vector<cudaEvent_t> ev_s;                 // 2 per iteration of the current call
     double last_ms_iter = 0.0, last_ms_sweep = 0.0;
@@ -236,7 +251,7 @@ void free_all(biot_ctx *c) {
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
-                    (void *)c->gm_small})
+                    (void *)c->gm_small, (void *)c->d_iter})
         if (p) cudaFree(p);
     for (double *p : c->gm_Vbase) cudaFree(p);
     for (double *p : c->cb_base)
@@ -244,6 +259,11 @@ void free_all(biot_ctx *c) {
     for (cudaEvent_t e : {c->ev_a, c->ev_b})
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_s) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->gev)
+        if (e) cudaEventDestroy(e);
+    for (cudaGraphExec_t g : c->gexec)
+        if (g) cudaGraphExecDestroy(g);
+    if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
     if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
@@ -476,15 +496,6 @@ bool detect_stencil(biot_ctx *c) {
     return true;
 }
 
-biot::StencilArgs stencil_args(biot_ctx *c, int mode, const double *xin, double *xout) {
-    biot::StencilArgs a{};
-    static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
-    for (int g = 0; g < 8; ++g) {
-        a.gbase[g] = c->gbase[g];
-        for (int k = 0; k < 3; ++k) a.slot[g][k] = c->slot[g][k];
-    }
-    return a;
-}
 
 // A time window of the panel (Gauss-Seidel waves): steps [t_off, t_off + len), the
 // predecessor of step t_off read from `ghost` with stride `stride`.
@@ -499,10 +510,6 @@ struct Window {
 // the context's own (the GMRES Krylov panels).
 cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, const Window *win = nullptr,
                         const CUtensorMap *tmo = nullptr, double *zb = nullptr) {
-    if (c->kern == 2) {
-        biot::StencilArgs a = stencil_args(c, mode, xin, xout);
-        return biot::launch_stencil(c->d, c->sR, c->sT, a, c->shape, c->stream);
-    }
     if (c->kern == 6) {
         biot::Tile3dArgs a{};
         static_cast<biot::SweepArgs &>(a) = sweep_args(c, mode, xin, xout);
@@ -592,26 +599,108 @@ int main_mode(const biot_ctx *c) {
     return c->precond == 2 ? biot::MODE_UPDATE_P2 : c->p1_fused ? biot::MODE_P1_FUSED : biot::MODE_P1_PASS1;
 }
 
-biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
-    const bool timing = e0 != nullptr;
-    biot_status st = halo_exchange(ctx);
-    if (st != BIOT_OK) return st;
-    const double *xin = ctx->x[ctx->cur];
-    double *xout = ctx->x[1 - ctx->cur];
+// The kernels of one outer iteration from panel `cur` (sweep, P~1 pass 2 if two-pass,
+// norm finalize).  graph_slot >= 0: the finalize writes history slot d_iter + graph_slot
+// (read on the device: replayable in a CUDA graph) and the events are graph nodes.
+biot_status enqueue_iteration(biot_ctx *ctx, int cur, cudaEvent_t e0, cudaEvent_t e1, int graph_slot) {
+    const double *xin = ctx->x[cur];
+    double *xout = ctx->x[1 - cur];
     const int mode = main_mode(ctx);
     biot::SweepArgs a = sweep_args(ctx, mode, xin, xout);
+    const unsigned evf = graph_slot >= 0 ? cudaEventRecordExternal : cudaEventRecordDefault;
     // timed span: every pass of the preconditioner (P~1 two-pass: both)
-    if (timing) CU(cudaEventRecord(e0, ctx->stream));
+    if (e0) CU(cudaEventRecordWithFlags(e0, ctx->stream, evf));
     CU(launch_main(ctx, mode, xin, xout));
     if (mode == biot::MODE_P1_PASS1) CU(launch_pass2_any(ctx, xin, xout, a.sendbuf, nullptr));
-    if (timing) CU(cudaEventRecord(e1, ctx->stream));
-    double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
-    CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, hslot, ctx->nonfinite,
-                             ctx->fin_scratch, ctx->stream));
+    if (e1) CU(cudaEventRecordWithFlags(e1, ctx->stream, evf));
+    if (graph_slot >= 0) {
+        CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, ctx->hist, ctx->nonfinite,
+                                 ctx->fin_scratch, ctx->stream, ctx->d_iter, graph_slot, ctx->hist_cap));
+    } else {
+        double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
+        CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, hslot, ctx->nonfinite,
+                                 ctx->fin_scratch, ctx->stream));
+    }
+    return BIOT_OK;
+}
+
+biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
+    biot_status st = halo_exchange(ctx);
+    if (st != BIOT_OK) return st;
+    if ((st = enqueue_iteration(ctx, ctx->cur, e0, e1, -1)) != BIOT_OK) return st;
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
     if (ctx->world > 1) ctx->send_dirty = false;   // the sweep (and pass 2) wrote the slice of x^{k+1}
     return BIOT_OK;
+}
+
+// Capture two outer iterations starting from panel `cur` (ending on it again) and the
+// history-counter advance into an executable graph.  Capture runs on a private stream
+// (the context's stream may be the legacy default stream, which cannot capture).
+biot_status build_graph(biot_ctx *ctx, int cur) {
+    if (!ctx->cap_stream) CU(cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking));
+    for (cudaEvent_t &e : ctx->gev)
+        if (!e) CU(cudaEventCreate(&e));
+    cudaStream_t saved = ctx->stream;
+    ctx->stream = ctx->cap_stream;
+    cudaError_t e = cudaStreamBeginCapture(ctx->cap_stream, cudaStreamCaptureModeRelaxed);
+    biot_status st = BIOT_OK;
+    if (e == cudaSuccess) {
+        st = enqueue_iteration(ctx, cur, ctx->gev[0], ctx->gev[1], 0);
+        if (st == BIOT_OK) st = enqueue_iteration(ctx, 1 - cur, ctx->gev[2], ctx->gev[3], 1);
+        if (st == BIOT_OK) {
+            cudaError_t e2 = biot::launch_counter(ctx->d_iter, 2, true, ctx->cap_stream);
+            if (e2 != cudaSuccess) st = fail(ctx, BIOT_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e2));
+        }
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e3 = cudaStreamEndCapture(ctx->cap_stream, &g);
+    ctx->stream = saved;
+    if (e != cudaSuccess) return fail(ctx, BIOT_E_CUDA, std::string("cudaStreamBeginCapture: ") + cudaGetErrorString(e));
+    if (st != BIOT_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+    }
+    if (e3 != cudaSuccess) return fail(ctx, BIOT_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e3));
+    e = cudaGraphInstantiate(&ctx->gexec[cur], g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(ctx, BIOT_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    return BIOT_OK;
+}
+
+// Wait for event `ev` on the host.  With an NCCL communicator, poll its asynchronous
+// error state meanwhile: a failed or silent peer (no progress for nccl_timeout_s) aborts
+// the communicator and returns BIOT_E_NCCL instead of hanging.
+biot_status wait_done(biot_ctx *ctx, cudaEvent_t ev) {
+    NcclApi *api = ctx->comm ? nccl() : nullptr;
+    if (!api || !api->CommGetAsyncError) {
+        CU(cudaEventSynchronize(ev));
+        return BIOT_OK;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return BIOT_OK;
+        if (q != cudaErrorNotReady) return fail(ctx, BIOT_E_CUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(q));
+        ncclResult_t ar = ncclSuccess;
+        api->CommGetAsyncError(ctx->comm, &ar);
+        const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if ((ar != ncclSuccess && ar != ncclInProgress) || el > ctx->nccl_timeout_s) {
+            if (api->CommAbort) api->CommAbort(ctx->comm);
+            ctx->comm = nullptr;
+            return fail(ctx, BIOT_E_NCCL, ar != ncclSuccess && ar != ncclInProgress
+                                              ? std::string("NCCL asynchronous error: ") +
+                                                    (api->GetErrorString ? api->GetErrorString(ar) : "?")
+                                              : "NCCL halo exchange made no progress within BIOT_NCCL_TIMEOUT_S (" +
+                                                    std::to_string(ctx->nccl_timeout_s) + " s): communicator aborted");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+}
+
+biot_status wait_stream(biot_ctx *ctx) {
+    CU(cudaEventRecord(ctx->ev_b, ctx->stream));
+    return wait_done(ctx, ctx->ev_b);
 }
 
 }  // namespace
@@ -1115,17 +1204,11 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     {
         const char *kenv = std::getenv("BIOT_KERNEL");
         const bool force_generic = kenv && std::string(kenv) == "generic";
-        if (const char *e = std::getenv("BIOT_STENCIL_R")) ctx->sR = std::atoi(e);
-        else ctx->sR = ctx->d == 2 ? 4 : 2;
-        if (const char *e = std::getenv("BIOT_STENCIL_T")) ctx->sT = std::atoi(e);
-        else ctx->sT = 2;
         ctx->stencil = detect_stencil(ctx);
         if (const char *e = std::getenv("BIOT_MARCH_T")) ctx->mT = std::atoi(e);
         std::string want = kenv ? std::string(kenv) : std::string();
         if (force_generic || !ctx->stencil) {
             ctx->kern = 1;
-        } else if (want == "stencil") {
-            ctx->kern = biot::stencil_supported(ctx->d, ctx->sR, ctx->sT) ? 2 : 1;
         } else if (ctx->d == 2) {
             ctx->row_w = -ctx->gbase[0];              // W
             ctx->n_rows = (int32_t)(ctx->N / ctx->row_w);
@@ -1156,8 +1239,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const char *tp = std::getenv("BIOT_P1_TWOPASS");
         ctx->p1_fused = ctx->precond == 1 && !(tp && std::atoi(tp) == 1);
     }
-    const int64_t chunk = ctx->kern == 2 ? 32 * ctx->sT
-                        : ctx->kern == 3 ? 32 * ctx->mT
+    const int64_t chunk = ctx->kern == 3 ? 32 * ctx->mT
                         : ctx->kern == 4 ? biot::tile2d_chunk()
                         : ctx->kern == 6 ? biot::tile3d_chunk()
                                          : biot::kChunk;
@@ -1174,6 +1256,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     }
     CU(cudaEventCreate(&ctx->ev_a));
     CU(cudaEventCreate(&ctx->ev_b));
+    ALLOC(ctx->d_iter, sizeof(int64_t));
+    ctx->use_graph = !(opts->flags & BIOT_FLAG_NO_GRAPH) && (opts->world == 1 || (opts->flags & BIOT_FLAG_MANUAL_HALO));
+    if (const char *e = std::getenv("BIOT_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(1.0, std::atof(e));
 
     const int nc = ctx->nc;
     const int W = biot::block_width(nc);
@@ -1243,10 +1328,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
 
     const int nwp = 8 / ctx->tw;
     ctx->shape.smem = (size_t)nwp * (nchunks * chunk) * 2 * sizeof(double);
-    if (ctx->kern == 2) {
-        CU(biot::stencil_shape(ctx->d, ctx->sR, ctx->sT, ctx->device, &ctx->shape));
-        ctx->groups = ctx->shape.grid;
-    } else if (ctx->kern == 3) {
+    if (ctx->kern == 3) {
         CU(biot::march_shape(ctx->mT, ctx->device, &ctx->shape));
         // rows per tile: enough tiles for ~8 waves, at least 16 rows per tile
         const int64_t n_seg = (ctx->row_w + 7) / 8;
@@ -1550,28 +1632,55 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
     if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
     if (K == 0) return BIOT_OK;
     CU(cudaSetDevice(ctx->device));
-    while ((int32_t)ctx->ev_s.size() < 2 * K) {
+    // pairs of iterations replay the context's CUDA graph (no NCCL inside: world == 1 or
+    // manual halo); an odd remainder, and every NCCL iteration, launches directly
+    const int32_t pairs = ctx->use_graph ? K / 2 : 0;
+    const int32_t eager = K - 2 * pairs;
+    if (pairs > 0 && !ctx->gexec[ctx->cur]) {
+        biot_status s = build_graph(ctx, ctx->cur);
+        if (s != BIOT_OK) return s;
+    }
+    while ((int32_t)ctx->ev_s.size() < 2 * eager) {
         cudaEvent_t e;
         CU(cudaEventCreate(&e));
         ctx->ev_s.push_back(e);
     }
     CU(cudaEventRecord(ctx->ev_a, ctx->stream));
-    for (int32_t k = 0; k < K; ++k) {
+    if (pairs > 0) {
+        CU(biot::launch_counter(ctx->d_iter, ctx->iterations, false, ctx->stream));
+        for (int32_t k = 0; k < pairs; ++k) CU(cudaGraphLaunch(ctx->gexec[ctx->cur], ctx->stream));
+        ctx->iterations += 2 * pairs;
+    }
+    for (int32_t k = 0; k < eager; ++k) {
         biot_status s = one_iteration(ctx, ctx->ev_s[2 * k], ctx->ev_s[2 * k + 1]);
         if (s != BIOT_OK) return s;
     }
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
-    CU(cudaEventSynchronize(ctx->ev_b));
+    {
+        biot_status s = wait_done(ctx, ctx->ev_b);
+        if (s != BIOT_OK) return s;
+    }
     float tot = 0.f;
     CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
+    // preconditioner-pass time per iteration: every direct launch, and (graph) the two
+    // iterations of the last replay
     double sweep_ms = 0.0;
-    for (int32_t k = 0; k < K; ++k) {
+    int spans = 0;
+    for (int32_t k = 0; k < eager; ++k) {
         float ms = 0.f;
         CU(cudaEventElapsedTime(&ms, ctx->ev_s[2 * k], ctx->ev_s[2 * k + 1]));
         sweep_ms += ms;
+        ++spans;
     }
+    if (pairs > 0)
+        for (int h = 0; h < 2; ++h) {
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ctx->gev[2 * h], ctx->gev[2 * h + 1]));
+            sweep_ms += ms;
+            ++spans;
+        }
     ctx->last_ms_iter = tot / K;
-    ctx->last_ms_sweep = sweep_ms / K;
+    ctx->last_ms_sweep = sweep_ms / spans;
     int nf = 0;
     CU(cudaMemcpyAsync(&nf, ctx->nonfinite, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -1694,7 +1803,10 @@ biot_status biot_gs_end(biot_ctx *ctx) {
     biot_status st = gs_parity_copy(ctx, ctx->x[1 - ctx->cur], ctx->x[ctx->cur], 1);
     if (st != BIOT_OK) return st;
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
-    CU(cudaEventSynchronize(ctx->ev_b));
+    {
+        biot_status ws = wait_done(ctx, ctx->ev_b);
+        if (ws != BIOT_OK) return ws;
+    }
     float tot = 0.f;
     CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
     ctx->last_ms_iter = tot / K;
@@ -1760,7 +1872,10 @@ biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
         ctx->iterations++;
     }
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
-    CU(cudaEventSynchronize(ctx->ev_b));
+    {
+        biot_status ws = wait_done(ctx, ctx->ev_b);
+        if (ws != BIOT_OK) return ws;
+    }
     float tot = 0.f;
     CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
     ctx->last_ms_iter = tot / K;
@@ -1908,7 +2023,10 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
         if (ctx->world > 1) ctx->send_dirty = false;
     }
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
-    CU(cudaEventSynchronize(ctx->ev_b));
+    {
+        biot_status ws = wait_done(ctx, ctx->ev_b);
+        if (ws != BIOT_OK) return ws;
+    }
     float tot = 0.f;
     CU(cudaEventElapsedTime(&tot, ctx->ev_a, ctx->ev_b));
     ctx->last_ms_iter = tot / K;
@@ -1931,7 +2049,7 @@ biot_status biot_residual_norms(biot_ctx *ctx, double *out) {
                              ctx->fin_scratch, ctx->stream));
     CU(cudaMemcpyAsync(out, ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    return wait_stream(ctx);
     return BIOT_OK;
 }
 
@@ -2011,7 +2129,7 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->n_t_local = ctx->n_tl;
     o->first_step = ctx->first_step;
     o->iterations = ctx->iterations;
-    o->kernel_path = ctx->kern == 1 ? ctx->path : ctx->kern + 1;   // 3 stencil, 4 march, 5 tile2d, 7 tile3d
+    o->kernel_path = ctx->kern == 1 ? ctx->path : ctx->kern + 1;   // 4 march, 5 tile2d, 7 tile3d
     o->n_slots = ctx->S;
     o->beta = ctx->beta;
     const double st = (double)ctx->N * ctx->nc * ctx->n_tl;
@@ -2022,6 +2140,9 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->launches_per_iter = 1 + (mm == biot::MODE_P1_PASS1 ? 1 : 0) +
                            (biot::finalize_scratch_doubles((int)groups_of(ctx, mm), ctx->n_tl) > 0 ? 2 : 1);
     o->interior_nodes = (int32_t)ctx->n_interior;
+    o->comm_nranks = 0;
+    if (ctx->comm && nccl() && nccl()->CommCount) nccl()->CommCount(ctx->comm, &o->comm_nranks);
+    o->graph = ctx->use_graph ? 1 : 0;
     return BIOT_OK;
 }
 

@@ -128,8 +128,12 @@ __global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
 
 // Deterministic second stage of the norm reduction: fixed split of the groups
 // over 8 y-lanes, then a fixed-order sum of the 8 lane totals.
+// norms: the output, or -- slot_ctr != null (CUDA-graph replays) -- the residual-history
+// ring, slot (*slot_ctr + slot_off) % cap of n_tl x 2 doubles
 __global__ void finalize_kernel(const double *__restrict__ partial, int groups, int n_tl,
-                                double *__restrict__ norms, int *nonfinite) {
+                                double *__restrict__ norms, int *nonfinite, const int64_t *slot_ctr,
+                                int64_t slot_off, int cap) {
+    if (slot_ctr) norms += ((*slot_ctr + slot_off) % cap) * (int64_t)n_tl * 2;
     __shared__ double sm[8][32][2];
     const int t = blockIdx.x * 32 + threadIdx.x;
     const int y = threadIdx.y;
@@ -302,8 +306,19 @@ int64_t finalize_scratch_doubles(int groups, int n_tl) {
     return groups > 2 * kGch ? (int64_t)((groups + kGch - 1) / kGch) * n_tl * 2 : 0;
 }
 
+__global__ void advance_kernel(int64_t *ctr, int64_t value, int add) {
+    if (add) *ctr += value;
+    else *ctr = value;
+}
+
+cudaError_t launch_counter(int64_t *ctr, int64_t value, bool add, cudaStream_t st) {
+    advance_kernel<<<1, 1, 0, st>>>(ctr, value, add ? 1 : 0);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
-                            int *nonfinite, double *scratch, cudaStream_t st) {
+                            int *nonfinite, double *scratch, cudaStream_t st, const int64_t *slot_ctr,
+                            int64_t slot_off, int cap) {
     dim3 block(32, 8);
     if (groups > 2 * kGch) {   // two fixed-order stages: many groups would serialise one pass
         const int g1 = (groups + kGch - 1) / kGch;
@@ -311,7 +326,8 @@ cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double 
         partial = scratch;
         groups = g1;
     }
-    finalize_kernel<<<dim3((n_tl + 31) / 32), block, 0, st>>>(partial, groups, n_tl, norms, nonfinite);
+    finalize_kernel<<<dim3((n_tl + 31) / 32), block, 0, st>>>(partial, groups, n_tl, norms, nonfinite, slot_ctr,
+                                                              slot_off, cap);
     return cudaGetLastError();
 }
 

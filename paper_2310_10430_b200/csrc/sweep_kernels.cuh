@@ -67,13 +67,6 @@ struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_
     int64_t off[32];
 };
 
-// Arguments of the register-blocked structured-stencil sweep (stencil_kernels.cu).
-struct StencilArgs : SweepArgs {
-    template <int D>
-    static constexpr int kBlockPitch = D == 2 ? 10 : 18;   // (d+1)^2 + 1, padded to 16 B
-    int64_t gbase[8];       // base offset of each run of consecutive column offsets
-    int32_t slot[8][3];     // BDIA slot of (run g, offset a - amin(g))
-};
 
 // Arguments of the TMA-pipelined 2D tile kernel (tile2d_kernels.cu).
 struct Tile2dArgs : SweepArgs {
@@ -201,15 +194,16 @@ cudaError_t launch_cheb_step(int dim, int path, int n_slots, const ChebArgs &a, 
 // update), and x_u^{k+1} = x_u + omega z_u
 cudaError_t launch_cheb_p1_rhs(int dim, int path, int n_slots, const ChebArgs &a, cudaStream_t st);
 
-bool stencil_supported(int dim, int R, int T);
-cudaError_t stencil_shape(int dim, int R, int T, int device, LaunchShape *out);
-cudaError_t launch_stencil(int dim, int R, int T, const StencilArgs &a, const LaunchShape &sh,
-                           cudaStream_t st);
 // scratch: finalize_scratch_doubles(groups, n_tl) doubles (two-stage reduction when
 // there are many groups; both stages in a fixed order, so the result is deterministic)
 int64_t finalize_scratch_doubles(int groups, int n_tl);
+// slot_ctr != null: norms is the history ring [cap][n_tl][2], written at slot
+// (*slot_ctr + slot_off) % cap read on the device (so a captured CUDA graph can be replayed)
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
-                            int *nonfinite, double *scratch, cudaStream_t st);
+                            int *nonfinite, double *scratch, cudaStream_t st, const int64_t *slot_ctr = nullptr,
+                            int64_t slot_off = 0, int cap = 1);
+// *ctr = value (add = false) or *ctr += value, on the stream
+cudaError_t launch_counter(int64_t *ctr, int64_t value, bool add, cudaStream_t st);
 // Gauss-Seidel wave: the window's steps t = lo..lo+len-1 carry iteration k = k0 - t;
 // norms of t >= t_first go to hist[(k % cap) * n_tl + t] (the residual-history ring)
 cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int lo, int t_first, int64_t k0,

@@ -7,21 +7,24 @@
 // The 2D path is HBM-bound (~88 FMAs per node and step against 48 bytes of x
 // traffic), so the kernel is built to stream the space-time panel once with as
 // few instructions per byte as possible:
-//  * work tile = SEG = 15 consecutive grid columns x a range of grid rows, for
+//  * work tile = kSeg = 12 consecutive grid columns x a range of grid rows, for
 //    every 128-step time chunk in turn (4 steps per lane: steps 2l, 2l+1 and
 //    64+2l, 64+2l+1, so each 16-B shared-memory load of the warp is one contiguous
 //    512-B run -- conflict-free; every coefficient and every loop/barrier
 //    instruction serves 4 steps);
-//  * a producer warp streams each grid row's strip (17 nodes x 3 comps x 128
-//    steps, one TMA tensor box, no time halo) and the 15 nodes' aux records
-//    (kappa-dependent AA_pp per slot, load, preconditioner diagonals, path flag)
-//    into a 4-stage ring;
-//  * 15 consumer warps (one column each) march the rows holding only two rows:
+//  * one lane of a producer warpgroup streams each grid row's strip (14 nodes x 3
+//    comps x 128 steps, one TMA tensor box, no time halo) and the 12 nodes' aux
+//    records (kappa-dependent AA_pp per slot, load, preconditioner diagonals, path
+//    flag) into a 5-stage ring (full/empty mbarriers); the producer warpgroup hands
+//    its registers to the consumers (setmaxnreg 24 / 160);
+//  * 12 consumer warps (one column each) march the rows holding only two rows:
 //    at step m (rows m-1, m resident) a warp finishes its node of row m-1 (the
 //    +W slots, then the epilogue) and starts its node of row m (-W and 0 slots);
 //  * interior nodes share one stencil (kernel parameters, uniform-register
 //    operands, structural zeros skipped); edge/corner nodes use the stencil of
 //    their geometric class (9 classes, shared memory).
+//  * P~1 in one pass (tile2d_p1_kernel below): 10 owned columns per tile, z_u
+//    recomputed on a one-node halo, the pressure update lagged one row.
 //
 // Previous-step coupling (A' x_{n-1})_p: lane l uses q(t-1) of lane l-1 (one
 // shuffle); lane 0 takes q(t0-1) from a shared-memory carry written by lane 31
@@ -433,7 +436,8 @@ struct Geo2 {
 __device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); }
 
 // Block = 3 consumer warpgroups + 1 producer warpgroup (only its first lane issues
-// copies); the producer group hands its registers to the consumers (setmaxnreg).
+// copies); the producer group hands its registers to the consumers (setmaxnreg:
+// 4 x 32 x 24 + 12 x 32 x 160 <= 65536).
 constexpr int kThreads2 = (kSeg + 4) * 32;
 constexpr int kProducerRegs = 24, kConsumerRegs = 160;
 
@@ -656,37 +660,41 @@ constexpr uint32_t kSmemBytes = cmax(cmax(Lay<1>::kSmemBytes, Lay<kMaxLoads>::kS
                                      cmax(LayP1<1>::kSmemBytes, LayP1<kMaxLoads>::kSmemBytes));
 static_assert(kSmemBytes <= 232448 - 128, "tile2d shared memory exceeds 227 KB");
 
-// B^T contributions of one published z_u row to the node at row delta -DR from it: the
-// node's slots of row delta DR, in column order (dc = -1, 0, +1), components u_x, u_y.
-template <int DR, bool CLS, bool S0, class A>
-__device__ __forceinline__ void bt_row(const A &a, const double *zrow, int p, int lane, const double *T,
-                                       double (&bt)[kT2]) {
-#pragma unroll
-    for (int dc = -1; dc <= 1; ++dc) {
-        const int s = slot2(DR, dc);
-        if (s < 0) continue;
+// B^T contribution of the z_u column at position p + DC of a published row to a node
+// whose row delta to that row is DR (its slot (DR, DC)), both displacement components.
+template <int DR, int DC, bool CLS, bool S0, class A>
+__device__ __forceinline__ void bt_col(const A &a, const double (&z)[2][kT2], const double *T, double (&bt)[kT2]) {
+    constexpr int s = slot2(DR, DC);
+    if constexpr (s >= 0) {
 #pragma unroll
         for (int cc = 0; cc < 2; ++cc) {
             if constexpr (!CLS) {
                 if (tmpl_zero(s, 6 + cc, S0)) continue;
             }
             const double cf = CLS ? T[s * kCW + cc * 3 + 2] : a.tmpl[s][6 + cc];
-            const double *src = zrow + ((p + dc - 1) * 2 + cc) * kCT + lane * 2;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const double2 w = *reinterpret_cast<const double2 *>(src + h * (kCT / 2));
-                bt[2 * h] = fma(cf, w.x, bt[2 * h]);
-                bt[2 * h + 1] = fma(cf, w.y, bt[2 * h + 1]);
-            }
+            for (int tt = 0; tt < kT2; ++tt) bt[tt] = fma(cf, z[cc][tt], bt[tt]);
         }
     }
 }
 
-template <int DR, bool S0, class A>
-__device__ __forceinline__ void bt_row_any(const A &a, const double *zrow, int p, int lane, int kind,
-                                           const double *T, double (&bt)[kT2]) {
-    if (kind == 1) bt_row<DR, false, S0, A>(a, zrow, p, lane, T, bt);
-    else bt_row<DR, true, S0, A>(a, zrow, p, lane, T, bt);
+template <int DR, int DC, bool S0, class A>
+__device__ __forceinline__ void bt_col_any(const A &a, int kind, const double (&z)[2][kT2], const double *T,
+                                           double (&bt)[kT2]) {
+    if (kind == 1) bt_col<DR, DC, false, S0, A>(a, z, T, bt);
+    else if (kind == 2) bt_col<DR, DC, true, S0, A>(a, z, T, bt);
+}
+
+__device__ __forceinline__ void load_z(double (&z)[2][kT2], const double *zrow, int pos, int lane) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const double2 w = *reinterpret_cast<const double2 *>(zrow + ((pos - 1) * 2 + c) * kCT + lane * 2 +
+                                                                 h * (kCT / 2));
+            z[c][2 * h] = w.x;
+            z[c][2 * h + 1] = w.y;
+        }
 }
 
 // Finish node (m-1) of the fused pass: the +W slots, the residual epilogue (norms of
@@ -697,7 +705,8 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
                                           const double *aux, const double *T, int64_t i, int t0, bool ghost,
                                           bool whole, bool own, double *carry, const double (&sv)[kT2],
                                           double (&acc)[3][kT2], double (&q)[kT2], double (&nu)[kT2],
-                                          double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2]) {
+                                          double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2],
+                                          double (&zo)[2][kT2]) {
     accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
     if constexpr (NL > 1) {
 #pragma unroll
@@ -748,8 +757,11 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
         // z_u published for the neighbours; the pressure part waits for B^T z_u:
         // x_p^{k+1} = x_p + omega D_S^{-1} (bt - r_p) = y + (omega D_S^{-1}) bt
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int c = 0; c < 2; ++c) {
             *reinterpret_cast<double2 *>(zd + c * kCT + h * (kCT / 2)) = make_double2(outz[c][0], outz[c][1]);
+            zo[c][2 * h] = outz[c][0];
+            zo[c][2 * h + 1] = outz[c][1];
+        }
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) y[2 * h + tt] = fma(-wdv, outz[2][tt], xs2[2][tt]);
         if (own) {
@@ -815,6 +827,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     constexpr uint32_t kAuxBytes = L::kAuxBytes, kStageBytes = L::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
+    __shared__ uint64_t zbar[2];                                         // z_u row published (per buffer)
     double *zbuf = reinterpret_cast<double *>(smem + L::kZOff);          // [2][12][2][kCT]
     double *qcarry = reinterpret_cast<double *>(smem + L::kCarryOff);    // [kMaxRR + 1][kSeg]
 
@@ -828,6 +841,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kSeg);
         }
+        mbar_init(&zbar[0], kSeg * 32);
+        mbar_init(&zbar[1], kSeg * 32);
         fence_barrier_init();
     }
     __syncthreads();
@@ -862,6 +877,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int p = warp + 1;                   // strip position: 1..12, owned 2..11
     const double *const cls_base = a.cls;     // class stencils (boundary nodes) from global memory
     uint32_t it = 0;
+    uint32_t zph[2] = {0u, 0u};               // phase of each z_u barrier
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int i0 = (tile % nseg) * kSegP1, ja = (tile / nseg) * rr, jb = min(nrows, ja + rr);
         const int col = i0 + p - 2;
@@ -913,6 +929,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 double *zrow = zbuf + (size_t)((m - 1) & 1) * (kSeg * 2 * kCT);
                 const bool orow1 = m - 1 >= ja && m - 1 < jb;       // node m-1 owned (row)
                 // (1) finish node m-1 and publish its z_u (zero off the mesh)
+                double zo[2][kT2];                       // this column's z_u of row m-1 (registers)
+#pragma unroll
+                for (int tt = 0; tt < kT2; ++tt) zo[0][tt] = zo[1][tt] = 0.0;
                 if (m >= ja) {
                     double *zd = zrow + (p - 1) * 2 * kCT + lane * 2;
                     if (kindP != 0) {
@@ -924,10 +943,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         wB = a.omega * aux[12];
                         if (kindP == 1)
                             finish_p1<false, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB, zo);
                         else
                             finish_p1<true, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB, zo);
                     } else {
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
@@ -938,32 +957,49 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 kindB = (orow1 && ocol) ? kindP : 0;
                 kindP = 0;
-                // (2) every z_u of row m-1 is published
-                named_barrier_sync(1, kSeg * 32);
-                // (3) B^T contributions of row m-1's z_u: node m-2 (its +W slots; then complete),
-                // node m-1 (0 slots), node m (-W slots)
+                // (2) this thread's z_u of row m-1 is published (the chunk's first row step
+                // instead fences the z buffers against the previous chunk's last reads)
+                const int zb = (m - 1) & 1;
+                if (m >= ja) mbar_arrive(&zbar[zb]);
+                else named_barrier_sync(1, kSeg * 32);
+                // (3) start node m (z rows ja-1..jb on the mesh): independent of the z_u
+                // exchange, so it overlaps the other warps' publishing
                 int kindC = 0;
-                if (m <= jb && valid) {
-                    const double *auxm = reinterpret_cast<const double *>(
-                                             reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
-                    if (m >= 0 && m < nrows) kindC = auxm[13] == 1.0 ? 1 : 2;
+                if (m <= jb && valid && m >= 0 && m < nrows) {
+                    const double *aux = reinterpret_cast<const double *>(
+                                            reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                    kindC = aux[13] == 1.0 ? 1 : 2;
+                    kindP = kindC;
+                    if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
+                    if (kindP == 1) start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
+                    else start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                 }
+                // (4) every z_u of row m-1 published: B^T contributions of row m-1's z_u to
+                // node m-2 (its +W slots; then complete), node m-1 (0 slots), node m (-W slots)
                 if (m >= ja) {
-                    if (kindA != 0) {
-                        const double *TA = cls_base + (ccx + 3 * axis_class(m - 2, nrows)) * 7 * kCW;
-                        bt_row_any<1, S0, Tile2dArgs>(a, zrow, p, lane, kindA, TA, btA);
-                        finish_zp<Tile2dArgs>(a, (int64_t)(m - 2) * W + col, t0, whole, wA, btA, yA);
-                    }
-                    if (kindB != 0) {
-                        const double *TB = cls_base + (ccx + 3 * axis_class(m - 1, nrows)) * 7 * kCW;
-                        bt_row_any<0, S0, Tile2dArgs>(a, zrow, p, lane, kindB, TB, btB);
-                    }
-                    if (kindC != 0 && m >= ja && m < jb && ocol) {
-                        const double *TC = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
-#pragma unroll
-                        for (int tt = 0; tt < kT2; ++tt) btC[tt] = 0.0;
-                        bt_row_any<-1, S0, Tile2dArgs>(a, zrow, p, lane, kindC, TC, btC);
-                    }
+                    mbar_wait(&zbar[zb], zph[zb]);
+                    zph[zb] ^= 1u;
+                }
+                if (m >= ja && ocol) {
+                    // the z_u columns p-1, p (registers), p+1, each read once and applied to
+                    // every node of this column that uses it, in ascending column order per node
+                    // (node m-2: slots (+1, 0), (+1, +1); node m-1: (0, -1), (0, 0), (0, +1);
+                    // node m: (-1, -1), (-1, 0))
+                    const int kC = (kindC != 0 && m < jb) ? kindC : 0;
+                    const double *TA = cls_base + (ccx + 3 * axis_class(m - 2, nrows)) * 7 * kCW;
+                    const double *TB = cls_base + (ccx + 3 * axis_class(m - 1, nrows)) * 7 * kCW;
+                    const double *TC = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
+                    double zn[2][kT2];
+                    load_z(zn, zrow, p - 1, lane);
+                    bt_col_any<0, -1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
+                    bt_col_any<-1, -1, S0, Tile2dArgs>(a, kC, zn, TC, btC);
+                    bt_col_any<1, 0, S0, Tile2dArgs>(a, kindA, zo, TA, btA);
+                    bt_col_any<0, 0, S0, Tile2dArgs>(a, kindB, zo, TB, btB);
+                    bt_col_any<-1, 0, S0, Tile2dArgs>(a, kC, zo, TC, btC);
+                    load_z(zn, zrow, p + 1, lane);
+                    bt_col_any<1, 1, S0, Tile2dArgs>(a, kindA, zn, TA, btA);
+                    bt_col_any<0, 1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
+                    if (kindA != 0) finish_zp<Tile2dArgs>(a, (int64_t)(m - 2) * W + col, t0, whole, wA, btA, yA);
                 }
                 // rotate the pending rows: m-1 -> A, m -> B
                 kindA = kindB;
@@ -974,15 +1010,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     yA[tt] = yB[tt];
                     btB[tt] = btC[tt];
                     btC[tt] = 0.0;
-                }
-                // (4) start node m (z rows ja-1..jb on the mesh)
-                if (m <= jb && kindC != 0) {
-                    const double *aux = reinterpret_cast<const double *>(
-                                            reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
-                    kindP = kindC;
-                    if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
-                    if (kindP == 1) start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
-                    else start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[sd]);   // row m-1 no longer needed

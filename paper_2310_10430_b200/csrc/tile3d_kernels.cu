@@ -8,20 +8,20 @@
 // x traffic), so the design goal is to keep the FP64 pipe busy: the operator is
 // not streamed per node but held as stencils -- the interior one in the kernel
 // parameters (uniform-register operands, structural zeros skipped), the face /
-// edge / corner ones (geometric classes) in shared memory -- the x values come
-// from shared memory staged by TMA, and each consumer warp computes two
-// x-adjacent nodes so one shared-memory load feeds up to 10 FMAs.
+// edge / corner ones (geometric classes) in shared memory -- and the x values come
+// from shared memory staged by TMA.
 //
 // Work tile = a 4x4 (x, y) node patch x a z range, for every 32-step time chunk
-// (lane = one step).  A producer warp streams, per z plane, one 4D TMA box
-// {32 steps, 6 x-nodes x 4 comps, 6 y-rows, 1 plane} (patch + halo; out-of-mesh
-// positions are zero-filled) and the 16 patch nodes' aux records (kappa-dependent
-// AA_pp per slot, load, preconditioner diagonals, path flag) into a 5-stage ring.
-// The 8 consumer warps march z holding only two planes: at step m (planes m-1, m
-// resident) a warp finishes its nodes of plane m-1 (the z+1 columns, from plane
-// m, then the epilogue) and starts its nodes of plane m (z-1 and z columns); the
-// partial sums ride in registers.  Every node's FMAs run in the fixed
-// (dz, dy, dx) column order.
+// (lane = one step).  One lane of a producer warpgroup streams, per z plane, one
+// 4D TMA box {32 steps, 6 x-nodes x 4 comps, 6 y-rows, 1 plane} (patch + halo;
+// out-of-mesh positions are zero-filled) and the 16 patch nodes' aux records
+// (kappa-dependent AA_pp per slot, load, preconditioner diagonals, path flag) into
+// a 5-stage ring.  16 consumer warps (one node each, R = 1) march z holding only
+// two planes: at step m (planes m-1, m resident) a warp finishes its node of plane
+// m-1 (the z+1 columns, from plane m, then the epilogue) and starts its node of
+// plane m (z-1 and z columns); the partial sums ride in registers.  Every node's
+// FMAs run in the fixed (dz, dy, dx) column order.  (R = 2, two x-adjacent nodes
+// per warp, is kept as a template option; measured slower, see kConsumersOf.)
 //
 // Previous-step coupling (A' x_{n-1})_p: lane l uses q(t-1) of lane l-1 (one
 // shuffle); lane 0 takes q(t0-1) from a shared-memory carry written by lane 31

@@ -23,14 +23,16 @@ def slab(n_t: int, world: int, rank: int):
     return rank * n_tl + 1, n_tl
 
 
-def broadcast_nccl_id(make_id, group=None, src: int = 0) -> bytes:
-    """Rank `src` calls make_id() -> 128 bytes; every rank returns the same bytes."""
+def broadcast_nccl_id(make_id, group=None, src: int = 0, device=None) -> bytes:
+    """Rank `src` calls make_id() -> 128 bytes; every rank returns the same bytes.
+    device: where the broadcast buffer lives (a CUDA device for the nccl backend,
+    None = host for gloo)."""
     import torch.distributed as dist
-    buf = torch.zeros(128, dtype=torch.uint8)
+    buf = torch.zeros(128, dtype=torch.uint8, device=device)
     if dist.get_rank(group) == src:
         raw = make_id()
         if len(raw) != 128:
             raise ValueError("ncclUniqueId must be 128 bytes")
         buf.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
     dist.broadcast(buf, src, group=group)
-    return bytes(buf.numpy().tobytes())
+    return bytes(buf.cpu().numpy().tobytes())

@@ -37,9 +37,7 @@ def main():
             if len(f) > 2:
                 os.environ["BIOT_MARCH_ROWS"] = f[2]
         else:
-            r, t = v.split(",")
-            os.environ["BIOT_KERNEL"] = "stencil"
-            os.environ["BIOT_STENCIL_R"], os.environ["BIOT_STENCIL_T"] = r, t
+            raise SystemExit(f"unknown variant {v}")
         for pc in (2, 1):
             if os.environ.get("BIOT_TILE_DRY") and pc == 1:
                 continue
