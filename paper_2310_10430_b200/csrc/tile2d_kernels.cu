@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 // (4) every z_u of row m-1 published: B^T contributions of row m-1's z_u to
                 // node m-2 (its +W slots; then complete), node m-1 (0 slots), node m (-W slots)
                 if (m >= ja) {
-                    mbar_wait(&zbar[zb], zph[zb]);
+                    mbar_wait_suspend(&zbar[zb], zph[zb]);
                     zph[zb] ^= 1u;
                 }
                 if (m >= ja && ocol) {
@@ -986,19 +986,32 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     // (node m-2: slots (+1, 0), (+1, +1); node m-1: (0, -1), (0, 0), (0, +1);
                     // node m: (-1, -1), (-1, 0))
                     const int kC = (kindC != 0 && m < jb) ? kindC : 0;
-                    const double *TA = cls_base + (ccx + 3 * axis_class(m - 2, nrows)) * 7 * kCW;
-                    const double *TB = cls_base + (ccx + 3 * axis_class(m - 1, nrows)) * 7 * kCW;
-                    const double *TC = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
                     double zn[2][kT2];
-                    load_z(zn, zrow, p - 1, lane);
-                    bt_col_any<0, -1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
-                    bt_col_any<-1, -1, S0, Tile2dArgs>(a, kC, zn, TC, btC);
-                    bt_col_any<1, 0, S0, Tile2dArgs>(a, kindA, zo, TA, btA);
-                    bt_col_any<0, 0, S0, Tile2dArgs>(a, kindB, zo, TB, btB);
-                    bt_col_any<-1, 0, S0, Tile2dArgs>(a, kC, zo, TC, btC);
-                    load_z(zn, zrow, p + 1, lane);
-                    bt_col_any<1, 1, S0, Tile2dArgs>(a, kindA, zn, TA, btA);
-                    bt_col_any<0, 1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
+                    if (kindA == 1 && kindB == 1 && kC == 1) {
+                        // interior rows (the common case): one template path, no per-node branches
+                        load_z(zn, zrow, p - 1, lane);
+                        bt_col<0, -1, false, S0, Tile2dArgs>(a, zn, cls_base, btB);
+                        bt_col<-1, -1, false, S0, Tile2dArgs>(a, zn, cls_base, btC);
+                        bt_col<1, 0, false, S0, Tile2dArgs>(a, zo, cls_base, btA);
+                        bt_col<0, 0, false, S0, Tile2dArgs>(a, zo, cls_base, btB);
+                        bt_col<-1, 0, false, S0, Tile2dArgs>(a, zo, cls_base, btC);
+                        load_z(zn, zrow, p + 1, lane);
+                        bt_col<1, 1, false, S0, Tile2dArgs>(a, zn, cls_base, btA);
+                        bt_col<0, 1, false, S0, Tile2dArgs>(a, zn, cls_base, btB);
+                    } else {
+                        const double *TA = cls_base + (ccx + 3 * axis_class(m - 2, nrows)) * 7 * kCW;
+                        const double *TB = cls_base + (ccx + 3 * axis_class(m - 1, nrows)) * 7 * kCW;
+                        const double *TC = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;
+                        load_z(zn, zrow, p - 1, lane);
+                        bt_col_any<0, -1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
+                        bt_col_any<-1, -1, S0, Tile2dArgs>(a, kC, zn, TC, btC);
+                        bt_col_any<1, 0, S0, Tile2dArgs>(a, kindA, zo, TA, btA);
+                        bt_col_any<0, 0, S0, Tile2dArgs>(a, kindB, zo, TB, btB);
+                        bt_col_any<-1, 0, S0, Tile2dArgs>(a, kC, zo, TC, btC);
+                        load_z(zn, zrow, p + 1, lane);
+                        bt_col_any<1, 1, S0, Tile2dArgs>(a, kindA, zn, TA, btA);
+                        bt_col_any<0, 1, S0, Tile2dArgs>(a, kindB, zn, TB, btB);
+                    }
                     if (kindA != 0) finish_zp<Tile2dArgs>(a, (int64_t)(m - 2) * W + col, t0, whole, wA, btA, yA);
                 }
                 // rotate the pending rows: m-1 -> A, m -> B
