@@ -238,7 +238,9 @@ def workload_config(args, prob, world):
             "model": f"biot-p1p1-{prob.dim}d", "n_dof": int(prob.n_dof), "n_t": int(prob.n_t),
             "global_batch": int(prob.n_dof * prob.n_t), "seq_len": int(prob.n_t),
             "precond": f"P~{args.precond}", "omega": args.omega, "parallelism": f"time-slab{world}",
-            "l2": f"inputs larger than L2 (x panels {ws_gb:.1f} GB vs 126 MB L2); no flush needed",
+            "l2": (f"inputs larger than L2 (x panels {ws_gb:.1f} GB vs 126 MB L2); no flush needed" if ws_gb > 0.5
+                   else f"x panels {ws_gb * 1e3:.1f} MB fit in the 126 MB L2 (L2-resident small configuration, "
+                        f"not flushed; the metric's configuration is config 3)"),
             "inputs": ("x^0 = 0, x_0 = the §4.1 initial condition, exact §4.1 data" if args.workload == "trig"
                        else "x^0 = 0, s_n = 1 (BJ metric inputs), synthetic mesh/material")}
 

@@ -121,6 +121,9 @@ typedef struct {
 
 #define BIOT_FLAG_MANUAL_HALO 1u     /* world > 1 without NCCL: caller moves the halo with
                                         biot_last_slice / biot_set_ghost (tests, emulation) */
+#define BIOT_FLAG_DEFER_STEP0 4u     /* with MANUAL_HALO, ranks > 0 run the overlapped-halo form
+                                        of biot_iterate (sweep with a zero ghost, then the first
+                                        local step completed from the ghost): tests / emulation  */
 #define BIOT_FLAG_NO_GRAPH    2u     /* biot_iterate launches kernels directly; default: pairs
                                         of iterations replay one captured CUDA graph (world == 1
                                         or MANUAL_HALO; NCCL iterations always launch directly) */
@@ -185,9 +188,10 @@ biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K);
 /* K outer iterations of PAPER.md Algorithm 3 with the per-step solver K = GMRES(k)
  * (the paper's experiments' solver): every step at once runs one GMRES(k) cycle on
  * AA x_n = A' x_{n-1} + f_n (Jacobi in time) from its current iterate, left-
- * preconditioned by the diagonal P~2 (reading R23).  1 <= k <= 16; needs a structured 2D
- * mesh and precond = 2 (BIOT_E_STATE otherwise); allocates k+1 Krylov panels on first
- * use.  The residual history records, per iteration and step, ||b - AA x|| (u, p) at
+ * preconditioned by the context's P~ with diagonal inner inverses (P~2, eq. p2, or P~1,
+ * eq. p1, the paper's choice for §4.1/§4.3; reading R23).  1 <= k <= 16; needs a
+ * structured 2D / 3D mesh (tile kernels; BIOT_E_STATE otherwise); allocates k+1 Krylov
+ * panels on first use.  The residual history records, per iteration and step, ||b - AA x|| (u, p) at
  * the cycle's start.  Collective for world > 1 (one slice per outer iteration). */
 biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k);
 
@@ -202,7 +206,7 @@ biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k);
 biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha);
 
 /* PAPER.md Algorithm 3 literally: Gauss-Seidel in time (b^{n,m} = A' X^{n-1,m} + f^n)
- * with one GMRES(k) cycle per step and sweep (left P~2), run as the wavefront of
+ * with one GMRES(k) cycle per step and sweep (left P~1 or P~2), run as the wavefront of
  * biot_iterate_gs.  Same conditions as biot_iterate_gmres; collective for world > 1.
  * biot_gs_begin_gmres: its wave-level form (k = 0: the Richardson update). */
 biot_status biot_iterate_gs_gmres(biot_ctx *ctx, int32_t K, int32_t k);

@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbiot_pit.so")
+# BIOT_LIB_OVERRIDE: load another build of the library (kernel-variant experiments only)
+LIB_PATH = os.environ.get("BIOT_LIB_OVERRIDE") or os.path.join(HERE, "libbiot_pit.so")
 
 _d = ctypes.POINTER(ctypes.c_double)
 _i32 = ctypes.POINTER(ctypes.c_int32)
@@ -24,6 +25,7 @@ STATUS = {0: "BIOT_OK", 1: "BIOT_E_INVALID", 2: "BIOT_E_NOMEM", 3: "BIOT_E_CUDA"
           4: "BIOT_E_NCCL", 5: "BIOT_E_STATE", 6: "BIOT_E_NONFINITE"}
 FLAG_MANUAL_HALO = 1
 FLAG_NO_GRAPH = 2
+FLAG_DEFER_STEP0 = 4
 
 
 class BiotMesh(ctypes.Structure):

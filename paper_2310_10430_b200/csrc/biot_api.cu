@@ -143,7 +143,19 @@ struct biot_ctx {
     int trac_term = 0;                // s row of the traction term (biot_set_load_scale), -1: none
     int64_t s_pitch = 0;              // doubles between the rows of s
     uint8_t *fixed = nullptr;
-    double *sendbuf = nullptr;
+    double *sendbuf = nullptr;        // the current last slice (what the next exchange sends)
+    double *send_w = nullptr;         // where the sweep writes the new slice (= sendbuf, or the
+                                      // other buffer of the overlapped exchange)
+    // overlapped time-slab halo (world > 1, tile kernels): the exchange of x^k's slice runs on
+    // comm_stream while the sweep runs; ranks > 0 sweep with a zero ghost (ghost_override) and
+    // complete their first local step after the ghost arrived (the step-0 kernels)
+    bool overlap = false, defer0 = false;
+    bool x0_zero = true;              // x_0 = 0 (rank 0's ghost is identically zero)
+    double *sendbuf2 = nullptr, *zero_ghost_base = nullptr, *zero_ghost = nullptr, *zu0 = nullptr, *part0 = nullptr;
+    const double *ghost_override = nullptr;
+    int step0_blocks = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
     double *partial = nullptr;
     double *fin_scratch = nullptr;    // two-stage norm reduction
     double *hist = nullptr, *norms = nullptr;
@@ -248,7 +260,8 @@ void free_all(biot_ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->loadx, (void *)c->dinv, (void *)c->s,
-                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->partial, (void *)c->hist,
+                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->zu0,
+                    (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
                     (void *)c->gm_small, (void *)c->d_iter})
@@ -264,6 +277,9 @@ void free_all(biot_ctx *c) {
     for (cudaGraphExec_t g : c->gexec)
         if (g) cudaGraphExecDestroy(g);
     if (c->cap_stream) cudaStreamDestroy(c->cap_stream);
+    if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+    for (cudaEvent_t e : {c->ev_ready, c->ev_comm})
+        if (e) cudaEventDestroy(e);
     if (c->comm && nccl()) nccl()->CommDestroy(c->comm);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
 }
@@ -281,7 +297,7 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     biot::SweepArgs a{};
     a.x = xin;
     a.xn = xout;
-    a.ghost = c->ghost;
+    a.ghost = c->ghost_override ? c->ghost_override : c->ghost;
     a.blk = c->blk;
     a.cols = c->cols;
     a.load = c->load;
@@ -291,7 +307,7 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.s_pitch = c->s_pitch;
     a.n_load = c->n_load;
     a.zbuf = c->z;
-    a.sendbuf = (c->world > 1 && mode != biot::MODE_RESIDUAL) ? c->sendbuf : nullptr;
+    a.sendbuf = (c->world > 1 && mode != biot::MODE_RESIDUAL) ? c->send_w : nullptr;
     a.partial = c->partial;
     a.n_nodes = c->N;
     a.pitch = c->pitch;
@@ -304,6 +320,8 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.row_w = c->row_w;
     a.n_rows = c->n_rows;
     a.rows_per_tile = c->rows_per_tile;
+    a.ghost_zero = (c->ghost_override && c->ghost_override == c->zero_ghost) || (c->rank == 0 && c->x0_zero) ? 1 : 0;
+    a.p1_out = (c->precond == 1 && (mode == biot::MODE_ZOUT || mode == biot::MODE_MATVEC)) ? 1 : 0;
     return a;
 }
 
@@ -530,6 +548,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost = win->ghost;
             a.ghost_stride = win->stride;
             a.sendbuf = win->send;
+            if (win->ghost != c->ghost) a.ghost_zero = 0;
         }
         if (zb) a.zbuf = zb;
         if (tmo) return biot::launch_tile3d(*tmo, a, c->shape, c->stream);
@@ -554,6 +573,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost = win->ghost;
             a.ghost_stride = win->stride;
             a.sendbuf = win->send;
+            if (win->ghost != c->ghost) a.ghost_zero = 0;
         }
         a.s0 = c->s0;
         a.dry = c->tile_dry;
@@ -591,6 +611,15 @@ cudaError_t launch_pass2_any(biot_ctx *ctx, const double *xin, double *xout, dou
     return biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream);
 }
 
+// With the overlapped exchange the persistent tile kernels leave BIOT_COMM_SMS (default 2)
+// SMs free, so NCCL's send/recv kernel is scheduled while the sweep runs instead of after it.
+void reserve_comm_sms(biot_ctx *c) {
+    if (!c->overlap && !(c->flags & BIOT_FLAG_DEFER_STEP0)) return;
+    int r = 2;
+    if (const char *e = std::getenv("BIOT_COMM_SMS")) r = std::max(0, std::atoi(e));
+    c->shape.grid = std::max(1, c->shape.grid - r);
+}
+
 // norm-partial groups written by a pass of `mode`
 int64_t groups_of(const biot_ctx *c, int mode) { return mode == biot::MODE_P1_FUSED ? c->groups_p1 : c->groups; }
 
@@ -624,10 +653,84 @@ biot_status enqueue_iteration(biot_ctx *ctx, int cur, cudaEvent_t e0, cudaEvent_
     return BIOT_OK;
 }
 
+// The deferred first local step of the current iterate (after the ghost is in place):
+// recompute it for every node with the ghost, overwrite x^{k+1} there (and the send slice
+// if the slab is one step), and replace the step's norms in history slot `hslot`.
+biot_status complete_step0(biot_ctx *ctx, int mode, const double *xin, double *xout, double *hslot) {
+    if (ctx->kern == 4) {
+        biot::Tile2dArgs a{};
+        static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, xin, xout);
+        a.ghost = ctx->ghost;
+        a.ghost_zero = 0;
+        std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
+        a.aux = ctx->aux;
+        a.cls = ctx->cls;
+        a.pad_nodes = ctx->pad;
+        a.ghost_stride = 1;
+        a.s0 = ctx->s0;
+        CU(biot::launch_tile2d_step0(a, ctx->zu0, ctx->part0, ctx->stream));
+    } else {
+        biot::Tile3dArgs a{};
+        static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, xin, xout);
+        a.ghost = ctx->ghost;
+        a.ghost_zero = 0;
+        std::memcpy(a.tmpl, ctx->tmpl3, sizeof(a.tmpl));
+        a.aux = ctx->aux;
+        a.cls = ctx->cls;
+        a.n1 = ctx->n1;
+        a.z_rows = ctx->z_rows;
+        a.s0 = ctx->s0;
+        a.ghost_stride = 1;
+        CU(biot::launch_tile3d_step0(a, ctx->zu0, ctx->part0, ctx->stream));
+    }
+    CU(biot::launch_finalize(ctx->part0, ctx->step0_blocks, 1, hslot, ctx->nonfinite,
+                             ctx->part0 + 2 * ctx->step0_blocks, ctx->stream));
+    return BIOT_OK;
+}
+
 biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
-    biot_status st = halo_exchange(ctx);
+    biot_status st = BIOT_OK;
+    if (!ctx->overlap) {
+        if ((st = halo_exchange(ctx)) != BIOT_OK) return st;
+    } else {
+        // the exchange of x^k's last slice on the comm stream, concurrent with the sweep,
+        // which writes x^{k+1}'s slice into the other buffer (the compute stream first waits
+        // for the previous exchange: it sent the buffer this sweep overwrites)
+        NcclApi *api = nccl();
+        if (!api || !ctx->comm) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
+        if (ctx->send_dirty) {
+            if ((st = pack_send(ctx)) != BIOT_OK) return st;
+        }
+        CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
+        CU(cudaEventRecord(ctx->ev_ready, ctx->stream));
+        CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_ready, 0));
+        const size_t n = (size_t)ctx->N * ctx->nc;
+        ncclResult_t r = api->GroupStart();
+        if (r == ncclSuccess && ctx->rank + 1 < ctx->world)
+            r = api->Send(ctx->sendbuf, n, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->comm_stream);
+        if (r == ncclSuccess && ctx->rank > 0)
+            r = api->Recv(ctx->ghost, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->comm_stream);
+        ncclResult_t r2 = api->GroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(ctx, BIOT_E_NCCL, std::string("NCCL halo exchange failed: ") +
+                                              (api->GetErrorString ? api->GetErrorString(r != ncclSuccess ? r : r2) : "?"));
+        CU(cudaEventRecord(ctx->ev_comm, ctx->comm_stream));
+        ctx->send_w = ctx->sendbuf2;
+    }
+    const int mode = main_mode(ctx);
+    double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
+    if (ctx->defer0) ctx->ghost_override = ctx->zero_ghost;
+    st = enqueue_iteration(ctx, ctx->cur, e0, e1, -1);
+    ctx->ghost_override = nullptr;
+    if (st == BIOT_OK && ctx->defer0) {
+        if (ctx->overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));   // the ghost arrived
+        st = complete_step0(ctx, mode, ctx->x[ctx->cur], ctx->x[1 - ctx->cur], hslot);
+    }
+    if (ctx->overlap) {
+        std::swap(ctx->sendbuf, ctx->sendbuf2);        // the slice just written is the current one
+        ctx->send_w = ctx->sendbuf;
+    }
     if (st != BIOT_OK) return st;
-    if ((st = enqueue_iteration(ctx, ctx->cur, e0, e1, -1)) != BIOT_OK) return st;
     ctx->cur = 1 - ctx->cur;
     ctx->iterations++;
     if (ctx->world > 1) ctx->send_dirty = false;   // the sweep (and pass 2) wrote the slice of x^{k+1}
@@ -811,14 +914,40 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
     };
     Window w = win;          // tile passes of the cycle never write the send slice
     w.send = nullptr;
+    // P~1 (eq. p1): the tile passes write the first half (z_u, r_p) of P~1^{-1} r; this pass
+    // completes z_p = D_S^{-1} (B^T z_u - r_p) in place on the window's columns of panel V
+    auto p1_complete = [&](double *V) -> cudaError_t {
+        if (ctx->precond != 1) return cudaSuccess;
+        biot::Pass2Args p{};
+        p.x = V;
+        p.xn = V;
+        p.zbuf = V;
+        p.blk = ctx->blk;
+        p.cols = ctx->cols;
+        p.dinv = ctx->dinv;
+        p.sendbuf = nullptr;
+        p.n_nodes = ctx->N;
+        p.pitch = ctx->pitch;
+        p.n_tl = w.len;
+        p.t_off = w.t_off;
+        p.t_lo = w.t_lo;
+        p.tw = ctx->tw;
+        p.node_block = ctx->node_block;
+        p.omega = 1.0;
+        p.pure = 1;
+        for (int s = 0; s < 32; ++s) p.off[s] = s < (int)ctx->offsets.size() ? ctx->offsets[s] : 0;
+        return biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream);
+    };
     CU(cudaMemsetAsync(d_H, 0, (size_t)(k + 1) * k * nt * sizeof(double), ctx->stream));
     // v_0 = P~2^{-1} (b - AA x_in) with b = A' x_prev + f, and the norms of b - AA x_in
     CU(launch_main(ctx, biot::MODE_ZOUT, xin, nullptr, &w, &tm, ctx->gm_V[0]));
+    CU(p1_complete(ctx->gm_V[0]));
     CU(dots(ctx->gm_V[0], Vd, 1, d_scale, d_beta, true));              // beta_t, 1 / beta_t
     CU(combine(ctx->gm_V[0], ctx->gm_V[0], nullptr, 0, 1.0, d_scale));
     for (int j = 0; j < k; ++j) {
         // w = P~2^{-1} AA v_j into v_{j+1}
         CU(launch_main(ctx, biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1], &w, &ctx->gm_tmap[j]));
+        CU(p1_complete(ctx->gm_V[j + 1]));
         // CGS2: two passes of h = V^T w (accumulated into column j of H), w -= V h
         for (int pass = 0; pass < 2; ++pass) {
             CU(dots(ctx->gm_V[j + 1], Vd, j + 1, d_h, hcol(0, j), false));
@@ -838,7 +967,6 @@ biot_status gmres_check(biot_ctx *ctx, int32_t K, int32_t k) {
         return fail(ctx, BIOT_E_INVALID, "need K >= 0 and 1 <= k <= " + std::to_string(biot::gmres_max_vectors() - 1));
     if (ctx->kern != 4 && ctx->kern != 6)
         return fail(ctx, BIOT_E_STATE, "per-step GMRES needs a tile kernel (structured 2D / 3D mesh)");
-    if (ctx->precond != 2) return fail(ctx, BIOT_E_STATE, "per-step GMRES is left-preconditioned by P~2 (precond = 2)");
     return BIOT_OK;
 }
 
@@ -1239,6 +1367,18 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const char *tp = std::getenv("BIOT_P1_TWOPASS");
         ctx->p1_fused = ctx->precond == 1 && !(tp && std::atoi(tp) == 1);
     }
+    {
+        // overlapped halo for the tile kernels' Jacobi sweep: NCCL exchange on a comm stream;
+        // ranks > 0 defer their first local step (also forced with MANUAL_HALO for tests).
+        // The step-0 kernels exist for P~2 and the fused 2D / two-pass 3D P~1.
+        const bool tile = ctx->kern == 4 || ctx->kern == 6;
+        const bool s0ok = ctx->precond == 2 || (ctx->kern == 4 ? ctx->p1_fused : true);
+        const char *no = std::getenv("BIOT_NO_OVERLAP");
+        const bool allow = tile && s0ok && !(no && std::atoi(no) == 1) && opts->world > 1;
+        ctx->overlap = allow && !(opts->flags & BIOT_FLAG_MANUAL_HALO);
+        ctx->defer0 = allow && opts->rank > 0 &&
+                      (ctx->overlap || (opts->flags & BIOT_FLAG_DEFER_STEP0));
+    }
     const int64_t chunk = ctx->kern == 3 ? 32 * ctx->mT
                         : ctx->kern == 4 ? biot::tile2d_chunk()
                         : ctx->kern == 6 ? biot::tile3d_chunk()
@@ -1257,7 +1397,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     CU(cudaEventCreate(&ctx->ev_a));
     CU(cudaEventCreate(&ctx->ev_b));
     ALLOC(ctx->d_iter, sizeof(int64_t));
-    ctx->use_graph = !(opts->flags & BIOT_FLAG_NO_GRAPH) && (opts->world == 1 || (opts->flags & BIOT_FLAG_MANUAL_HALO));
+    ctx->use_graph = !(opts->flags & BIOT_FLAG_NO_GRAPH) && (opts->world == 1 || (opts->flags & BIOT_FLAG_MANUAL_HALO)) &&
+                     !(opts->flags & BIOT_FLAG_DEFER_STEP0);
     if (const char *e = std::getenv("BIOT_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(1.0, std::atof(e));
 
     const int nc = ctx->nc;
@@ -1283,6 +1424,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         std::vector<double> x0(bc->x_initial, bc->x_initial + (size_t)ctx->N * nc);
         for (size_t q = 0; q < x0.size(); ++q)
             if (op->fixed[q]) x0[q] = 0.0;
+        for (double v : x0) ctx->x0_zero = ctx->x0_zero && v == 0.0;
         CU(h2d(ctx, ctx->ghost, x0.data(), vec_bytes));
     }
     // operator arrays padded to n_alloc nodes with zeros (dummy rows of the blocked kernel)
@@ -1325,6 +1467,25 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     }
     ALLOC(ctx->sendbuf, vec_bytes);
     CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
+    ctx->send_w = ctx->sendbuf;
+    if (ctx->overlap) {
+        ALLOC(ctx->sendbuf2, vec_bytes);
+        CU(cudaMemsetAsync(ctx->sendbuf2, 0, vec_bytes, ctx->stream));
+        CU(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&ctx->ev_ready, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&ctx->ev_comm, cudaEventDisableTiming));
+        CU(cudaEventRecord(ctx->ev_comm, ctx->stream));
+    }
+    if (ctx->defer0) {
+        ALLOC(ctx->zero_ghost_base, (size_t)ctx->rows_alloc * sizeof(double));
+        CU(cudaMemsetAsync(ctx->zero_ghost_base, 0, (size_t)ctx->rows_alloc * sizeof(double), ctx->stream));
+        ctx->zero_ghost = ctx->zero_ghost_base + ctx->pad * nc;
+        ALLOC(ctx->zu0, (size_t)ctx->N * (ctx->nc - 1) * sizeof(double));
+        ctx->step0_blocks = ctx->kern == 4 ? biot::tile2d_step0_blocks(ctx->N) : biot::tile3d_step0_blocks(ctx->N);
+        // step-0 norm partials [blocks][2] + the two-stage finalize's scratch behind them
+        ALLOC(ctx->part0, (size_t)(ctx->step0_blocks * 2 + std::max<int64_t>(1, biot::finalize_scratch_doubles(ctx->step0_blocks, 1))) *
+                              sizeof(double));
+    }
 
     const int nwp = 8 / ctx->tw;
     ctx->shape.smem = (size_t)nwp * (nchunks * chunk) * 2 * sizeof(double);
@@ -1341,6 +1502,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ctx->groups = biot::march_groups(tmp);
     } else if (ctx->kern == 4) {
         CU(biot::tile2d_shape(ctx->device, &ctx->shape));
+        reserve_comm_sms(ctx);
         // rows per tile: minimise (waves of tiles) x (rows + halo cost)
         const int64_t n_seg = (ctx->row_w + biot::tile2d_seg() - 1) / biot::tile2d_seg();
         int64_t rpt = 1;
@@ -1452,14 +1614,15 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         }
     } else if (ctx->kern == 6) {
         CU(biot::tile3d_shape(ctx->device, &ctx->shape));
+        reserve_comm_sms(ctx);
         // planes per tile: minimise (waves of tiles) x (planes + halo cost)
-        const int64_t n1 = ctx->n1, np = (n1 + 3) / 4;
+        const int64_t n1 = ctx->n1, npp = biot::tile3d_patches(n1);
         int64_t best_zr = n1;
         double best = 1e300;
         for (int64_t nzr = std::max<int64_t>(2, (n1 + biot::tile3d_max_zrows() - 1) / biot::tile3d_max_zrows());
              nzr <= 8; ++nzr) {
             const int64_t zr = (n1 + nzr - 1) / nzr;
-            const int64_t waves = (np * np * ((n1 + zr - 1) / zr) + ctx->shape.grid - 1) / ctx->shape.grid;
+            const int64_t waves = (npp * ((n1 + zr - 1) / zr) + ctx->shape.grid - 1) / ctx->shape.grid;
             const double cost = (double)waves * ((double)zr + 0.25);
             if (cost < best - 1e-9) { best = cost; best_zr = zr; }
         }
@@ -1655,6 +1818,9 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
         biot_status s = one_iteration(ctx, ctx->ev_s[2 * k], ctx->ev_s[2 * k + 1]);
         if (s != BIOT_OK) return s;
     }
+    // the last overlapped exchange completes inside the call (later collectives of the
+    // communicator, and the caller's reads of the ghost, are ordered after it)
+    if (ctx->overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
     {
         biot_status s = wait_done(ctx, ctx->ev_b);
@@ -2113,6 +2279,7 @@ biot_status biot_set_ghost(biot_ctx *ctx, const double *x) {
     if (ctx->rank == 0 && ctx->world > 1)
         return fail(ctx, BIOT_E_STATE, "rank 0's ghost is x_0 (fixed)");
     CU(cudaSetDevice(ctx->device));
+    if (ctx->rank == 0) ctx->x0_zero = false;   // a replaced x_0 is no longer known to be zero
     CU(cudaMemcpyAsync(ctx->ghost, x, (size_t)ctx->N * ctx->nc * sizeof(double), cudaMemcpyHostToDevice,
                        ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));

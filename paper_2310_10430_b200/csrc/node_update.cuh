@@ -31,7 +31,8 @@ __device__ __forceinline__ double cload(const double *p) {
 // sweep kernel so the results are identical): r = s_t f + q(t-1) - acc, norms,
 // z = P^-1 r (P~2, or the displacement half of P~1), x^{k+1} = x^k + omega z.
 // MASK = false: the caller guarantees no Dirichlet row (interior stencil nodes).
-// ZFULL: outz = z = P~2^{-1} r for every component (GMRES); else outz = (z_u, r_p)
+// ZFULL: outz = z = P~2^{-1} r for every component (GMRES; zfull_rt = false: the first
+// half (z_u, r_p) of P~1^{-1} r for GMRES with P~1); else outz = (z_u, r_p)
 // (the P~1 first pass).
 // The load of step t at one node: f_t = sum_j s_j(t) F_j.  The epilogue applies term 0
 // (the traction load s_t F of R16, or the first term of R24); the kMaxLoads kernels
@@ -63,7 +64,8 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
                                               double qprev, const LD &ld,
                                               const double (&Dv)[D + 1], const double (&xs)[D + 1][T],
                                               double (&nu)[T], double (&npn)[T],
-                                              double (&outx)[D + 1][T], double (&outz)[D + 1][T]) {
+                                              double (&outx)[D + 1][T], double (&outz)[D + 1][T],
+                                              bool zfull_rt = true) {
     constexpr int NC = D + 1;
 #pragma unroll
     for (int tt = 0; tt < T; ++tt) {
@@ -90,7 +92,7 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             outx[c][tt] = fma(omega, z[c], xs[c][tt]);
-            outz[c][tt] = (c < D || ZFULL) ? z[c] : r[D];
+            outz[c][tt] = (c < D || (ZFULL && zfull_rt)) ? z[c] : r[D];
         }
     }
 }

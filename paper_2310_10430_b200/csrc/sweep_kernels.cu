@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kThreads) pass2_kernel(const Pass2Args a) {
                 for (int tt = 0; tt < kT; ++tt) {
                     if (t0 + tt < n_tl && t0 + tt >= a.t_lo) {
                         const double zp = dv * (bt[tt] - rp[tt]);
-                        const double v = fma(a.omega, zp, xp[tt]);
+                        const double v = a.pure ? zp : fma(a.omega, zp, xp[tt]);
                         dst[tt] = v;
                         if (a.sendbuf && t0 + tt == n_tl - 1) a.sendbuf[i * NC + D] = v;
                     }

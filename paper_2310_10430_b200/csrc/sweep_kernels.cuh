@@ -50,6 +50,10 @@ struct SweepArgs {
     int64_t row_w;          // nodes per grid row (n+1)
     int32_t n_rows;         // grid rows (n+1)
     int32_t rows_per_tile;  // rows marched by one tile
+    int32_t ghost_zero;     // tile kernels: the ghost is identically zero (x_0 = 0 on rank 0, or the
+                            // deferred sweep of the overlapped halo): q(t0-1) = A' 0 = +0 without loads
+    int32_t p1_out;         // GMRES modes (ZOUT / MATVEC) with P~1: write the first half (z_u, r_p) of
+                            // P~1^{-1} r; pass2 (pure) then completes z_p in place
 };
 
 struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
@@ -65,6 +69,8 @@ struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_
     int32_t n_tl, tw, node_block;
     double omega;
     int64_t off[32];
+    int32_t pure;           // 1: xn_p = D_S^{-1} (B^T z_u - r_p) itself (GMRES with P~1, in place on
+                            // a Krylov panel: zbuf = xn), not x_p + omega times it
 };
 
 
@@ -134,9 +140,15 @@ void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
+// Deferred first local step (overlapped halo): recompute step t_off of every node with
+// the ghost, overwrite x^{k+1} there, norm partials per block -> part[blocks][2].
+// Modes MODE_UPDATE_P2 and MODE_P1_FUSED (zu0: 2 doubles per node scratch).
+int tile2d_step0_blocks(int64_t n_nodes);
+cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *zu0, double *part, cudaStream_t st);
 
-// 3D TMA tile kernel: 4x4 (x,y) node patches x 32-step chunks, marching z
+// 3D TMA tile kernel: 4x2 (x,y) node patches x 64-step chunks, marching z
 int64_t tile3d_groups(const Tile3dArgs &a);
+int64_t tile3d_patches(int64_t n1);   // (x, y) patches of an n1^3 mesh
 int tile3d_chunk();
 int tile3d_max_zrows();
 int tile3d_min_n1();
@@ -144,6 +156,10 @@ void tile3d_box(uint32_t *box);      // {time, x*4+c, y, z}
 cudaError_t tile3d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
+// deferred first local step (see launch_tile2d_step0): MODE_UPDATE_P2 or MODE_P1_PASS1
+// (the two-pass P~1; zu0: 3 doubles per node scratch)
+int tile3d_step0_blocks(int64_t n_nodes);
+cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *zu0, double *part, cudaStream_t st);
 
 // Per-step GMRES panel kernels (gmres_kernels.cu): column-wise (per time step) dot
 // products of a panel with nb panels (b_dev: device array of panel pointers) and

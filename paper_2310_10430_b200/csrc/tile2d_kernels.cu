@@ -236,7 +236,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
     double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
     // ghost: q(t0-1) from the ghost column now (single-chunk windows); otherwise from the
     // carry, which the chunk loop prefilled from the ghost column for chunk 0
-    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
+    if (lane == 0) qp0 = ghost ? (a.ghost_zero ? 0.0 : ghost_q<CLS, S0, A>(a, i, T)) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
     double Dv[3], xs[3][kT2];
@@ -267,7 +267,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
             }
         }
         epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2,
-                                                    outx, outz);
+                                                    outx, outz, !a.p1_out);
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             nu[2 * h + tt] = nu2[tt];
@@ -401,8 +401,9 @@ __device__ __forceinline__ void finish_mv(const A &a, const double *pu, int p, i
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
             const double dv = aux[10 + c];
-            const double w0 = c < 2 ? dv * acc[c][2 * h] : -(dv * acc[c][2 * h]);
-            const double w1 = c < 2 ? dv * acc[c][2 * h + 1] : -(dv * acc[c][2 * h + 1]);
+            // P~2^{-1} AA v; P~1: its first half (D_A^{-1} (AA v)_u, (AA v)_p)
+            const double w0 = c < 2 ? dv * acc[c][2 * h] : a.p1_out ? acc[c][2 * h] : -(dv * acc[c][2 * h]);
+            const double w1 = c < 2 ? dv * acc[c][2 * h + 1] : a.p1_out ? acc[c][2 * h + 1] : -(dv * acc[c][2 * h + 1]);
             double *dst = a.xn + row + c * P + h * (kCT / 2);
             if (whole) {
                 *reinterpret_cast<double2 *>(dst) = make_double2(w0, w1);
@@ -545,9 +546,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const int64_t i = (int64_t)mm * g.W + col;
                         const bool intr = __ldg(a.aux + i * kAuxRec + 13) == 1.0;
                         qcarry[(mm - ja) * kSeg + warp] =
-                            intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
-                                 : ghost_q<true, S0, Tile2dArgs>(
-                                       a, i, cls_base + (ccx + 3 * axis_class(mm, g.nrows)) * 7 * kCW);
+                            a.ghost_zero ? 0.0
+                            : intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
+                                   : ghost_q<true, S0, Tile2dArgs>(
+                                         a, i, cls_base + (ccx + 3 * axis_class(mm, g.nrows)) * 7 * kCW);
                     }
                     __syncwarp();
                 }
@@ -725,7 +727,7 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
     }
     double qp0 = __shfl_up_sync(0xffffffffu, q[1], 1);
     double qp1 = __shfl_sync(0xffffffffu, lane == 31 ? q[1] : q[3], (lane + 31) & 31);
-    if (lane == 0) qp0 = ghost ? ghost_q<CLS, S0, A>(a, i, T) : *carry;
+    if (lane == 0) qp0 = ghost ? (a.ghost_zero ? 0.0 : ghost_q<CLS, S0, A>(a, i, T)) : *carry;
     __syncwarp();
     if (lane == 31) *carry = q[3];
     double Dv[3], xs[3][kT2];
@@ -904,8 +906,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     const int64_t i = (int64_t)mm * W + col;
                     const bool intr = __ldg(a.aux + i * kAuxRec + 13) == 1.0;
                     qcarry[(mm - ja) * kSeg + warp] =
-                        intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
-                             : ghost_q<true, S0, Tile2dArgs>(a, i, cls_base + (ccx + 3 * axis_class(mm, nrows)) * 7 * kCW);
+                        a.ghost_zero ? 0.0
+                        : intr ? ghost_q<false, S0, Tile2dArgs>(a, i, cls_base)
+                               : ghost_q<true, S0, Tile2dArgs>(a, i, cls_base + (ccx + 3 * axis_class(mm, nrows)) * 7 * kCW);
                 }
                 __syncwarp();
             }
@@ -1052,6 +1055,148 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
 }
 
+
+// ============================================================================
+// Deferred first step (overlapped time-slab halo): the sweep of a rank
+// r > 0 runs while the ghost x^k_{first-1} is still in flight, with a zero ghost, so
+// only the p-residual of the slab's first local step is wrong (A' enters through
+// q(t0-1) alone).  Once the ghost has arrived this kernel recomputes that step for
+// every node -- one thread per node, the tile kernel's slot order (ascending offsets),
+// coefficient sources (template / class / aux) and epilogue, so x^{k+1} is bitwise the
+// value the undeferred sweep would store -- overwrites it, and reduces the step's norm
+// partials per block in a fixed order.  Fused P~1 needs z_u of the neighbours at that
+// step: phase 0 writes it for every node, phase 1 completes the step.
+// ============================================================================
+template <bool CLS, bool S0>
+__device__ __forceinline__ void col_residual(const Tile2dArgs &a, int64_t i, const double *col, int64_t stride,
+                                             const double *aux, const double *T, double (&acc)[3], double &q) {
+#pragma unroll
+    for (int c = 0; c < 3; ++c) acc[c] = 0.0;
+    q = 0.0;
+#pragma unroll
+    for (int dr = -1; dr <= 1; ++dr)
+#pragma unroll
+        for (int dc = -1; dc <= 1; ++dc) {
+            const int s = slot2(dr, dc);
+            if (s < 0) continue;
+            const int64_t j = i + a.off[s];
+            double v[3];
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) v[cc] = __ldg(col + (j * 3 + cc) * stride);
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc) {
+                if constexpr (CLS) {
+                    const double *Ts = T + s * kCW;
+                    acc[0] = fma(Ts[cc * 3], v[cc], acc[0]);
+                    acc[1] = fma(Ts[cc * 3 + 1], v[cc], acc[1]);
+                    acc[2] = fma(cc == 2 ? aux[s] : Ts[cc * 3 + 2], v[cc], acc[2]);
+                    q = fma(cc < 2 ? Ts[cc * 3 + 2] : Ts[9], v[cc], q);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        const int e = c * 3 + cc;
+                        if (tmpl_zero(s, e, S0)) continue;
+                        acc[c] = fma(e == 8 ? aux[s] : a.tmpl[s][e], v[cc], acc[c]);
+                    }
+                    const int eq = cc < 2 ? 6 + cc : 9;
+                    if (!tmpl_zero(s, eq, S0)) q = fma(a.tmpl[s][eq], v[cc], q);
+                }
+            }
+        }
+}
+
+template <bool S0, int MODE, int NL>
+__global__ void __launch_bounds__(256) tile2d_step0_kernel(const Tile2dArgs a, int phase, double *zu0, double *part) {
+    constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
+    const int64_t N = a.n_nodes, P = a.pitch;
+    const int W = (int)a.row_w;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const double *col = a.x + a.t_off;            // x^k of the first local step, stride = pitch
+    double su = 0.0, sp = 0.0;
+    if (i < N) {
+        const double *aux = a.aux + i * kAuxRec;
+        const bool intr = aux[13] == 1.0;
+        const double *T = a.cls + (axis_class((int)(i % W), W) + 3 * axis_class((int)(i / W), a.n_rows)) * 7 * kCW;
+        double acc[3], q;
+        if (intr) col_residual<false, S0>(a, i, col, P, aux, T, acc, q);
+        else col_residual<true, S0>(a, i, col, P, aux, T, acc, q);
+        if constexpr (NL > 1) {
+#pragma unroll
+            for (int jt = 1; jt < NL; ++jt) {
+                const double sj = a.s[jt * a.s_pitch + a.t_off];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) acc[c] = fma(-sj, aux[14 + 3 * (jt - 1) + c], acc[c]);
+            }
+        }
+        const double qp = intr ? ghost_q<false, S0, Tile2dArgs>(a, i, T) : ghost_q<true, S0, Tile2dArgs>(a, i, T);
+        double acc1[3][1], q1[1] = {q}, xs[3][1], nu1[1] = {0.0}, np1[1] = {0.0}, outx[3][1], outz[3][1], Dv[3];
+        Loads<3, 1, 1> ld;
+        ld.sv[0][0] = a.s[a.t_off];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            acc1[c][0] = acc[c];
+            xs[c][0] = col[(i * 3 + c) * P];
+            Dv[c] = aux[10 + c];
+            ld.F[0][c] = aux[7 + c];
+        }
+        if (intr) epilogue_math<2, 1, false, false>(a.omega, acc1, q1, qp, ld, Dv, xs, nu1, np1, outx, outz);
+        else epilogue_math<2, 1, true, false>(a.omega, acc1, q1, qp, ld, Dv, xs, nu1, np1, outx, outz);
+        if (MODE == MODE_P1_FUSED && phase == 0) {
+            zu0[i * 2] = outz[0][0];
+            zu0[i * 2 + 1] = outz[1][0];
+            return;
+        }
+        su = nu1[0];
+        sp = np1[0];
+        double *xo = a.xn + i * 3 * P + a.t_off;
+        double out[3] = {outx[0][0], outx[1][0], outx[2][0]};
+        if constexpr (MODE == MODE_P1_FUSED) {
+            // z_p = D_S^{-1} (B^T z_u - r_p), B^T in slot order, as finish_zp of the fused pass
+            const double wdv = a.omega * aux[12];
+            const double y = fma(-wdv, outz[2][0], xs[2][0]);
+            double bt = 0.0;
+#pragma unroll
+            for (int dr = -1; dr <= 1; ++dr)
+#pragma unroll
+                for (int dc = -1; dc <= 1; ++dc) {
+                    const int s = slot2(dr, dc);
+                    if (s < 0) continue;
+                    const int64_t j = i + a.off[s];
+                    if (j < 0 || j >= N) continue;       // off the mesh: z_u = 0 there (the fused pass's zeros)
+#pragma unroll
+                    for (int cc = 0; cc < 2; ++cc) {
+                        if (intr && tmpl_zero(s, 6 + cc, S0)) continue;
+                        const double cf = intr ? a.tmpl[s][6 + cc] : T[s * kCW + cc * 3 + 2];
+                        bt = fma(cf, zu0[j * 2 + cc], bt);
+                    }
+                }
+            out[2] = fma(wdv, bt, y);
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) xo[c * P] = out[c];
+        if (a.sendbuf && a.n_tl == 1)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) a.sendbuf[i * 3 + c] = out[c];
+    }
+    if (MODE == MODE_P1_FUSED && phase == 0) return;
+    // fixed-order block reduction of the step's norm contributions
+    __shared__ double red[2][256];
+    red[0][threadIdx.x] = su;
+    red[1][threadIdx.x] = sp;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) {
+            red[0][threadIdx.x] += red[0][threadIdx.x + w];
+            red[1][threadIdx.x] += red[1][threadIdx.x + w];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[blockIdx.x * 2] = red[0][0];
+        part[blockIdx.x * 2 + 1] = red[1][0];
+    }
+}
+
 }  // namespace
 
 int tile2d_seg() { return kSeg; }
@@ -1125,6 +1270,28 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
     else { if (a.s0) BIOT_T2L(true, MODE_RESIDUAL) else BIOT_T2L(false, MODE_RESIDUAL) }
 #undef BIOT_T2L
 #undef BIOT_T2
+    return cudaGetLastError();
+}
+
+int tile2d_step0_blocks(int64_t n_nodes) { return (int)((n_nodes + 255) / 256); }
+
+cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *zu0, double *part, cudaStream_t st) {
+    const int nb = tile2d_step0_blocks(a.n_nodes);
+#define BIOT_S0(S0_, M_, NL_)                                                                \
+    {                                                                                         \
+        if ((M_) == MODE_P1_FUSED) tile2d_step0_kernel<S0_, M_, NL_><<<nb, 256, 0, st>>>(a, 0, zu0, part); \
+        tile2d_step0_kernel<S0_, M_, NL_><<<nb, 256, 0, st>>>(a, 1, zu0, part);              \
+    }
+#define BIOT_S0M(M_)                                                                          \
+    {                                                                                         \
+        if (a.n_load > 1) { if (a.s0) BIOT_S0(true, M_, kMaxLoads) else BIOT_S0(false, M_, kMaxLoads) } \
+        else { if (a.s0) BIOT_S0(true, M_, 1) else BIOT_S0(false, M_, 1) }                   \
+    }
+    if (a.mode == MODE_P1_FUSED) BIOT_S0M(MODE_P1_FUSED)
+    else if (a.mode == MODE_UPDATE_P2) BIOT_S0M(MODE_UPDATE_P2)
+    else return cudaErrorInvalidValue;
+#undef BIOT_S0M
+#undef BIOT_S0
     return cudaGetLastError();
 }
 

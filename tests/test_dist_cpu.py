@@ -110,3 +110,20 @@ def test_time_slab_protocol_bitwise_gloo():
     for r in range(world):
         got = np.frombuffer(out[r], dtype=np.float64).reshape(ntl, S.ndof)
         assert np.array_equal(got, X[1 + r * ntl:1 + (r + 1) * ntl])
+
+
+def test_bench_self_spawns_ranks_reference_arm():
+    """bench.py --gpus N without a launcher re-runs itself under torch.distributed.run with N
+    local ranks; rank 0 alone prints the (reference-arm) line with n_gpus = N."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "1", "--steps", "2", "--warmup", "1"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    assert lines[0]["impl"] == "reference" and lines[0]["n_gpus"] == 2 and lines[0]["steps"] == 2

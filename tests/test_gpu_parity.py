@@ -272,11 +272,11 @@ def test_gs_parity_3d(precond, omega):
 
 # ---- per-step GMRES (Alg. 3 with K = GMRES) ----
 
-def _gmres_pair(prob, nt, K, k):
+def _gmres_pair(prob, nt, K, k, precond=2):
     from oracle import gmres as ogm
     s = load_scales(nt, parity=True)
     x0 = _x0(prob, np.arange(1, nt + 1))
-    g = BiotSolver(prob, n_t=nt, precond=2, omega=0.5, load_scale=s)
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=0.5, load_scale=s)
     try:
         g.set_iterate(1, x0)
         g.iterate_gmres(K, k)
@@ -287,7 +287,7 @@ def _gmres_pair(prob, nt, K, k):
     S = oracle.OracleSystem(prob)
     X = np.zeros((nt + 1, S.ndof))
     X[1:] = S.to_paper(x0)
-    Xo, ho = ogm.iterate(S, X, s, K, k)
+    Xo, ho = ogm.iterate(S, X, s, K, k, precond=precond)
     return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho)
 
 
@@ -308,11 +308,11 @@ def test_gmres_parity_config2():
     assert norm_errors(hg, ho).max() < TOL
 
 
-def _gs_gmres_pair(prob, nt, K, k):
+def _gs_gmres_pair(prob, nt, K, k, precond=2):
     from oracle import gmres as ogm
     s = load_scales(nt, parity=True)
     x0 = _x0(prob, np.arange(1, nt + 1))
-    g = BiotSolver(prob, n_t=nt, precond=2, omega=0.5, load_scale=s)
+    g = BiotSolver(prob, n_t=nt, precond=precond, omega=0.5, load_scale=s)
     try:
         g.set_iterate(1, x0)
         g.iterate_gs_gmres(K, k)
@@ -323,7 +323,7 @@ def _gs_gmres_pair(prob, nt, K, k):
     S = oracle.OracleSystem(prob)
     X = np.zeros((nt + 1, S.ndof))
     X[1:] = S.to_paper(x0)
-    Xo, ho = ogm.iterate(S, X, s, K, k, gauss_seidel=True)
+    Xo, ho = ogm.iterate(S, X, s, K, k, gauss_seidel=True, precond=precond)
     return (xg, hg), (np.stack([S.from_paper(v) for v in Xo[1:]]), ho)
 
 
@@ -363,4 +363,31 @@ def test_gmres_parity_3d(gs):
     prob = make_problem(3, 6, 20, 1.0 / 20, 1, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0, kappa_seed=2)
     (xg, hg), (xo, ho) = (_gs_gmres_pair if gs else _gmres_pair)(prob, 20, 2, 4)
     assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+# ---- per-step GMRES left-preconditioned by P~1 (eq. p1; the paper's §4.1 / §4.3 choice) ----
+
+@pytest.mark.parametrize("nt,K,k", [(32, 3, 2), (7, 3, 10), (150, 2, 4)])
+def test_gmres_p1_parity_config1(nt, K, k):
+    """GMRES(k) per step with P~1 (tile ZOUT/MATVEC first half + the in-place z_p pass)
+    vs the oracle's Alg. 3 with P~1: x^K and the residual history at 1e-9."""
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gmres_pair(prob, nt, K, k, precond=1)
+    assert field_errors(xg, xo, 2).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+@pytest.mark.parametrize("gs", [False, True])
+def test_gmres_p1_parity_3d(gs):
+    prob = make_problem(3, 6, 20, 1.0 / 20, 1, storage=1e-3, kappa_median=1e-3, kappa_sigma=1.0, kappa_seed=2)
+    (xg, hg), (xo, ho) = (_gs_gmres_pair if gs else _gmres_pair)(prob, 20, 2, 4, precond=1)
+    assert field_errors(xg, xo, 3).max() < TOL
+    assert norm_errors(hg, ho).max() < TOL
+
+
+def test_gs_gmres_p1_parity_config1():
+    prob = config_problem(1)
+    (xg, hg), (xo, ho) = _gs_gmres_pair(prob, 32, 3, 4, precond=1)
+    assert field_errors(xg, xo, 2).max() < TOL
     assert norm_errors(hg, ho).max() < TOL

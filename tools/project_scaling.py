@@ -1,11 +1,12 @@
 """Projected time-slab scaling from one GPU.
 
 Only one B200 is reachable, so the P-GPU run is projected from the work one rank does:
-rank P-1's slab (N_t/P steps, the ghost fixed: BIOT_FLAG_MANUAL_HALO -- the same kernels
-and launch shapes the NCCL run launches on that rank) timed on this GPU, plus the halo
-(one slice of N_dof doubles per outer iteration) at the NVLink 5 per-direction bandwidth
-(900 GB/s, B200_PROFILING.md) and a fixed latency, counted as NOT overlapped (an upper
-bound on the exchange cost).
+rank P-1's slab (N_t/P steps) in the overlapped-halo form the NCCL run uses on that rank
+(BIOT_FLAG_MANUAL_HALO | BIOT_FLAG_DEFER_STEP0: the sweep with a zero ghost on the SMs
+left after the NCCL reservation, then the first-step completion) timed on this GPU, plus
+the halo (one slice of N_dof doubles per outer iteration) at the NVLink 5 per-direction
+bandwidth (900 GB/s, B200_PROFILING.md) and a fixed latency, counted as NOT overlapped
+(an upper bound: in the NCCL run the exchange runs during the sweep).
 
     efficiency(P) = T_1 / (P * (T_slab(P) + t_halo))
 
@@ -17,7 +18,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2310_10430_b200 import BiotSolver, FLAG_MANUAL_HALO  # noqa: E402
+from paper_2310_10430_b200 import BiotSolver, FLAG_MANUAL_HALO, FLAG_DEFER_STEP0  # noqa: E402
 from workloads import config_problem  # noqa: E402
 
 NVLINK_GBS = 900.0          # per direction, B200 NVLink 5 (B200_PROFILING.md)
@@ -26,7 +27,7 @@ HALO_LAT_US = 15.0          # assumed send/recv latency per exchange (NCCL p2p o
 
 def slab_ms(prob, P, K, precond, omega):
     g = BiotSolver(prob, precond=precond, omega=omega, rank=P - 1, world=P,
-                   flags=FLAG_MANUAL_HALO if P > 1 else 0)
+                   flags=(FLAG_MANUAL_HALO | FLAG_DEFER_STEP0) if P > 1 else 0)
     try:
         g.iterate(3)
         best = []
