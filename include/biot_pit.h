@@ -124,6 +124,16 @@ typedef struct {
 #define BIOT_FLAG_DEFER_STEP0 4u     /* with MANUAL_HALO, ranks > 0 run the overlapped-halo form
                                         of biot_iterate (sweep with a zero ghost, then the first
                                         local step completed from the ghost): tests / emulation  */
+#define BIOT_FLAG_SWEEP_SLABS 8u     /* world > 1: partition the Gauss-Seidel SWEEPS across ranks
+                                        (Alg. 4/5 pipeline) instead of time slabs:
+                                        every rank holds all n_t steps; biot_iterate_gs(K) runs
+                                        global sweeps rank*K/world+1 .. (rank+1)*K/world and streams
+                                        each finished step's slice to rank+1 (one per wave);
+                                        x^K is broadcast from rank world-1 at the end.  With
+                                        MANUAL_HALO: drive biot_gs_begin/wave/end; before wave W,
+                                        rank r > 0 whose step W - (r*K/world) is in range takes
+                                        rank r-1's biot_last_slice through biot_set_ghost; the
+                                        result stays on rank world-1.  biot_iterate: BIOT_E_STATE */
 #define BIOT_FLAG_NO_GRAPH    2u     /* biot_iterate launches kernels directly; default: pairs
                                         of iterations replay one captured CUDA graph (world == 1
                                         or MANUAL_HALO; NCCL iterations always launch directly) */

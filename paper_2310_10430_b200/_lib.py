@@ -26,6 +26,7 @@ STATUS = {0: "BIOT_OK", 1: "BIOT_E_INVALID", 2: "BIOT_E_NOMEM", 3: "BIOT_E_CUDA"
 FLAG_MANUAL_HALO = 1
 FLAG_NO_GRAPH = 2
 FLAG_DEFER_STEP0 = 4
+FLAG_SWEEP_SLABS = 8
 
 
 class BiotMesh(ctypes.Structure):

@@ -44,6 +44,7 @@ struct NcclApi {
     ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;   // optional
     ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;                           // optional
     ncclResult_t (*CommCount)(const ncclComm_t, int *) = nullptr;              // optional
+    ncclResult_t (*Bcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi *nccl() {
@@ -68,6 +69,7 @@ NcclApi *nccl() {
             api.CommGetAsyncError = (decltype(api.CommGetAsyncError))dlsym(api.h, "ncclCommGetAsyncError");
             api.CommAbort = (decltype(api.CommAbort))dlsym(api.h, "ncclCommAbort");
             api.CommCount = (decltype(api.CommCount))dlsym(api.h, "ncclCommCount");
+            api.Bcast = (decltype(api.Bcast))dlsym(api.h, "ncclBroadcast");
             if (!api.GetUniqueId || !api.CommInitRank || !api.Send || !api.Recv || !api.GroupStart ||
                 !api.GroupEnd || !api.CommDestroy)
                 api.h = nullptr;
@@ -151,6 +153,10 @@ struct biot_ctx {
     // complete their first local step after the ghost arrived (the step-0 kernels)
     bool overlap = false, defer0 = false;
     bool x0_zero = true;              // x_0 = 0 (rank 0's ghost is identically zero)
+    // Gauss-Seidel sweeps partitioned across ranks (BIOT_FLAG_SWEEP_SLABS, Alg. 4/5):
+    // every rank holds all steps; sweep_in receives the predecessor rank's finished slices
+    bool sweep_mode = false;
+    double *sweep_in = nullptr;
     double *sendbuf2 = nullptr, *zero_ghost_base = nullptr, *zero_ghost = nullptr, *zu0 = nullptr, *part0 = nullptr;
     const double *ghost_override = nullptr;
     int step0_blocks = 0;
@@ -180,6 +186,8 @@ struct biot_ctx {
     int32_t rows_per_tile_p1 = 0;
     int64_t groups_p1 = 0;
     double *aux_base = nullptr;       // aux records with front padding (tile2d halo columns)
+    int32_t aux_geo = 0, ux0 = 0, ux1 = -1, uy0 = 0, uy1 = -1;   // tile2d aux-uniform rectangle
+    double aux_u[biot::kAuxRecU] = {0};
     // 4: TMA-pipelined 2D tile kernel
     double *aux = nullptr;
     double tmpl[7][10] = {{0}};
@@ -260,7 +268,7 @@ void free_all(biot_ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->loadx, (void *)c->dinv, (void *)c->s,
-                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->zu0,
+                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->zu0, (void *)c->sweep_in,
                     (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
@@ -320,7 +328,8 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.row_w = c->row_w;
     a.n_rows = c->n_rows;
     a.rows_per_tile = c->rows_per_tile;
-    a.ghost_zero = (c->ghost_override && c->ghost_override == c->zero_ghost) || (c->rank == 0 && c->x0_zero) ? 1 : 0;
+    a.ghost_zero = (c->ghost_override && c->ghost_override == c->zero_ghost) ||
+                   ((c->rank == 0 || c->sweep_mode) && c->x0_zero) ? 1 : 0;
     a.p1_out = (c->precond == 1 && (mode == biot::MODE_ZOUT || mode == biot::MODE_MATVEC)) ? 1 : 0;
     return a;
 }
@@ -335,7 +344,7 @@ biot_status pack_send(biot_ctx *ctx) {
 }
 
 biot_status halo_exchange(biot_ctx *ctx) {
-    if (ctx->world == 1 || (ctx->flags & BIOT_FLAG_MANUAL_HALO)) return BIOT_OK;
+    if (ctx->world == 1 || (ctx->flags & BIOT_FLAG_MANUAL_HALO) || ctx->sweep_mode) return BIOT_OK;
     NcclApi *api = nccl();
     if (!api || !ctx->comm) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
     if (ctx->send_dirty) {
@@ -562,6 +571,12 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         a.aux = c->aux;
         a.cls = c->cls;
         a.pad_nodes = c->pad;
+        a.aux_geo = c->aux_geo;
+        a.ux0 = c->ux0;
+        a.ux1 = c->ux1;
+        a.uy0 = c->uy0;
+        a.uy1 = c->uy1;
+        std::memcpy(a.aux_u, c->aux_u, sizeof(a.aux_u));
         if (mode == biot::MODE_P1_FUSED) a.rows_per_tile = c->rows_per_tile_p1;
         a.ghost_stride = 1;
         a.t_off = 0;
@@ -1214,7 +1229,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         return fail(nullptr, BIOT_E_INVALID, "omega must be > 0");
     if (opts->world < 1 || opts->rank < 0 || opts->rank >= opts->world)
         return fail(nullptr, BIOT_E_INVALID, "need 0 <= rank < world");
-    if (n_t % opts->world != 0)
+    const bool sweep_slabs = opts->world > 1 && (opts->flags & BIOT_FLAG_SWEEP_SLABS);
+    if (n_t % opts->world != 0 && !sweep_slabs)
         return fail(nullptr, BIOT_E_INVALID, "n_t must be divisible by world (time slabs)");
     if (opts->world > 1 && !(opts->flags & BIOT_FLAG_MANUAL_HALO) && !opts->nccl_id)
         return fail(nullptr, BIOT_E_INVALID, "world > 1 needs nccl_id (or BIOT_FLAG_MANUAL_HALO)");
@@ -1292,8 +1308,9 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ctx->n_t = n_t;
     ctx->rank = opts->rank;
     ctx->world = opts->world;
-    ctx->n_tl = n_t / opts->world;
-    ctx->first_step = ctx->rank * ctx->n_tl + 1;
+    ctx->sweep_mode = sweep_slabs;
+    ctx->n_tl = sweep_slabs ? n_t : n_t / opts->world;            // sweep partition: every rank holds all steps
+    ctx->first_step = sweep_slabs ? 1 : ctx->rank * ctx->n_tl + 1;
     ctx->flags = opts->flags;
     ctx->precond = opts->precond;
     ctx->omega = opts->omega;
@@ -1374,7 +1391,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         const bool tile = ctx->kern == 4 || ctx->kern == 6;
         const bool s0ok = ctx->precond == 2 || (ctx->kern == 4 ? ctx->p1_fused : true);
         const char *no = std::getenv("BIOT_NO_OVERLAP");
-        const bool allow = tile && s0ok && !(no && std::atoi(no) == 1) && opts->world > 1;
+        const bool allow = tile && s0ok && !(no && std::atoi(no) == 1) && opts->world > 1 && !sweep_slabs;
         ctx->overlap = allow && !(opts->flags & BIOT_FLAG_MANUAL_HALO);
         ctx->defer0 = allow && opts->rank > 0 &&
                       (ctx->overlap || (opts->flags & BIOT_FLAG_DEFER_STEP0));
@@ -1420,7 +1437,7 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ALLOC(ctx->ghost_base, (size_t)ctx->rows_alloc * sizeof(double));
     CU(cudaMemsetAsync(ctx->ghost_base, 0, (size_t)ctx->rows_alloc * sizeof(double), ctx->stream));
     ctx->ghost = ctx->ghost_base + ctx->pad * nc;
-    if (bc->x_initial && ctx->rank == 0) {
+    if (bc->x_initial && (ctx->rank == 0 || ctx->sweep_mode)) {
         std::vector<double> x0(bc->x_initial, bc->x_initial + (size_t)ctx->N * nc);
         for (size_t q = 0; q < x0.size(); ++q)
             if (op->fixed[q]) x0[q] = 0.0;
@@ -1468,6 +1485,10 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ALLOC(ctx->sendbuf, vec_bytes);
     CU(cudaMemsetAsync(ctx->sendbuf, 0, vec_bytes, ctx->stream));
     ctx->send_w = ctx->sendbuf;
+    if (ctx->sweep_mode) {
+        ALLOC(ctx->sweep_in, vec_bytes);
+        CU(cudaMemsetAsync(ctx->sweep_in, 0, vec_bytes, ctx->stream));
+    }
     if (ctx->overlap) {
         ALLOC(ctx->sendbuf2, vec_bytes);
         CU(cudaMemsetAsync(ctx->sendbuf2, 0, vec_bytes, ctx->stream));
@@ -1578,6 +1599,41 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             n_int += same;
         }
         ctx->n_interior = n_int;
+        {
+            // aux-uniform rectangle (single-load problems): the largest [m, W-1-m] x [m, n_rows-1-m]
+            // (m = 1, 2) whose nodes all carry the template node's record, up to pp entries that
+            // are 0 against a fixed pressure column (they multiply x = 0 there)
+            const double *R = aux.data() + (size_t)(aux_front + tnode) * KA;
+            auto uniform = [&](int64_t i) {
+                const double *r = aux.data() + (size_t)(aux_front + i) * KA;
+                if (r[13] != 1.0) return false;
+                for (int k = 0; k < 14; ++k) {
+                    if (r[k] == R[k]) continue;
+                    if (k < 7 && r[k] == 0.0) {
+                        const int64_t j = i + ctx->offsets[k];
+                        if (j >= 0 && j < ctx->N && op->fixed[(size_t)j * 3 + 2]) continue;
+                    }
+                    return false;
+                }
+                return true;
+            };
+            for (int m = 1; m <= 2 && ctx->n_load == 1 && !std::getenv("BIOT_NO_AUX_SKIP"); ++m) {
+                const int64_t x0 = m, x1 = ctx->row_w - 1 - m, y0 = m, y1 = ctx->n_rows - 1 - m;
+                if (x1 - x0 < 2 * biot::tile2d_seg() || y1 < y0) break;
+                bool ok = true;
+                for (int64_t y = y0; y <= y1 && ok; ++y)
+                    for (int64_t x = x0; x <= x1 && ok; ++x) ok = uniform(y * ctx->row_w + x);
+                if (ok) {
+                    ctx->aux_geo = 1;
+                    ctx->ux0 = (int32_t)x0;
+                    ctx->ux1 = (int32_t)x1;
+                    ctx->uy0 = (int32_t)y0;
+                    ctx->uy1 = (int32_t)y1;
+                    for (int k = 0; k < biot::kAuxRecU; ++k) ctx->aux_u[k] = R[k];
+                    break;
+                }
+            }
+        }
         if (std::getenv("BIOT_DEBUG"))
             std::fprintf(stderr, "[biot] tile2d: W=%lld rows/tile=%d groups=%lld interior=%lld/%lld s0=%d\n",
                          (long long)ctx->row_w, ctx->rows_per_tile, (long long)ctx->groups, (long long)n_int,
@@ -1793,6 +1849,8 @@ biot_status biot_set_load_scale(biot_ctx *ctx, const double *s) {
 biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
+    if (ctx->sweep_mode && K > 0)
+        return fail(ctx, BIOT_E_STATE, "sweep partition (BIOT_FLAG_SWEEP_SLABS): use the Gauss-Seidel calls");
     if (K == 0) return BIOT_OK;
     CU(cudaSetDevice(ctx->device));
     // pairs of iterations replay the context's CUDA graph (no NCCL inside: world == 1 or
@@ -1881,8 +1939,48 @@ biot_status gs_parity_copy(biot_ctx *ctx, const double *src, double *dst, int pa
     return BIOT_OK;
 }
 
+// Sweep partition (BIOT_FLAG_SWEEP_SLABS): this rank runs global sweeps u0..u1 of the K; at
+// global wave W it receives step W - u0 + 1 at its sweep u0 - 1 (from rank - 1's last sweep,
+// finished at wave W - 1) and finishes step W - u1 + 1 at its last sweep (sent at W + 1).
+int sw_u0(const biot_ctx *c) { return (int)((int64_t)c->rank * c->gs_K / c->world) + 1; }
+int sw_u1(const biot_ctx *c) { return (int)((int64_t)(c->rank + 1) * c->gs_K / c->world); }
+bool sw_in(const biot_ctx *c, int W, int *t) {
+    *t = W - sw_u0(c) + 1;
+    return c->rank > 0 && *t >= 0 && *t < c->n_t;
+}
+bool sw_out(const biot_ctx *c, int W, int *t) {
+    *t = W - sw_u1(c) + 1;
+    return c->rank + 1 < c->world && *t >= 0 && *t < c->n_t;
+}
+
+biot_status gs_window(biot_ctx *ctx, int w, int K, int64_t kbase);
+
 biot_status gs_run_wave(biot_ctx *ctx) {
-    const int w = ctx->gs_w++, K = ctx->gs_K, L = ctx->n_tl, g0 = ctx->first_step - 1;
+    const int W = ctx->gs_w++;
+    if (!ctx->sweep_mode) return gs_window(ctx, W, ctx->gs_K, ctx->gs_k0);
+    const int u0 = sw_u0(ctx), Kg = sw_u1(ctx) - u0 + 1;
+    const size_t rows = (size_t)ctx->N * ctx->nc;
+    int t;
+    if (sw_in(ctx, W, &t))   // X^{t, u0-1} (the predecessor's last sweep) into panel (cur + t) % 2
+        CU(cudaMemcpy2DAsync(ctx->x[(ctx->cur + t) % 2] + t, ctx->pitch * sizeof(double), ctx->sweep_in, sizeof(double),
+                             sizeof(double), rows, cudaMemcpyDeviceToDevice, ctx->stream));
+    const int wl = W - (u0 - 1);
+    if (wl >= 0 && wl < ctx->n_t + Kg - 1) {
+        biot_status st = gs_window(ctx, wl, Kg, ctx->gs_k0 + (u0 - 1));
+        if (st != BIOT_OK) return st;
+    }
+    if (sw_out(ctx, W, &t)) {   // X^{t, u1} (this rank's last sweep) for rank + 1
+        CU(cudaMemcpy2DAsync(ctx->sendbuf, sizeof(double), ctx->x[(ctx->cur + t + Kg) % 2] + t,
+                             ctx->pitch * sizeof(double), sizeof(double), rows, cudaMemcpyDeviceToDevice, ctx->stream));
+        ctx->send_dirty = false;
+    }
+    return BIOT_OK;
+}
+
+// One wave of the wavefront: window of steps whose sweeps 1..K (local numbering) update at
+// wave w; history slots kbase + sweep - 1.
+biot_status gs_window(biot_ctx *ctx, int w, int K, int64_t kbase) {
+    const int L = ctx->n_tl, g0 = ctx->first_step - 1;
     const int lo = std::max(0, w - K + 1 - g0), hi = std::min(L - 1, w - g0);
     if (lo > hi) return BIOT_OK;   // the wavefront is not in this slab
     const int r = (ctx->cur + w) % 2;
@@ -1897,7 +1995,7 @@ biot_status gs_run_wave(biot_ctx *ctx) {
         win.ghost = ctx->x[r] + (win.t_off - 1);
         win.stride = ctx->pitch;
     }
-    win.send = (ctx->world > 1 && hi == L - 1) ? ctx->sendbuf : nullptr;
+    win.send = (ctx->world > 1 && hi == L - 1 && !ctx->sweep_mode) ? ctx->sendbuf : nullptr;
     int64_t wave_groups = ctx->groups;
     if (ctx->gs_k > 0) {   // Alg. 3 literal: a GMRES(k) cycle per step of the window
         biot_status st = gmres_cycle(ctx, ctx->gs_k, ctx->tmap[r], ctx->x[r], ctx->x[1 - r], win);
@@ -1911,7 +2009,7 @@ biot_status gs_run_wave(biot_ctx *ctx) {
         if (mode == biot::MODE_P1_PASS1) CU(launch_pass2_any(ctx, ctx->x[r], ctx->x[1 - r], win.send, &win));
         wave_groups = groups_of(ctx, mode);
     }
-    CU(biot::launch_finalize_wave(ctx->partial, (int)wave_groups, win.len, win.t_off, lo, ctx->gs_k0 + w - g0,
+    CU(biot::launch_finalize_wave(ctx->partial, (int)wave_groups, win.len, win.t_off, lo, kbase + w - g0,
                                   ctx->hist_cap, L, ctx->hist, ctx->nonfinite, ctx->fin_scratch, ctx->stream));
     if (win.send) ctx->send_dirty = false;
     return BIOT_OK;
@@ -1931,6 +2029,8 @@ biot_status biot_gs_begin_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
     if (ctx->kern != 4 && ctx->kern != 6)
         return fail(ctx, BIOT_E_STATE, "Gauss-Seidel in time needs a tile kernel (structured 2D / 3D mesh)");
     if (ctx->gs_K) return fail(ctx, BIOT_E_STATE, "a Gauss-Seidel run is already open");
+    if (ctx->sweep_mode && K < ctx->world)
+        return fail(ctx, BIOT_E_INVALID, "sweep partition: K must be >= world (at least one sweep per rank)");
     CU(cudaSetDevice(ctx->device));
     ctx->gs_K = K;
     ctx->gs_k = k;
@@ -1964,8 +2064,10 @@ biot_status biot_gs_end(biot_ctx *ctx) {
     if (ctx->gs_w != ctx->n_t + ctx->gs_K - 1) return fail(ctx, BIOT_E_STATE, "waves of the run still pending");
     CU(cudaSetDevice(ctx->device));
     const int K = ctx->gs_K;
-    // global step g0 + t ends in panel (cur + g0 + t + K) % 2: gather it into cur'
-    ctx->cur = (ctx->cur + K + ctx->first_step - 1) % 2;
+    // global step g0 + t ends in panel (cur + g0 + t + K) % 2 (sweep partition: this rank's
+    // K_g sweeps): gather it into cur'
+    const int Kl = ctx->sweep_mode ? sw_u1(ctx) - sw_u0(ctx) + 1 : K;
+    ctx->cur = (ctx->cur + Kl + ctx->first_step - 1) % 2;
     biot_status st = gs_parity_copy(ctx, ctx->x[1 - ctx->cur], ctx->x[ctx->cur], 1);
     if (st != BIOT_OK) return st;
     CU(cudaEventRecord(ctx->ev_b, ctx->stream));
@@ -1988,12 +2090,15 @@ biot_status biot_gs_end(biot_ctx *ctx) {
     return BIOT_OK;
 }
 
+static biot_status iterate_gs_sweeps(biot_ctx *ctx, int32_t K, int32_t k);
+
 biot_status biot_iterate_gs_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
     if (!ctx) return fail(nullptr, BIOT_E_INVALID, "ctx is NULL");
     if (K < 0) return fail(ctx, BIOT_E_INVALID, "K must be >= 0");
     if (K == 0) return BIOT_OK;
     if (ctx->world > 1 && (ctx->flags & BIOT_FLAG_MANUAL_HALO))
         return fail(ctx, BIOT_E_STATE, "manual halo: drive the waves with biot_gs_begin/wave/end");
+    if (ctx->sweep_mode) return iterate_gs_sweeps(ctx, K, k);
     NcclApi *api = ctx->world > 1 ? nccl() : nullptr;
     if (ctx->world > 1 && (!api || !ctx->comm)) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
     biot_status st = biot_gs_begin_gmres(ctx, K, k);
@@ -2013,6 +2118,35 @@ biot_status biot_iterate_gs_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
         if (st != BIOT_OK) return st;
     }
     return biot_gs_end(ctx);
+}
+
+// Sweep partition over NCCL: lockstep global waves; at the start of wave W every rank sends
+// the slice it finished at wave W - 1 and receives the one it starts from at W; at the end
+// the last rank's x^K is broadcast so that every rank continues from it.
+static biot_status iterate_gs_sweeps(biot_ctx *ctx, int32_t K, int32_t k) {
+    NcclApi *api = nccl();
+    if (!api || !ctx->comm || !api->Bcast) return fail(ctx, BIOT_E_NCCL, "NCCL not initialised");
+    biot_status st = biot_gs_begin_gmres(ctx, K, k);
+    if (st != BIOT_OK) return st;
+    const size_t n = (size_t)ctx->N * ctx->nc;
+    for (int W = 0; W < ctx->n_t + K - 1; ++W) {
+        int ti, to;
+        const bool rin = sw_in(ctx, W, &ti), sout = W > 0 && sw_out(ctx, W - 1, &to);
+        if (rin || sout) {
+            ncclResult_t r = api->GroupStart();
+            if (r == ncclSuccess && sout) r = api->Send(ctx->sendbuf, n, ncclFloat64, ctx->rank + 1, ctx->comm, ctx->stream);
+            if (r == ncclSuccess && rin) r = api->Recv(ctx->sweep_in, n, ncclFloat64, ctx->rank - 1, ctx->comm, ctx->stream);
+            ncclResult_t r2 = api->GroupEnd();
+            if (r != ncclSuccess || r2 != ncclSuccess) return fail(ctx, BIOT_E_NCCL, "NCCL sweep-pipeline exchange failed");
+        }
+        if ((st = gs_run_wave(ctx)) != BIOT_OK) return st;
+    }
+    if ((st = biot_gs_end(ctx)) != BIOT_OK) return st;
+    const size_t panel = (size_t)ctx->rows_alloc * ctx->pitch;
+    ncclResult_t r = api->Bcast(ctx->xbase[ctx->cur], ctx->xbase[ctx->cur], panel, ncclFloat64, ctx->world - 1,
+                                ctx->comm, ctx->stream);
+    if (r != ncclSuccess) return fail(ctx, BIOT_E_NCCL, "NCCL broadcast of x^K failed");
+    return wait_stream(ctx);
 }
 
 biot_status biot_iterate_gs(biot_ctx *ctx, int32_t K) { return biot_iterate_gs_gmres(ctx, K, 0); }
@@ -2279,6 +2413,12 @@ biot_status biot_set_ghost(biot_ctx *ctx, const double *x) {
     if (ctx->rank == 0 && ctx->world > 1)
         return fail(ctx, BIOT_E_STATE, "rank 0's ghost is x_0 (fixed)");
     CU(cudaSetDevice(ctx->device));
+    if (ctx->sweep_mode) {   // the predecessor's finished slice for the next wave
+        CU(cudaMemcpyAsync(ctx->sweep_in, x, (size_t)ctx->N * ctx->nc * sizeof(double), cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        return BIOT_OK;
+    }
     if (ctx->rank == 0) ctx->x0_zero = false;   // a replaced x_0 is no longer known to be zero
     CU(cudaMemcpyAsync(ctx->ghost, x, (size_t)ctx->N * ctx->nc * sizeof(double), cudaMemcpyHostToDevice,
                        ctx->stream));

@@ -75,6 +75,7 @@ struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_
 
 
 // Arguments of the TMA-pipelined 2D tile kernel (tile2d_kernels.cu).
+constexpr int kAuxRecU = 16;
 struct Tile2dArgs : SweepArgs {
     static constexpr int kAux = 16;   // per-node record: AA_pp per slot [7], f [3], dinv [3], path flag
     static constexpr int kAuxML = 24; // kMaxLoads kernels: + the further load vectors F_j at [14 + 3 (j-1) + c]
@@ -88,6 +89,12 @@ struct Tile2dArgs : SweepArgs {
     int32_t t_lo;                     // window steps below t_lo are computed but not stored or counted
     int32_t s0;                       // zero-storage variant: extra structural zeros (see tile2d)
     int32_t dry;                      // dev/measurement only: stream the ring without computing
+    // aux-uniform rectangle (single-load problems with uniform coefficients, e.g. config 3):
+    // every node with ux0 <= column <= ux1 and uy0 <= row <= uy1 has the aux record aux_u
+    // (pp entries against fixed pressure columns may differ: they multiply x = 0), so row
+    // strips inside it skip the aux bulk copy and read aux_u (staged once in shared memory)
+    int32_t aux_geo, ux0, ux1, uy0, uy1;
+    double aux_u[kAuxRecU];
 };
 
 // Arguments of the TMA-pipelined 3D tile kernel (tile3d_kernels.cu): structured

@@ -436,6 +436,11 @@ struct Geo2 {
 
 __device__ __forceinline__ int axis_class(int v, int n) { return v == 0 ? 0 : (v == n - 1 ? 2 : 1); }
 
+// the 12 aux records of grid row r from column c0 are all aux_u (see Tile2dArgs::aux_geo)
+__device__ __forceinline__ bool seg_uniform(const Tile2dArgs &a, int r, int c0) {
+    return a.aux_geo && r >= a.uy0 && r <= a.uy1 && c0 >= a.ux0 && c0 + kSeg - 1 <= a.ux1;
+}
+
 // Block = 3 consumer warpgroups + 1 producer warpgroup (only its first lane issues
 // copies); the producer group hands its registers to the consumers (setmaxnreg:
 // 4 x 32 x 24 + 12 x 32 x 160 <= 65536).
@@ -453,6 +458,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     __shared__ uint64_t full[kStages], empty[kStages];
     double *cls_sm = reinterpret_cast<double *>(smem + kClsOff);     // [9][7][kCW]
     double *qcarry = reinterpret_cast<double *>(smem + kCarryOff);   // [kMaxRR][kSeg]
+    __shared__ __align__(16) double aux_u[kAuxRecU];                 // the aux-uniform record
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const Geo2 g(a);
@@ -466,6 +472,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
     if constexpr (NL == 1)
         for (int k = threadIdx.x; k < 9 * 7 * kCW; k += blockDim.x) cls_sm[k] = a.cls[k];
+    if (threadIdx.x < kAuxRecU) aux_u[threadIdx.x] = a.aux_u[threadIdx.x];
     __syncthreads();
 
     if (warp >= kSeg) {
@@ -481,7 +488,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const int st = it % kStages;
                         if (it >= (uint32_t)kStages) mbar_wait_suspend(&empty[st], ((it / kStages) - 1) & 1);
                         unsigned char *base = smem + (size_t)st * kStageBytes;
-                        const bool real = (r >= 0 && r < g.nrows);
+                        const bool real = (r >= 0 && r < g.nrows) && !(NL == 1 && seg_uniform(a, r, i0));
                         mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
                         const int64_t node0 = (int64_t)r * g.W + i0 - 1;
                         load_2d(base, &tmx, a.t_off + chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
@@ -565,8 +572,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 const double *pm = reinterpret_cast<const double *>(smem + (size_t)sm_ * kStageBytes);
                 if (a.dry != 1) {
                     if (kindP != 0) {            // finish row m-1
-                        const double *aux = reinterpret_cast<const double *>(
-                                                reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
+                        const double *aux = (NL == 1 && seg_uniform(a, m - 1, i0)) ? aux_u
+                                            : reinterpret_cast<const double *>(
+                                                  reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
                         const int64_t i = (int64_t)(m - 1) * g.W + col;
                         double *carry = qcarry + (m - 1 - ja) * kSeg + warp;
                         if constexpr (MODE == MODE_PASS2) {
@@ -586,8 +594,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     }
                     kindP = 0;
                     if (m < jb && valid) {       // start row m
-                        const double *aux = reinterpret_cast<const double *>(
-                                                reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                        const double *aux = (NL == 1 && seg_uniform(a, m, i0)) ? aux_u
+                                            : reinterpret_cast<const double *>(
+                                                  reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
                         kindP = aux[13] == 1.0 ? 1 : 2;
                         if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, g.nrows)) * 7 * kCW;
                         if constexpr (MODE == MODE_PASS2) {   // bt rides in q
@@ -830,6 +839,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     __shared__ uint64_t zbar[2];                                         // z_u row published (per buffer)
+    __shared__ __align__(16) double aux_u[kAuxRecU];                     // the aux-uniform record
     double *zbuf = reinterpret_cast<double *>(smem + L::kZOff);          // [2][12][2][kCT]
     double *qcarry = reinterpret_cast<double *>(smem + L::kCarryOff);    // [kMaxRR + 1][kSeg]
 
@@ -847,6 +857,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         mbar_init(&zbar[1], kSeg * 32);
         fence_barrier_init();
     }
+    if (threadIdx.x < kAuxRecU) aux_u[threadIdx.x] = a.aux_u[threadIdx.x];
     __syncthreads();
 
     if (warp >= kSeg) {
@@ -861,7 +872,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         const int st = it % kStages;
                         if (it >= (uint32_t)kStages) mbar_wait_suspend(&empty[st], ((it / kStages) - 1) & 1);
                         unsigned char *base = smem + (size_t)st * kStageBytes;
-                        const bool real = (r >= 0 && r < nrows);
+                        const bool real = (r >= 0 && r < nrows) && !(NL == 1 && seg_uniform(a, r, i0 - 1));
                         mbar_expect_tx(&full[st], kXBytes + (real ? kAuxBytes : 0u));
                         const int64_t node0 = (int64_t)r * W + i0 - 2;
                         load_2d(base, &tmx, a.t_off + chunk * kCT, (int)((node0 + a.pad_nodes) * 3), &full[st]);
@@ -938,8 +949,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 if (m >= ja) {
                     double *zd = zrow + (p - 1) * 2 * kCT + lane * 2;
                     if (kindP != 0) {
-                        const double *aux = reinterpret_cast<const double *>(
-                                                reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
+                        const double *aux = (NL == 1 && seg_uniform(a, m - 1, i0 - 1)) ? aux_u
+                                            : reinterpret_cast<const double *>(
+                                                  reinterpret_cast<const unsigned char *>(pd) + kXBytes) + warp * kAuxRec;
                         const int64_t i = (int64_t)(m - 1) * W + col;
                         double *carry = qcarry + (orow1 ? (m - 1 - ja) : kMaxRR) * kSeg + warp;
                         const bool own = orow1 && ocol;
@@ -969,8 +981,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 // exchange, so it overlaps the other warps' publishing
                 int kindC = 0;
                 if (m <= jb && valid && m >= 0 && m < nrows) {
-                    const double *aux = reinterpret_cast<const double *>(
-                                            reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
+                    const double *aux = (NL == 1 && seg_uniform(a, m, i0 - 1)) ? aux_u
+                                        : reinterpret_cast<const double *>(
+                                              reinterpret_cast<const unsigned char *>(pm) + kXBytes) + warp * kAuxRec;
                     kindC = aux[13] == 1.0 ? 1 : 2;
                     kindP = kindC;
                     if (kindP == 2) T = cls_base + (ccx + 3 * axis_class(m, nrows)) * 7 * kCW;

@@ -11,18 +11,20 @@
 // operands, structural zeros skipped), the face / edge / corner ones (geometric
 // classes) in shared memory -- and the x values come from shared memory staged by TMA.
 //
-// Work tile = a 4x2 (x, y) node patch x a z range, for every 64-step time chunk;
+// Work tile = a 4x3 (x, y) node patch x a z range, for every 64-step time chunk;
 // every lane carries TWO consecutive steps (2l, 2l+1), so one 16-B shared-memory load
 // brings both steps of a column component and every coefficient (an LDCU into a
 // uniform register: DFMA takes no constant-bank operand on sm_100a) feeds two DFMAs.
 // One lane of a producer warpgroup streams, per z plane, one 4D TMA box {64 steps,
-// 6 x-nodes x 4 comps, 4 y-rows, 1 plane} (patch + halo; out-of-mesh positions are
-// zero-filled) and the 8 patch nodes' aux records (kappa-dependent AA_pp per slot,
-// load, preconditioner diagonals, path flag) into a 4-stage ring.  8 consumer warps
+// 6 x-nodes x 4 comps, 5 y-rows, 1 plane} (patch + halo; out-of-mesh positions are
+// zero-filled) and the 12 patch nodes' aux records (kappa-dependent AA_pp per slot,
+// load, preconditioner diagonals, path flag) into a 3-stage ring.  12 consumer warps
 // (one node each) march z holding only two planes: at step m (planes m-1, m resident)
 // a warp finishes its node of plane m-1 (the z+1 columns, from plane m, then the
 // epilogue) and starts its node of plane m (z-1 and z columns); the partial sums ride
-// in registers (setmaxnreg: 240 per consumer thread).  Every node's FMAs run in the
+// in registers (setmaxnreg: 160 per consumer thread).  Measured (config 4): 4x4 patch,
+// one step per lane, 32-step chunks: 4.87 ms; 4x2 patch, 8 warps, 4 stages: 4.18 ms; 4x3,
+// 12 warps, 3 stages: 3.90 ms (the largest patch whose 3 stages fit 227 KB).  Every node's FMAs run in the
 // fixed (dz, dy, dx) column order.
 //
 // Previous-step coupling (A' x_{n-1})_p: step 2l+1 uses the lane's own q(2l); step
@@ -45,26 +47,26 @@ namespace {
 using namespace dev;
 using namespace tma;
 
-constexpr int kBX = 4, kBY = 2;            // patch (nodes): x, y
+constexpr int kBX = 4, kBY = 3;            // patch (nodes): x, y (4x3: 12 consumer warps)
 constexpr int kSX = kBX + 2, kSY = kBY + 2;   // staged incl. halo
 constexpr int kNodes = kBX * kBY;          // consumer warps (one node each)
 constexpr int kT3 = 2;                     // time steps per lane
 constexpr int kTc = 32 * kT3;              // time steps per chunk
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 constexpr int kMaxZ = 24;                  // planes per tile (q carry capacity)
 constexpr int kCW = Tile3dArgs::kClsW;     // doubles per class-stencil slot
 constexpr int kClsD = 272;                 // doubles per class stencil in shared memory (15*18 padded)
 constexpr int kClsLocal = 8;               // classes a tile can touch: 2 (x) x 2 (y) x 2 (z; one z face per tile)
-constexpr uint32_t kXBytes = kSX * kSY * 4 * kTc * 8;                          // 49152
+constexpr uint32_t kXBytes = kSX * kSY * 4 * kTc * 8;                          // 61440
 constexpr uint32_t kAuxRec = Tile3dArgs::kAux;                                 // doubles per record
 constexpr uint32_t kAuxRowBytes = kBX * kAuxRec * 8;                           // 768
-constexpr uint32_t kAuxBytes = kBY * kAuxRowBytes;                             // 1536
-constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;      // 50688
+constexpr uint32_t kAuxBytes = kBY * kAuxRowBytes;                             // 2304
+constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;      // 63744
 constexpr uint32_t kClsOff = kStages * kStageBytes;
 constexpr uint32_t kCarryOff = kClsOff + kClsLocal * kClsD * 8;
 constexpr uint32_t kSmemBytes = kCarryOff + kMaxZ * kNodes * 8;
 constexpr int kThreads3 = (kNodes + 4) * 32;
-constexpr int kProducerRegs = 24, kConsumerRegs = 240;   // 4*32*24 + 8*32*240 <= 65536
+constexpr int kProducerRegs = 24, kConsumerRegs = 160;   // 4*32*24 + 12*32*160 <= 65536
 static_assert(kSmemBytes + kNodes * kTc * 2 * 8 + 2 * kStages * 8 <= 232448, "tile3d shared memory exceeds 227 KB");
 
 // (dx, dy, dz) of the 15 BDIA slots in storage order (offsets sorted ascending,

@@ -235,3 +235,24 @@ def test_gs_gmres_time_slabs_bitwise():
     for g in ranks:
         g.gs_end()
     assert np.array_equal(np.concatenate([g.solution() for g in ranks]), xr)
+
+
+@pytest.mark.parametrize("precond", [2, 1])
+def test_aux_uniform_skip_bitwise(precond, monkeypatch):
+    """Uniform coefficients (config 3's kind: S = 0, one kappa): row strips inside the
+    aux-uniform rectangle skip the aux-record copy and read the shared record; iterates and
+    norms are bitwise those of the run that streams every record (BIOT_NO_AUX_SKIP=1)."""
+    prob = make_problem(2, 64, 256, 1e-3, 5, storage=0.0, kappa_median=1e-6, x0_seed=5)
+    res = []
+    for skip in (False, True):
+        if skip:
+            monkeypatch.delenv("BIOT_NO_AUX_SKIP", raising=False)
+        else:
+            monkeypatch.setenv("BIOT_NO_AUX_SKIP", "1")
+        g = _seeded(prob, 256, precond=precond, omega=0.5 if precond == 2 else 0.3)
+        g.iterate(5)
+        res.append((g.solution(), [g.residual_history(k) for k in range(5)], g.residual_norms()))
+        g.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][1], res[1][1]))
+    assert np.array_equal(res[0][2], res[1][2])
