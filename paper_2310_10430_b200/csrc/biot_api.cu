@@ -157,7 +157,7 @@ struct biot_ctx {
     // every rank holds all steps; sweep_in receives the predecessor rank's finished slices
     bool sweep_mode = false;
     double *sweep_in = nullptr;
-    double *sendbuf2 = nullptr, *zero_ghost_base = nullptr, *zero_ghost = nullptr, *zu0 = nullptr, *part0 = nullptr;
+    double *sendbuf2 = nullptr, *zero_ghost_base = nullptr, *zero_ghost = nullptr, *s0buf = nullptr, *part0 = nullptr;
     const double *ghost_override = nullptr;
     int step0_blocks = 0;
     cudaStream_t comm_stream = nullptr;
@@ -268,7 +268,7 @@ void free_all(biot_ctx *c) {
     cudaSetDevice(c->device);
     for (void *p : {(void *)c->xbase[0], (void *)c->xbase[1], (void *)c->zbase, (void *)c->ghost_base,
                     (void *)c->blk, (void *)c->cols, (void *)c->load, (void *)c->loadx, (void *)c->dinv, (void *)c->s,
-                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->zu0, (void *)c->sweep_in,
+                    (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->s0buf, (void *)c->sweep_in,
                     (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
@@ -331,6 +331,8 @@ biot::SweepArgs sweep_args(biot_ctx *c, int mode, const double *xin, double *xou
     a.ghost_zero = (c->ghost_override && c->ghost_override == c->zero_ghost) ||
                    ((c->rank == 0 || c->sweep_mode) && c->x0_zero) ? 1 : 0;
     a.p1_out = (c->precond == 1 && (mode == biot::MODE_ZOUT || mode == biot::MODE_MATVEC)) ? 1 : 0;
+    // the deferred sweep saves the ghost-independent pieces of its first step's p-update
+    a.s0buf = (c->ghost_override && c->ghost_override == c->zero_ghost) ? c->s0buf : nullptr;
     return a;
 }
 
@@ -677,18 +679,20 @@ biot_status complete_step0(biot_ctx *ctx, int mode, const double *xin, double *x
         static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, xin, xout);
         a.ghost = ctx->ghost;
         a.ghost_zero = 0;
+        a.s0buf = ctx->s0buf;
         std::memcpy(a.tmpl, ctx->tmpl, sizeof(a.tmpl));
         a.aux = ctx->aux;
         a.cls = ctx->cls;
         a.pad_nodes = ctx->pad;
         a.ghost_stride = 1;
         a.s0 = ctx->s0;
-        CU(biot::launch_tile2d_step0(a, ctx->zu0, ctx->part0, ctx->stream));
+        CU(biot::launch_tile2d_step0(a, ctx->part0, ctx->stream));
     } else {
         biot::Tile3dArgs a{};
         static_cast<biot::SweepArgs &>(a) = sweep_args(ctx, mode, xin, xout);
         a.ghost = ctx->ghost;
         a.ghost_zero = 0;
+        a.s0buf = ctx->s0buf;
         std::memcpy(a.tmpl, ctx->tmpl3, sizeof(a.tmpl));
         a.aux = ctx->aux;
         a.cls = ctx->cls;
@@ -696,10 +700,9 @@ biot_status complete_step0(biot_ctx *ctx, int mode, const double *xin, double *x
         a.z_rows = ctx->z_rows;
         a.s0 = ctx->s0;
         a.ghost_stride = 1;
-        CU(biot::launch_tile3d_step0(a, ctx->zu0, ctx->part0, ctx->stream));
+        CU(biot::launch_tile3d_step0(a, ctx->part0, ctx->stream));
     }
-    CU(biot::launch_finalize(ctx->part0, ctx->step0_blocks, 1, hslot, ctx->nonfinite,
-                             ctx->part0 + 2 * ctx->step0_blocks, ctx->stream));
+    CU(biot::launch_finalize_p0(ctx->part0, ctx->step0_blocks, hslot, ctx->nonfinite, ctx->stream));
     return BIOT_OK;
 }
 
@@ -1501,11 +1504,10 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ALLOC(ctx->zero_ghost_base, (size_t)ctx->rows_alloc * sizeof(double));
         CU(cudaMemsetAsync(ctx->zero_ghost_base, 0, (size_t)ctx->rows_alloc * sizeof(double), ctx->stream));
         ctx->zero_ghost = ctx->zero_ghost_base + ctx->pad * nc;
-        ALLOC(ctx->zu0, (size_t)ctx->N * (ctx->nc - 1) * sizeof(double));
+        ALLOC(ctx->s0buf, (size_t)ctx->N * 4 * sizeof(double));
+        CU(cudaMemsetAsync(ctx->s0buf, 0, (size_t)ctx->N * 4 * sizeof(double), ctx->stream));
         ctx->step0_blocks = ctx->kern == 4 ? biot::tile2d_step0_blocks(ctx->N) : biot::tile3d_step0_blocks(ctx->N);
-        // step-0 norm partials [blocks][2] + the two-stage finalize's scratch behind them
-        ALLOC(ctx->part0, (size_t)(ctx->step0_blocks * 2 + std::max<int64_t>(1, biot::finalize_scratch_doubles(ctx->step0_blocks, 1))) *
-                              sizeof(double));
+        ALLOC(ctx->part0, (size_t)ctx->step0_blocks * sizeof(double));   // step-0 p-norm partials
     }
 
     const int nwp = 8 / ctx->tw;

@@ -47,6 +47,15 @@ struct Loads {
         for (int j = 1; j < NL; ++j) l = fma(sv[j][tt], F[j][c], l);
         return l;
     }
+    // the load plus `add` with explicit fused multiply-adds (term 0 first): no rounding
+    // left to the compiler's contraction choices, so a kernel that completes the update
+    // later (the deferred first step of the overlapped halo) reproduces it bitwise
+    __device__ __forceinline__ double at_plus(int c, int tt, double add) const {
+        double l = __fma_rn(sv[0][tt], F[0][c], add);
+#pragma unroll
+        for (int j = 1; j < NL; ++j) l = __fma_rn(sv[j][tt], F[j][c], l);
+        return l;
+    }
 };
 
 template <int NC, int T>
@@ -73,7 +82,7 @@ __device__ __forceinline__ void epilogue_math(double omega, const double (&acc)[
         double r[NC];
 #pragma unroll
         for (int c = 0; c < D; ++c) r[c] = ld.at(c, tt) - acc[c][tt];
-        r[D] = (ld.at(D, tt) + qp) - acc[D][tt];
+        r[D] = __dsub_rn(ld.at_plus(D, tt, qp), acc[D][tt]);
         // Dirichlet rows (D^{-1} = 0) carry no residual: kernels that apply a shared
         // stencil to such rows (tile3d class templates) rely on this mask
         if constexpr (MASK) {

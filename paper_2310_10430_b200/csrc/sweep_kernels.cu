@@ -288,6 +288,28 @@ cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int
     return cudaGetLastError();
 }
 
+__global__ void finalize_p0_kernel(const double *__restrict__ part, int blocks, double *hist_slot, int *nonfinite) {
+    __shared__ double red[256];
+    double s = 0.0;
+    for (int b = threadIdx.x; b < blocks; b += 256) s += part[b];
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double v = sqrt(red[0]);
+        hist_slot[1] = v;
+        if (!isfinite(v)) atomicOr(nonfinite, 1);
+    }
+}
+
+cudaError_t launch_finalize_p0(const double *part, int blocks, double *hist_slot, int *nonfinite, cudaStream_t st) {
+    finalize_p0_kernel<<<1, 256, 0, st>>>(part, blocks, hist_slot, nonfinite);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int lo, int t_first, int64_t k0,
                                  int cap, int n_tl, double *hist, int *nonfinite, double *scratch, cudaStream_t st) {
     dim3 block(32, 8);

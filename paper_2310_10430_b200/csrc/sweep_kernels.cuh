@@ -54,6 +54,9 @@ struct SweepArgs {
                             // deferred sweep of the overlapped halo): q(t0-1) = A' 0 = +0 without loads
     int32_t p1_out;         // GMRES modes (ZOUT / MATVEC) with P~1: write the first half (z_u, r_p) of
                             // P~1^{-1} r; pass2 (pure) then completes z_p in place
+    double *s0buf;          // deferred sweep (overlapped halo): per node, the pieces of the first local
+                            // step's pressure update that do not depend on the ghost:
+                            // [acc_p, -, x_p^k, (B^T z_u)_p] (tile kernels), else null
 };
 
 struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
@@ -147,11 +150,12 @@ void tile2d_box(uint32_t *box);
 cudaError_t tile2d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
-// Deferred first local step (overlapped halo): recompute step t_off of every node with
-// the ghost, overwrite x^{k+1} there, norm partials per block -> part[blocks][2].
-// Modes MODE_UPDATE_P2 and MODE_P1_FUSED (zu0: 2 doubles per node scratch).
+// Deferred first local step (overlapped halo): complete step t_off of every node from the
+// ghost and the pieces the sweep saved in a.s0buf (bitwise the undeferred update),
+// overwrite x_p^{k+1} there; the step's pressure-norm partials per block -> part[blocks].
+// Modes MODE_UPDATE_P2 and MODE_P1_FUSED.
 int tile2d_step0_blocks(int64_t n_nodes);
-cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *zu0, double *part, cudaStream_t st);
+cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *part, cudaStream_t st);
 
 // 3D TMA tile kernel: 4x2 (x,y) node patches x 64-step chunks, marching z
 int64_t tile3d_groups(const Tile3dArgs &a);
@@ -164,9 +168,10 @@ cudaError_t tile3d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);
 // deferred first local step (see launch_tile2d_step0): MODE_UPDATE_P2 or MODE_P1_PASS1
-// (the two-pass P~1; zu0: 3 doubles per node scratch)
 int tile3d_step0_blocks(int64_t n_nodes);
-cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *zu0, double *part, cudaStream_t st);
+cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *part, cudaStream_t st);
+// hist_slot[1] = sqrt(fixed-order sum of part[0..blocks)): the completed step's p-norm
+cudaError_t launch_finalize_p0(const double *part, int blocks, double *hist_slot, int *nonfinite, cudaStream_t st);
 
 // Per-step GMRES panel kernels (gmres_kernels.cu): column-wise (per time step) dot
 // products of a panel with nb panels (b_dev: device array of panel pointers) and

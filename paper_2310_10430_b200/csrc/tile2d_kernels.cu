@@ -268,6 +268,10 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
         }
         epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2,
                                                     outx, outz, !a.p1_out);
+        if (MODE == MODE_UPDATE_P2 && a.s0buf && h == 0 && t0 == 0) {   // deferred first step (lane 0)
+            a.s0buf[i * 4 + 0] = acc2[2][0];
+            a.s0buf[i * 4 + 2] = xs2[2][0];
+        }
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
             nu[2 * h + tt] = nu2[tt];
@@ -764,6 +768,10 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
             }
         }
         epilogue_math<2, 2, CLS, false>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2, outx, outz);
+        if (a.s0buf && own && h == 0 && t0 == 0) {   // deferred first step (lane 0)
+            a.s0buf[i * 4 + 0] = acc2[2][0];
+            a.s0buf[i * 4 + 2] = xs2[2][0];
+        }
         const int th = t0 + h * (kCT / 2);
         // z_u published for the neighbours; the pressure part waits for B^T z_u:
         // x_p^{k+1} = x_p + omega D_S^{-1} (bt - r_p) = y + (omega D_S^{-1}) bt
@@ -807,6 +815,7 @@ template <class A>
 __device__ __forceinline__ void finish_zp(const A &a, int64_t i, int t0, bool whole, double wdv,
                                           const double (&bt)[kT2], const double (&y)[kT2]) {
     const int64_t P = a.pitch, row = i * 3 * P + 2 * P + a.t_off + t0;
+    if (a.s0buf && t0 == 0) a.s0buf[i * 4 + 3] = bt[0];   // deferred first step (lane 0)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const double v0 = fma(wdv, bt[2 * h], y[2 * h]);
@@ -1072,142 +1081,49 @@ __global__ void __launch_bounds__(kThreads2, 1)
 // ============================================================================
 // Deferred first step (overlapped time-slab halo): the sweep of a rank
 // r > 0 runs while the ghost x^k_{first-1} is still in flight, with a zero ghost, so
-// only the p-residual of the slab's first local step is wrong (A' enters through
-// q(t0-1) alone).  Once the ghost has arrived this kernel recomputes that step for
-// every node -- one thread per node, the tile kernel's slot order (ascending offsets),
-// coefficient sources (template / class / aux) and epilogue, so x^{k+1} is bitwise the
-// value the undeferred sweep would store -- overwrites it, and reduces the step's norm
-// partials per block in a fixed order.  Fused P~1 needs z_u of the neighbours at that
-// step: phase 0 writes it for every node, phase 1 completes the step.
+// only the pressure update of the slab's first local step is wrong (A' enters through
+// q(t0-1) alone).  The sweep saves, per node, the pieces of that update the ghost does
+// not touch (a.s0buf: acc_p, load_p, x_p^k and, for the fused P~1, B^T z_u); once the
+// ghost has arrived this kernel (one thread per node) forms q(t0-1) in the sweep's order,
+// r_p = (load_p + q) - acc_p and the sweep's update formula, so x^{k+1} is bitwise the
+// undeferred value, and reduces the step's pressure-norm contributions per block.
 // ============================================================================
-template <bool CLS, bool S0>
-__device__ __forceinline__ void col_residual(const Tile2dArgs &a, int64_t i, const double *col, int64_t stride,
-                                             const double *aux, const double *T, double (&acc)[3], double &q) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) acc[c] = 0.0;
-    q = 0.0;
-#pragma unroll
-    for (int dr = -1; dr <= 1; ++dr)
-#pragma unroll
-        for (int dc = -1; dc <= 1; ++dc) {
-            const int s = slot2(dr, dc);
-            if (s < 0) continue;
-            const int64_t j = i + a.off[s];
-            double v[3];
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) v[cc] = __ldg(col + (j * 3 + cc) * stride);
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc) {
-                if constexpr (CLS) {
-                    const double *Ts = T + s * kCW;
-                    acc[0] = fma(Ts[cc * 3], v[cc], acc[0]);
-                    acc[1] = fma(Ts[cc * 3 + 1], v[cc], acc[1]);
-                    acc[2] = fma(cc == 2 ? aux[s] : Ts[cc * 3 + 2], v[cc], acc[2]);
-                    q = fma(cc < 2 ? Ts[cc * 3 + 2] : Ts[9], v[cc], q);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const int e = c * 3 + cc;
-                        if (tmpl_zero(s, e, S0)) continue;
-                        acc[c] = fma(e == 8 ? aux[s] : a.tmpl[s][e], v[cc], acc[c]);
-                    }
-                    const int eq = cc < 2 ? 6 + cc : 9;
-                    if (!tmpl_zero(s, eq, S0)) q = fma(a.tmpl[s][eq], v[cc], q);
-                }
-            }
-        }
-}
-
 template <bool S0, int MODE, int NL>
-__global__ void __launch_bounds__(256) tile2d_step0_kernel(const Tile2dArgs a, int phase, double *zu0, double *part) {
+__global__ void __launch_bounds__(256) tile2d_step0_kernel(const Tile2dArgs a, double *part) {
     constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
     const int64_t N = a.n_nodes, P = a.pitch;
     const int W = (int)a.row_w;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const double *col = a.x + a.t_off;            // x^k of the first local step, stride = pitch
-    double su = 0.0, sp = 0.0;
+    double sp = 0.0;
     if (i < N) {
         const double *aux = a.aux + i * kAuxRec;
         const bool intr = aux[13] == 1.0;
         const double *T = a.cls + (axis_class((int)(i % W), W) + 3 * axis_class((int)(i / W), a.n_rows)) * 7 * kCW;
-        double acc[3], q;
-        if (intr) col_residual<false, S0>(a, i, col, P, aux, T, acc, q);
-        else col_residual<true, S0>(a, i, col, P, aux, T, acc, q);
-        if constexpr (NL > 1) {
-#pragma unroll
-            for (int jt = 1; jt < NL; ++jt) {
-                const double sj = a.s[jt * a.s_pitch + a.t_off];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) acc[c] = fma(-sj, aux[14 + 3 * (jt - 1) + c], acc[c]);
-            }
-        }
         const double qp = intr ? ghost_q<false, S0, Tile2dArgs>(a, i, T) : ghost_q<true, S0, Tile2dArgs>(a, i, T);
-        double acc1[3][1], q1[1] = {q}, xs[3][1], nu1[1] = {0.0}, np1[1] = {0.0}, outx[3][1], outz[3][1], Dv[3];
-        Loads<3, 1, 1> ld;
-        ld.sv[0][0] = a.s[a.t_off];
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            acc1[c][0] = acc[c];
-            xs[c][0] = col[(i * 3 + c) * P];
-            Dv[c] = aux[10 + c];
-            ld.F[0][c] = aux[7 + c];
+        const double *sv = a.s0buf + i * 4;
+        const double dv = aux[12];
+        double r = __dsub_rn(__fma_rn(a.s[a.t_off], aux[9], qp), sv[0]);   // epilogue_math's r_p
+        if (dv == 0.0) r = 0.0;                 // Dirichlet pressure row (the epilogue's mask)
+        sp = r * r;
+        double xn;
+        if constexpr (MODE == MODE_P1_FUSED) {   // finish_p1 / finish_zp
+            const double wdv = a.omega * dv;
+            const double y = fma(-wdv, r, sv[2]);
+            xn = fma(wdv, sv[3], y);
+        } else {                                 // P~2: z_p = -D_S^{-1} r_p
+            xn = fma(a.omega, -(dv * r), sv[2]);
         }
-        if (intr) epilogue_math<2, 1, false, false>(a.omega, acc1, q1, qp, ld, Dv, xs, nu1, np1, outx, outz);
-        else epilogue_math<2, 1, true, false>(a.omega, acc1, q1, qp, ld, Dv, xs, nu1, np1, outx, outz);
-        if (MODE == MODE_P1_FUSED && phase == 0) {
-            zu0[i * 2] = outz[0][0];
-            zu0[i * 2 + 1] = outz[1][0];
-            return;
-        }
-        su = nu1[0];
-        sp = np1[0];
-        double *xo = a.xn + i * 3 * P + a.t_off;
-        double out[3] = {outx[0][0], outx[1][0], outx[2][0]};
-        if constexpr (MODE == MODE_P1_FUSED) {
-            // z_p = D_S^{-1} (B^T z_u - r_p), B^T in slot order, as finish_zp of the fused pass
-            const double wdv = a.omega * aux[12];
-            const double y = fma(-wdv, outz[2][0], xs[2][0]);
-            double bt = 0.0;
-#pragma unroll
-            for (int dr = -1; dr <= 1; ++dr)
-#pragma unroll
-                for (int dc = -1; dc <= 1; ++dc) {
-                    const int s = slot2(dr, dc);
-                    if (s < 0) continue;
-                    const int64_t j = i + a.off[s];
-                    if (j < 0 || j >= N) continue;       // off the mesh: z_u = 0 there (the fused pass's zeros)
-#pragma unroll
-                    for (int cc = 0; cc < 2; ++cc) {
-                        if (intr && tmpl_zero(s, 6 + cc, S0)) continue;
-                        const double cf = intr ? a.tmpl[s][6 + cc] : T[s * kCW + cc * 3 + 2];
-                        bt = fma(cf, zu0[j * 2 + cc], bt);
-                    }
-                }
-            out[2] = fma(wdv, bt, y);
-        }
-#pragma unroll
-        for (int c = 0; c < 3; ++c) xo[c * P] = out[c];
-        if (a.sendbuf && a.n_tl == 1)
-#pragma unroll
-            for (int c = 0; c < 3; ++c) a.sendbuf[i * 3 + c] = out[c];
+        a.xn[(i * 3 + 2) * P + a.t_off] = xn;
+        if (a.sendbuf && a.n_tl == 1) a.sendbuf[i * 3 + 2] = xn;
     }
-    if (MODE == MODE_P1_FUSED && phase == 0) return;
-    // fixed-order block reduction of the step's norm contributions
-    __shared__ double red[2][256];
-    red[0][threadIdx.x] = su;
-    red[1][threadIdx.x] = sp;
+    __shared__ double red[256];
+    red[threadIdx.x] = sp;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + w];
-            red[1][threadIdx.x] += red[1][threadIdx.x + w];
-        }
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        part[blockIdx.x * 2] = red[0][0];
-        part[blockIdx.x * 2 + 1] = red[1][0];
-    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
 }  // namespace
@@ -1288,17 +1204,13 @@ cudaError_t launch_tile2d(const CUtensorMap &tmx, const Tile2dArgs &a, const Lau
 
 int tile2d_step0_blocks(int64_t n_nodes) { return (int)((n_nodes + 255) / 256); }
 
-cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *zu0, double *part, cudaStream_t st) {
+cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *part, cudaStream_t st) {
     const int nb = tile2d_step0_blocks(a.n_nodes);
-#define BIOT_S0(S0_, M_, NL_)                                                                \
-    {                                                                                         \
-        if ((M_) == MODE_P1_FUSED) tile2d_step0_kernel<S0_, M_, NL_><<<nb, 256, 0, st>>>(a, 0, zu0, part); \
-        tile2d_step0_kernel<S0_, M_, NL_><<<nb, 256, 0, st>>>(a, 1, zu0, part);              \
-    }
-#define BIOT_S0M(M_)                                                                          \
-    {                                                                                         \
-        if (a.n_load > 1) { if (a.s0) BIOT_S0(true, M_, kMaxLoads) else BIOT_S0(false, M_, kMaxLoads) } \
-        else { if (a.s0) BIOT_S0(true, M_, 1) else BIOT_S0(false, M_, 1) }                   \
+#define BIOT_S0(S0_, M_, NL_) tile2d_step0_kernel<S0_, M_, NL_><<<nb, 256, 0, st>>>(a, part)
+#define BIOT_S0M(M_)                                                                                     \
+    {                                                                                                    \
+        if (a.n_load > 1) { if (a.s0) BIOT_S0(true, M_, kMaxLoads); else BIOT_S0(false, M_, kMaxLoads); } \
+        else { if (a.s0) BIOT_S0(true, M_, 1); else BIOT_S0(false, M_, 1); }                              \
     }
     if (a.mode == MODE_P1_FUSED) BIOT_S0M(MODE_P1_FUSED)
     else if (a.mode == MODE_UPDATE_P2) BIOT_S0M(MODE_UPDATE_P2)

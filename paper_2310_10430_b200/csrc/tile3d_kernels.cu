@@ -268,6 +268,10 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
     }
     epilogue_math<3, kT3, CLS, MODE == MODE_ZOUT>(a.omega, acc, q, qp, single_load(F, sv), Dv, xs, nu, npn, outx, outz,
                                                   !a.p1_out);
+    if ((MODE == MODE_UPDATE_P2 || MODE == MODE_P1_PASS1) && a.s0buf && t == 0) {   // deferred first step
+        a.s0buf[iA * 4 + 0] = acc[3][0];
+        a.s0buf[iA * 4 + 2] = xs[3][0];
+    }
     if constexpr (MODE == MODE_ZOUT) {       // GMRES start: z = P~2^{-1} r, x untouched
 #pragma unroll
         for (int c = 0; c < 4; ++c) store2(a.zbuf + row + c * P, outz[c][0], outz[c][1], t, a.t_lo, a.n_tl);
@@ -345,6 +349,7 @@ __device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po,
     } else if (t < a.n_tl) {
         x0 = __ldg(a.x + row);
     }
+    if (a.s0buf && t == 0) a.s0buf[i * 4 + 3] = bt[0];   // deferred first step
     const double v0 = fma(a.omega, aux[22] * (bt[0] - rp.x), x0);
     const double v1 = fma(a.omega, aux[22] * (bt[1] - rp.y), x1);
     store2(a.xn + row, v0, v1, t, a.t_lo, a.n_tl);
@@ -538,114 +543,38 @@ __global__ void __launch_bounds__(kThreads3, 1)
 }
 
 // Deferred first local step (overlapped time-slab halo; see tile2d_step0_kernel): the
-// step recomputed per node with the ghost, in this kernel's (dz, dy, dx) slot order,
-// coefficient sources and epilogue (bitwise the undeferred sweep's values).  P~1 (two
-// passes here): phase 0 writes z_u of every node, phase 1 completes the step with
-// x_p + omega D_S^{-1} (B^T z_u - r_p) as finish_bt does.
-template <bool CLS, bool S0>
-__device__ __forceinline__ void col_residual3(const Tile3dArgs &a, int64_t i, const double *col, int64_t stride,
-                                              const double *aux, const double *T, double (&acc)[4], double &q) {
-    const int64_t n1 = a.n1;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c] = 0.0;
-    q = 0.0;
-#pragma unroll
-    for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-        for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-            for (int dx = -1; dx <= 1; ++dx) {
-                const int s = slot_of(dx, dy, dz);
-                if (s < 0) continue;
-                const int64_t j = i + ((int64_t)dz * n1 + dy) * n1 + dx;
-                double v[4];
-#pragma unroll
-                for (int cc = 0; cc < 4; ++cc) v[cc] = __ldg(col + (j * 4 + cc) * stride);
-                if constexpr (CLS) fma_cls1(acc, q, T + s * kCW, aux[s], v);
-                else fma_tmpl1<S0>(acc, q, a, s, aux[s], v);
-            }
-}
-
+// pressure update of the first local step completed from the ghost and the pieces the
+// sweep saved (P~1 here is two-pass: pass 1 saves acc_p, load_p, x_p^k, pass 2 B^T z_u).
 template <bool S0, int MODE>
-__global__ void __launch_bounds__(256) tile3d_step0_kernel(const Tile3dArgs a, int phase, double *zu0, double *part) {
+__global__ void __launch_bounds__(256) tile3d_step0_kernel(const Tile3dArgs a, double *part) {
     const int64_t n1 = a.n1, N = a.n_nodes, P = a.pitch;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const double *col = a.x + a.t_off;
-    double su = 0.0, sp = 0.0;
+    double sp = 0.0;
     if (i < N) {
         const double *aux = a.aux + i * kAuxRec;
         const bool intr = aux[23] == 1.0;
         const int x = (int)(i % n1), y = (int)((i / n1) % n1), z = (int)(i / (n1 * n1));
         const double *T = a.cls + (size_t)(axis_class(x, (int)n1) + 3 * axis_class(y, (int)n1) +
                                            9 * axis_class(z, (int)n1)) * (15 * kCW);
-        double acc[4], q;
-        if (intr) col_residual3<false, S0>(a, i, col, P, aux, T, acc, q);
-        else col_residual3<true, S0>(a, i, col, P, aux, T, acc, q);
-        const double g0 = intr ? ghost_q<false, S0>(a.ghost, n1, i, a, T) : ghost_q<true, S0>(a.ghost, n1, i, a, T);
-        double F[4], Dv[4], xs[4][1], acc1[4][1], q1[1] = {q}, sv1[1] = {a.s[a.t_off]}, nu1[1] = {0.0},
-               np1[1] = {0.0}, outx[4][1], outz[4][1];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            F[c] = aux[15 + c];
-            Dv[c] = aux[19 + c];
-            xs[c][0] = col[(i * 4 + c) * P];
-            acc1[c][0] = acc[c];
-        }
-        if (intr) epilogue_math<3, 1, false, false>(a.omega, acc1, q1, g0, single_load(F, sv1), Dv, xs, nu1, np1, outx, outz);
-        else epilogue_math<3, 1, true, false>(a.omega, acc1, q1, g0, single_load(F, sv1), Dv, xs, nu1, np1, outx, outz);
-        if (MODE == MODE_P1_PASS1 && phase == 0) {
-#pragma unroll
-            for (int c = 0; c < 3; ++c) zu0[i * 3 + c] = outz[c][0];
-            return;
-        }
-        su = nu1[0];
-        sp = np1[0];
-        double out[4] = {outx[0][0], outx[1][0], outx[2][0], outx[3][0]};
-        if constexpr (MODE == MODE_P1_PASS1) {
-            double bt = 0.0;
-#pragma unroll
-            for (int dz = -1; dz <= 1; ++dz)
-#pragma unroll
-                for (int dy = -1; dy <= 1; ++dy)
-#pragma unroll
-                    for (int dx = -1; dx <= 1; ++dx) {
-                        const int s = slot_of(dx, dy, dz);
-                        if (s < 0) continue;
-                        const int xx = x + dx, yy = y + dy, zz = z + dz;
-                        if (xx < 0 || yy < 0 || zz < 0 || xx >= n1 || yy >= n1 || zz >= n1) continue;   // zero-filled
-                        const int64_t j = i + ((int64_t)dz * n1 + dy) * n1 + dx;
-#pragma unroll
-                        for (int cc = 0; cc < 3; ++cc) {
-                            if (intr && tmpl3_zero(s, 12 + cc, S0)) continue;
-                            const double cf = intr ? a.tmpl[s][12 + cc] : T[s * kCW + cc * 4 + 3];
-                            bt = fma(cf, zu0[j * 3 + cc], bt);
-                        }
-                    }
-            out[3] = fma(a.omega, aux[22] * (bt - outz[3][0]), xs[3][0]);
-        }
-        double *xo = a.xn + i * 4 * P + a.t_off;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) xo[c * P] = out[c];
-        if (a.sendbuf && a.n_tl == 1)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) a.sendbuf[i * 4 + c] = out[c];
+        const double qp = intr ? ghost_q<false, S0>(a.ghost, n1, i, a, T) : ghost_q<true, S0>(a.ghost, n1, i, a, T);
+        const double *sv = a.s0buf + i * 4;
+        const double dv = aux[22];
+        double r = __dsub_rn(__fma_rn(a.s[a.t_off], aux[18], qp), sv[0]);   // epilogue_math's r_p
+        if (dv == 0.0) r = 0.0;
+        sp = r * r;
+        const double xn = MODE == MODE_P1_PASS1 ? fma(a.omega, dv * (sv[3] - r), sv[2])   // finish_bt
+                                                : fma(a.omega, -(dv * r), sv[2]);         // P~2
+        a.xn[(i * 4 + 3) * P + a.t_off] = xn;
+        if (a.sendbuf && a.n_tl == 1) a.sendbuf[i * 4 + 3] = xn;
     }
-    if (MODE == MODE_P1_PASS1 && phase == 0) return;
-    __shared__ double red[2][256];
-    red[0][threadIdx.x] = su;
-    red[1][threadIdx.x] = sp;
+    __shared__ double red[256];
+    red[threadIdx.x] = sp;
     __syncthreads();
     for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) {
-            red[0][threadIdx.x] += red[0][threadIdx.x + w];
-            red[1][threadIdx.x] += red[1][threadIdx.x + w];
-        }
+        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        part[blockIdx.x * 2] = red[0][0];
-        part[blockIdx.x * 2 + 1] = red[1][0];
-    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
 }
 
 }  // namespace
@@ -693,16 +622,14 @@ cudaError_t tile3d_shape(int device, LaunchShape *out) {
 
 int tile3d_step0_blocks(int64_t n_nodes) { return (int)((n_nodes + 255) / 256); }
 
-cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *zu0, double *part, cudaStream_t st) {
+cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *part, cudaStream_t st) {
     const int nb = tile3d_step0_blocks(a.n_nodes);
     if (a.mode == MODE_UPDATE_P2) {
-        if (a.s0) tile3d_step0_kernel<true, MODE_UPDATE_P2><<<nb, 256, 0, st>>>(a, 1, zu0, part);
-        else tile3d_step0_kernel<false, MODE_UPDATE_P2><<<nb, 256, 0, st>>>(a, 1, zu0, part);
+        if (a.s0) tile3d_step0_kernel<true, MODE_UPDATE_P2><<<nb, 256, 0, st>>>(a, part);
+        else tile3d_step0_kernel<false, MODE_UPDATE_P2><<<nb, 256, 0, st>>>(a, part);
     } else if (a.mode == MODE_P1_PASS1) {
-        for (int ph = 0; ph < 2; ++ph) {
-            if (a.s0) tile3d_step0_kernel<true, MODE_P1_PASS1><<<nb, 256, 0, st>>>(a, ph, zu0, part);
-            else tile3d_step0_kernel<false, MODE_P1_PASS1><<<nb, 256, 0, st>>>(a, ph, zu0, part);
-        }
+        if (a.s0) tile3d_step0_kernel<true, MODE_P1_PASS1><<<nb, 256, 0, st>>>(a, part);
+        else tile3d_step0_kernel<false, MODE_P1_PASS1><<<nb, 256, 0, st>>>(a, part);
     } else {
         return cudaErrorInvalidValue;
     }

@@ -45,15 +45,16 @@ def main():
     ap.add_argument("--configs", type=int, nargs="+", default=[3, 4])
     ap.add_argument("--K", type=int, default=20)
     ap.add_argument("--precond", type=int, default=2)
+    ap.add_argument("--P", type=int, nargs="+", default=[1, 2, 4, 8])
     args = ap.parse_args()
     out = {"what": __doc__.strip().splitlines()[0], "nvlink_gbs": NVLINK_GBS, "halo_latency_us": HALO_LAT_US,
            "precond": args.precond, "lines": []}
     for cid in args.configs:
         prob = config_problem(cid)
         omega = 0.5 if args.precond == 2 else 0.3
-        t1, info1 = slab_ms(prob, 1, args.K, args.precond, omega)
+        t1, info1 = slab_ms(prob, 1, args.K, args.precond, omega) if 1 in args.P else (float("nan"), None)
         halo_ms = prob.n_dof * 8 / (NVLINK_GBS * 1e9) * 1e3 + HALO_LAT_US * 1e-3
-        for P in (1, 2, 4, 8):
+        for P in args.P:
             tp, info = (t1, info1) if P == 1 else slab_ms(prob, P, args.K, args.precond, omega)
             th = 0.0 if P == 1 else halo_ms
             eff = t1 / (P * (tp + th))
