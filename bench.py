@@ -407,6 +407,7 @@ def main():
                     "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
                                     "profiles/traffic.json)",
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if pk else "fallback 6.65 TB/s",
+                    "frac_of_nominal_8tbs": achieved_gbs / 8000.0,
                     "fp64_tflops": achieved_tf, "fp64_peak_tflops_measured": fp64_meas_tf}
         else:
             roof = {"bound": "alu", "achieved": achieved_tf, "peak": fp64_meas_tf, "unit": "TFLOP/s",

@@ -337,18 +337,11 @@ __device__ __forceinline__ void accum_plane_bt(const Tile3dArgs &a, const double
 template <bool CLS, bool S0>
 __device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po, const double *pu,
                                           const double *aux, int64_t i, int sx, int sy, int lane, int t,
-                                          const double *T, double (&bt)[kT3]) {
+                                          const double *T, double (&bt)[kT3], const double (&xpre)[kT3]) {
     accum_plane_bt<1, CLS, S0>(a, pu, sx, sy, lane, T, bt);
     const int64_t P = a.pitch, row = i * 4 * P + 3 * P + a.t_off + t;
     const double2 rp = *reinterpret_cast<const double2 *>(col_ptr(po, sx, sy, lane) + 3 * kTc);
-    double x0 = 0.0, x1 = 0.0;
-    if (t + 1 < a.n_tl) {
-        const double2 xv = __ldg(reinterpret_cast<const double2 *>(a.x + row));
-        x0 = xv.x;
-        x1 = xv.y;
-    } else if (t < a.n_tl) {
-        x0 = __ldg(a.x + row);
-    }
+    const double x0 = xpre[0], x1 = xpre[1];   // x_p^k, prefetched when the node was started
     if (a.s0buf && t == 0) a.s0buf[i * 4 + 3] = bt[0];   // deferred first step
     const double v0 = fma(a.omega, aux[22] * (bt[0] - rp.x), x0);
     const double v1 = fma(a.omega, aux[22] * (bt[1] - rp.y), x1);
@@ -478,8 +471,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
                         const int64_t iA = ((int64_t)(m - 1) * g.n1 + y) * g.n1 + xA;
                         double *carry = qcarry + (m - 1 - za) * kNodes + warp;
                         if constexpr (MODE == MODE_PASS2) {   // bt rides in q
-                            if (kindP == 1) finish_bt<false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q);
-                            else finish_bt<true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q);
+                            if (kindP == 1) finish_bt<false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3]);
+                            else finish_bt<true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3]);
                         } else {
                             if (kindP == 1)
                                 finish<false, S0, MODE>(a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp, acc, q,
@@ -499,6 +492,17 @@ __global__ void __launch_bounds__(kThreads3, 1)
                             TAp = cls_sm + ((axis_class(m, g.n1) != 1) * 4 + (ccy - cyl) * 2 + ccxA - cxl) * kClsD;
                         if constexpr (MODE == MODE_PASS2) {
                             q[0] = q[1] = 0.0;
+                            // prefetch x_p^k of the node (used at its finish, one plane later): its
+                            // global-load latency then overlaps the plane march instead of stalling it
+                            const int64_t rowp = (((int64_t)m * g.n1 + y) * g.n1 + xA) * 4 * a.pitch + 3 * a.pitch + a.t_off + t;
+                            acc[3][0] = acc[3][1] = 0.0;
+                            if (t + 1 < a.n_tl) {
+                                const double2 xv = __ldg(reinterpret_cast<const double2 *>(a.x + rowp));
+                                acc[3][0] = xv.x;
+                                acc[3][1] = xv.y;
+                            } else if (t < a.n_tl) {
+                                acc[3][0] = __ldg(a.x + rowp);
+                            }
                             if (kindP == 1) {
                                 accum_plane_bt<-1, false, S0>(a, pd, sx, sy, lane, TAp, q);
                                 accum_plane_bt<0, false, S0>(a, pm, sx, sy, lane, TAp, q);
