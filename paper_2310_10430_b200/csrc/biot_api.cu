@@ -163,7 +163,8 @@ struct biot_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_comm = nullptr;
     double *partial = nullptr;
-    double *fin_scratch = nullptr;    // two-stage norm reduction
+    double *fin_scratch = nullptr;    // norm reduction scratch (chunk sums)
+    int *fin_tickets = nullptr;       // one-launch finalize: per 32-step column tile
     double *hist = nullptr, *norms = nullptr;
     int *nonfinite = nullptr;
     double *staging = nullptr;
@@ -271,7 +272,7 @@ void free_all(biot_ctx *c) {
                     (void *)c->fixed, (void *)c->sendbuf, (void *)c->sendbuf2, (void *)c->zero_ghost_base, (void *)c->s0buf, (void *)c->sweep_in,
                     (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
-                    (void *)c->cls, (void *)c->fin_scratch, (void *)c->gm_Vdev, (void *)c->gm_scratch,
+                    (void *)c->cls, (void *)c->fin_scratch, (void *)c->fin_tickets, (void *)c->gm_Vdev, (void *)c->gm_scratch,
                     (void *)c->gm_small, (void *)c->d_iter})
         if (p) cudaFree(p);
     for (double *p : c->gm_Vbase) cudaFree(p);
@@ -648,7 +649,8 @@ int main_mode(const biot_ctx *c) {
 // The kernels of one outer iteration from panel `cur` (sweep, P~1 pass 2 if two-pass,
 // norm finalize).  graph_slot >= 0: the finalize writes history slot d_iter + graph_slot
 // (read on the device: replayable in a CUDA graph) and the events are graph nodes.
-biot_status enqueue_iteration(biot_ctx *ctx, int cur, cudaEvent_t e0, cudaEvent_t e1, int graph_slot) {
+biot_status enqueue_iteration(biot_ctx *ctx, int cur, cudaEvent_t e0, cudaEvent_t e1, int graph_slot,
+                              bool finalize = true) {
     const double *xin = ctx->x[cur];
     double *xout = ctx->x[1 - cur];
     const int mode = main_mode(ctx);
@@ -659,13 +661,15 @@ biot_status enqueue_iteration(biot_ctx *ctx, int cur, cudaEvent_t e0, cudaEvent_
     CU(launch_main(ctx, mode, xin, xout));
     if (mode == biot::MODE_P1_PASS1) CU(launch_pass2_any(ctx, xin, xout, a.sendbuf, nullptr));
     if (e1) CU(cudaEventRecordWithFlags(e1, ctx->stream, evf));
+    if (!finalize) return BIOT_OK;
     if (graph_slot >= 0) {
         CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, ctx->hist, ctx->nonfinite,
-                                 ctx->fin_scratch, ctx->stream, ctx->d_iter, graph_slot, ctx->hist_cap));
+                                 ctx->fin_scratch, ctx->stream, ctx->d_iter, graph_slot, ctx->hist_cap,
+                                 ctx->fin_tickets));
     } else {
         double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
         CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, hslot, ctx->nonfinite,
-                                 ctx->fin_scratch, ctx->stream));
+                                 ctx->fin_scratch, ctx->stream, nullptr, 0, 1, ctx->fin_tickets));
     }
     return BIOT_OK;
 }
@@ -702,7 +706,10 @@ biot_status complete_step0(biot_ctx *ctx, int mode, const double *xin, double *x
         a.ghost_stride = 1;
         CU(biot::launch_tile3d_step0(a, ctx->part0, ctx->stream));
     }
-    CU(biot::launch_finalize_p0(ctx->part0, ctx->step0_blocks, hslot, ctx->nonfinite, ctx->stream));
+    // the norms of the iteration, with step 0's p-part from the completion's partials
+    CU(biot::launch_finalize(ctx->partial, (int)groups_of(ctx, mode), ctx->n_tl, hslot, ctx->nonfinite,
+                             ctx->fin_scratch, ctx->stream, nullptr, 0, 1, ctx->fin_tickets, ctx->part0,
+                             ctx->step0_blocks));
     return BIOT_OK;
 }
 
@@ -738,7 +745,7 @@ biot_status one_iteration(biot_ctx *ctx, cudaEvent_t e0, cudaEvent_t e1) {
     const int mode = main_mode(ctx);
     double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
     if (ctx->defer0) ctx->ghost_override = ctx->zero_ghost;
-    st = enqueue_iteration(ctx, ctx->cur, e0, e1, -1);
+    st = enqueue_iteration(ctx, ctx->cur, e0, e1, -1, !ctx->defer0);   // deferred: finalized after step 0
     ctx->ghost_override = nullptr;
     if (st == BIOT_OK && ctx->defer0) {
         if (ctx->overlap) CU(cudaStreamWaitEvent(ctx->stream, ctx->ev_comm, 0));   // the ghost arrived
@@ -1504,8 +1511,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         ALLOC(ctx->zero_ghost_base, (size_t)ctx->rows_alloc * sizeof(double));
         CU(cudaMemsetAsync(ctx->zero_ghost_base, 0, (size_t)ctx->rows_alloc * sizeof(double), ctx->stream));
         ctx->zero_ghost = ctx->zero_ghost_base + ctx->pad * nc;
-        ALLOC(ctx->s0buf, (size_t)ctx->N * 4 * sizeof(double));
-        CU(cudaMemsetAsync(ctx->s0buf, 0, (size_t)ctx->N * 4 * sizeof(double), ctx->stream));
+        ALLOC(ctx->s0buf, (size_t)ctx->N * 8 * sizeof(double));
+        CU(cudaMemsetAsync(ctx->s0buf, 0, (size_t)ctx->N * 8 * sizeof(double), ctx->stream));
         ctx->step0_blocks = ctx->kern == 4 ? biot::tile2d_step0_blocks(ctx->N) : biot::tile3d_step0_blocks(ctx->N);
         ALLOC(ctx->part0, (size_t)ctx->step0_blocks * sizeof(double));   // step-0 p-norm partials
     }
@@ -1791,6 +1798,8 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     ALLOC(ctx->partial, (size_t)gmax * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->fin_scratch, (size_t)std::max<int64_t>(1, biot::finalize_scratch_doubles((int)gmax, ctx->n_tl)) *
                                 sizeof(double));
+    ALLOC(ctx->fin_tickets, (size_t)biot::finalize_tickets(ctx->n_tl) * sizeof(int));
+    CU(cudaMemsetAsync(ctx->fin_tickets, 0, (size_t)biot::finalize_tickets(ctx->n_tl) * sizeof(int), ctx->stream));
     ALLOC(ctx->hist, (size_t)ctx->hist_cap * ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double));
     ALLOC(ctx->nonfinite, sizeof(int));
@@ -2169,7 +2178,7 @@ biot_status biot_iterate_gmres(biot_ctx *ctx, int32_t K, int32_t k) {
         if ((st = gmres_cycle(ctx, k, ctx->tmap[ctx->cur], x, x, win)) != BIOT_OK) return st;
         double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
         CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite, ctx->fin_scratch,
-                                 ctx->stream));
+                                 ctx->stream, nullptr, 0, 1, ctx->fin_tickets));
         ctx->send_dirty = true;
         ctx->iterations++;
     }
@@ -2244,7 +2253,7 @@ biot_status biot_iterate_cheb(biot_ctx *ctx, int32_t K, int32_t m, double alpha)
         CU(e);
         double *hslot = ctx->hist + (size_t)(ctx->iterations % ctx->hist_cap) * ctx->n_tl * 2;
         CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, hslot, ctx->nonfinite,
-                                 ctx->fin_scratch, ctx->stream));
+                                 ctx->fin_scratch, ctx->stream, nullptr, 0, 1, ctx->fin_tickets));
         c.s = ctx->cb[0];
         c.x = xin;
         c.xn = xout;
@@ -2348,7 +2357,7 @@ biot_status biot_residual_norms(biot_ctx *ctx, double *out) {
     if (st != BIOT_OK) return st;
     CU(launch_main(ctx, biot::MODE_RESIDUAL, ctx->x[ctx->cur], nullptr));
     CU(biot::launch_finalize(ctx->partial, (int)ctx->groups, ctx->n_tl, ctx->norms, ctx->nonfinite,
-                             ctx->fin_scratch, ctx->stream));
+                             ctx->fin_scratch, ctx->stream, nullptr, 0, 1, ctx->fin_tickets));
     CU(cudaMemcpyAsync(out, ctx->norms, (size_t)ctx->n_tl * 2 * sizeof(double), cudaMemcpyDeviceToHost,
                        ctx->stream));
     return wait_stream(ctx);
@@ -2446,8 +2455,7 @@ biot_status biot_get_info(const biot_ctx *ctx, biot_info *o) {
     o->flops_per_iter = 2.0 * (double)(ctx->nnz_AA + ctx->nnz_AP) * ctx->n_tl;
     o->device_bytes = (double)ctx->device_bytes;
     const int mm = main_mode(ctx);
-    o->launches_per_iter = 1 + (mm == biot::MODE_P1_PASS1 ? 1 : 0) +
-                           (biot::finalize_scratch_doubles((int)groups_of(ctx, mm), ctx->n_tl) > 0 ? 2 : 1);
+    o->launches_per_iter = 1 + (mm == biot::MODE_P1_PASS1 ? 1 : 0) + 1 + (ctx->defer0 ? 1 : 0);   // sweep (+ pass 2), finalize (+ step 0)
     o->interior_nodes = (int32_t)ctx->n_interior;
     o->comm_nranks = 0;
     if (ctx->comm && nccl() && nccl()->CommCount) nccl()->CommCount(ctx->comm, &o->comm_nranks);

@@ -164,6 +164,7 @@ __global__ void finalize_kernel(const double *__restrict__ partial, int groups, 
 // First stage for many groups: block column by sums groups [by*kGch, (by+1)*kGch)
 // (fixed split over 8 y-lanes, then a fixed-order sum of the lane totals).
 constexpr int kGch = 128;
+constexpr int kGchT = 32;   // groups per block of the one-launch finalize (4 per y-lane)
 __global__ void finalize_stage1_kernel(const double *__restrict__ partial, int groups, int n_tl,
                                        double *__restrict__ out) {
     __shared__ double sm[8][32][2];
@@ -288,28 +289,6 @@ cudaError_t launch_pass2(int dim, int path, int n_slots, const Pass2Args &a, int
     return cudaGetLastError();
 }
 
-__global__ void finalize_p0_kernel(const double *__restrict__ part, int blocks, double *hist_slot, int *nonfinite) {
-    __shared__ double red[256];
-    double s = 0.0;
-    for (int b = threadIdx.x; b < blocks; b += 256) s += part[b];
-    red[threadIdx.x] = s;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        const double v = sqrt(red[0]);
-        hist_slot[1] = v;
-        if (!isfinite(v)) atomicOr(nonfinite, 1);
-    }
-}
-
-cudaError_t launch_finalize_p0(const double *part, int blocks, double *hist_slot, int *nonfinite, cudaStream_t st) {
-    finalize_p0_kernel<<<1, 256, 0, st>>>(part, blocks, hist_slot, nonfinite);
-    return cudaGetLastError();
-}
-
 cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int lo, int t_first, int64_t k0,
                                  int cap, int n_tl, double *hist, int *nonfinite, double *scratch, cudaStream_t st) {
     dim3 block(32, 8);
@@ -325,7 +304,7 @@ cudaError_t launch_finalize_wave(const double *partial, int groups, int len, int
 }
 
 int64_t finalize_scratch_doubles(int groups, int n_tl) {
-    return groups > 2 * kGch ? (int64_t)((groups + kGch - 1) / kGch) * n_tl * 2 : 0;
+    return (int64_t)((groups + kGchT - 1) / kGchT) * n_tl * 2;   // both forms (two-stage, ticketed)
 }
 
 __global__ void advance_kernel(int64_t *ctr, int64_t value, int add) {
@@ -338,10 +317,100 @@ cudaError_t launch_counter(int64_t *ctr, int64_t value, bool add, cudaStream_t s
     return cudaGetLastError();
 }
 
+// One-launch form of the two stages: block (x, c) sums groups [c kGchT, (c+1) kGchT) of the
+// 32 steps of column tile x (fixed split over 8 y-lanes, fixed-order lane sum) into
+// scratch[c]; the LAST block of column tile x to finish (ticket counter) sums scratch over
+// c in order and writes the norms -- deterministic, since the order is the chunk index, not
+// the arrival.  part0 (deferred first step of the overlapped halo): the p-norm of step 0 is
+// the fixed-order sum of part0[0..nb0) instead.
+__global__ void finalize_ticket_kernel(const double *__restrict__ partial, int groups, int n_tl, double *norms,
+                                       int *nonfinite, double *scratch, int *tickets, const double *part0, int nb0,
+                                       const int64_t *slot_ctr, int64_t slot_off, int cap) {
+    if (slot_ctr) norms += ((*slot_ctr + slot_off) % cap) * (int64_t)n_tl * 2;
+    __shared__ double sm[8][32][2];
+    __shared__ int last;
+    const int t = blockIdx.x * 32 + threadIdx.x, y = threadIdx.y, c = blockIdx.y;
+    const int g0 = c * kGchT, g1 = min(groups, g0 + kGchT);
+    double su = 0.0, sp = 0.0;
+    if (t < n_tl)
+        for (int g = g0 + y; g < g1; g += 8) {
+            su += partial[((int64_t)g * n_tl + t) * 2 + 0];
+            sp += partial[((int64_t)g * n_tl + t) * 2 + 1];
+        }
+    sm[y][threadIdx.x][0] = su;
+    sm[y][threadIdx.x][1] = sp;
+    __syncthreads();
+    if (y == 0 && t < n_tl) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            a += sm[k][threadIdx.x][0];
+            b += sm[k][threadIdx.x][1];
+        }
+        scratch[((int64_t)c * n_tl + t) * 2 + 0] = a;
+        scratch[((int64_t)c * n_tl + t) * 2 + 1] = b;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && y == 0) last = atomicAdd(&tickets[blockIdx.x], 1) == (int)gridDim.y - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double p0 = 0.0;
+    if (part0 && blockIdx.x == 0) {   // the completed first step's p-norm: fixed-order tree over part0
+        __shared__ double r0[256];
+        const int tid = y * 32 + threadIdx.x;
+        double s = 0.0;
+        for (int b = tid; b < nb0; b += 256) s += part0[b];
+        r0[tid] = s;
+        __syncthreads();
+        for (int w = 128; w > 0; w >>= 1) {
+            if (tid < w) r0[tid] += r0[tid + w];
+            __syncthreads();
+        }
+        p0 = r0[0];
+    }
+    // chunk sums: fixed split over the 8 y-lanes, then a fixed-order sum of the lane totals
+    {
+        double a = 0.0, b = 0.0;
+        if (t < n_tl)
+            for (int k = y; k < (int)gridDim.y; k += 8) {
+                a += __ldcg(scratch + ((int64_t)k * n_tl + t) * 2 + 0);
+                b += __ldcg(scratch + ((int64_t)k * n_tl + t) * 2 + 1);
+            }
+        __syncthreads();
+        sm[y][threadIdx.x][0] = a;
+        sm[y][threadIdx.x][1] = b;
+        __syncthreads();
+    }
+    if (y == 0 && t < n_tl) {
+        double a = 0.0, b = 0.0;
+        for (int k = 0; k < 8; ++k) {
+            a += sm[k][threadIdx.x][0];
+            b += sm[k][threadIdx.x][1];
+        }
+        if (part0 && t == 0) b = p0;
+        a = sqrt(a);
+        b = sqrt(b);
+        norms[t * 2 + 0] = a;
+        norms[t * 2 + 1] = b;
+        if (!isfinite(a) || !isfinite(b)) atomicOr(nonfinite, 1);
+    }
+    if (threadIdx.x == 0 && y == 0) tickets[blockIdx.x] = 0;   // ready for the next launch
+}
+
+int finalize_tickets(int n_tl) { return (n_tl + 31) / 32; }
+
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
                             int *nonfinite, double *scratch, cudaStream_t st, const int64_t *slot_ctr,
-                            int64_t slot_off, int cap) {
+                            int64_t slot_off, int cap, int *tickets, const double *part0, int nb0) {
     dim3 block(32, 8);
+    if (tickets) {
+        const int g1 = (groups + kGchT - 1) / kGchT;
+        finalize_ticket_kernel<<<dim3((n_tl + 31) / 32, g1), block, 0, st>>>(partial, groups, n_tl, norms, nonfinite,
+                                                                             scratch, tickets, part0, nb0, slot_ctr,
+                                                                             slot_off, cap);
+        return cudaGetLastError();
+    }
     if (groups > 2 * kGch) {   // two fixed-order stages: many groups would serialise one pass
         const int g1 = (groups + kGch - 1) / kGch;
         finalize_stage1_kernel<<<dim3((n_tl + 31) / 32, g1), block, 0, st>>>(partial, groups, n_tl, scratch);

@@ -56,7 +56,8 @@ struct SweepArgs {
                             // P~1^{-1} r; pass2 (pure) then completes z_p in place
     double *s0buf;          // deferred sweep (overlapped halo): per node, the pieces of the first local
                             // step's pressure update that do not depend on the ghost:
-                            // [acc_p, -, x_p^k, (B^T z_u)_p] (tile kernels), else null
+                            // [acc_p, f_p, x_p^k, (B^T z_u)_p, D_S^{-1}, path flag, -, -] (tile
+                            // kernels), else null
 };
 
 struct Pass2Args {          // P~1 second pass: x_p += omega DSinv (B^T z_u - r_p)
@@ -170,8 +171,7 @@ cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const Lau
 // deferred first local step (see launch_tile2d_step0): MODE_UPDATE_P2 or MODE_P1_PASS1
 int tile3d_step0_blocks(int64_t n_nodes);
 cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *part, cudaStream_t st);
-// hist_slot[1] = sqrt(fixed-order sum of part[0..blocks)): the completed step's p-norm
-cudaError_t launch_finalize_p0(const double *part, int blocks, double *hist_slot, int *nonfinite, cudaStream_t st);
+
 
 // Per-step GMRES panel kernels (gmres_kernels.cu): column-wise (per time step) dot
 // products of a panel with nb panels (b_dev: device array of panel pointers) and
@@ -227,9 +227,13 @@ cudaError_t launch_cheb_p1_rhs(int dim, int path, int n_slots, const ChebArgs &a
 int64_t finalize_scratch_doubles(int groups, int n_tl);
 // slot_ctr != null: norms is the history ring [cap][n_tl][2], written at slot
 // (*slot_ctr + slot_off) % cap read on the device (so a captured CUDA graph can be replayed)
+// tickets (finalize_tickets(n_tl) zeroed ints): one launch instead of two (the last block
+// of each column tile completes it); part0/nb0: the deferred first step's p-norm partials
 cudaError_t launch_finalize(const double *partial, int groups, int n_tl, double *norms,
                             int *nonfinite, double *scratch, cudaStream_t st, const int64_t *slot_ctr = nullptr,
-                            int64_t slot_off = 0, int cap = 1);
+                            int64_t slot_off = 0, int cap = 1, int *tickets = nullptr, const double *part0 = nullptr,
+                            int nb0 = 0);
+int finalize_tickets(int n_tl);
 // *ctr = value (add = false) or *ctr += value, on the stream
 cudaError_t launch_counter(int64_t *ctr, int64_t value, bool add, cudaStream_t st);
 // Gauss-Seidel wave: the window's steps t = lo..lo+len-1 carry iteration k = k0 - t;

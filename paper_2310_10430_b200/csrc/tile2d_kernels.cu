@@ -269,8 +269,12 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
         epilogue_math<2, 2, CLS, MODE == MODE_ZOUT>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2,
                                                     outx, outz, !a.p1_out);
         if (MODE == MODE_UPDATE_P2 && a.s0buf && h == 0 && t0 == 0) {   // deferred first step (lane 0)
-            a.s0buf[i * 4 + 0] = acc2[2][0];
-            a.s0buf[i * 4 + 2] = xs2[2][0];
+            double *sb = a.s0buf + i * 8;
+            sb[0] = acc2[2][0];
+            sb[1] = aux[9];
+            sb[2] = xs2[2][0];
+            sb[4] = aux[12];
+            sb[5] = aux[13];
         }
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
@@ -769,8 +773,12 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
         }
         epilogue_math<2, 2, CLS, false>(a.omega, acc2, q2, h == 0 ? qp0 : qp1, ld, Dv, xs2, nu2, np2, outx, outz);
         if (a.s0buf && own && h == 0 && t0 == 0) {   // deferred first step (lane 0)
-            a.s0buf[i * 4 + 0] = acc2[2][0];
-            a.s0buf[i * 4 + 2] = xs2[2][0];
+            double *sb = a.s0buf + i * 8;
+            sb[0] = acc2[2][0];
+            sb[1] = aux[9];
+            sb[2] = xs2[2][0];
+            sb[4] = aux[12];
+            sb[5] = aux[13];
         }
         const int th = t0 + h * (kCT / 2);
         // z_u published for the neighbours; the pressure part waits for B^T z_u:
@@ -815,7 +823,7 @@ template <class A>
 __device__ __forceinline__ void finish_zp(const A &a, int64_t i, int t0, bool whole, double wdv,
                                           const double (&bt)[kT2], const double (&y)[kT2]) {
     const int64_t P = a.pitch, row = i * 3 * P + 2 * P + a.t_off + t0;
-    if (a.s0buf && t0 == 0) a.s0buf[i * 4 + 3] = bt[0];   // deferred first step (lane 0)
+    if (a.s0buf && t0 == 0) a.s0buf[i * 8 + 3] = bt[0];   // deferred first step (lane 0)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
         const double v0 = fma(wdv, bt[2 * h], y[2 * h]);
@@ -1090,19 +1098,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
 // ============================================================================
 template <bool S0, int MODE, int NL>
 __global__ void __launch_bounds__(256) tile2d_step0_kernel(const Tile2dArgs a, double *part) {
-    constexpr int kAuxRec = NL == 1 ? Tile2dArgs::kAux : Tile2dArgs::kAuxML;
     const int64_t N = a.n_nodes, P = a.pitch;
     const int W = (int)a.row_w;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double sp = 0.0;
     if (i < N) {
-        const double *aux = a.aux + i * kAuxRec;
-        const bool intr = aux[13] == 1.0;
+        const double *sv = a.s0buf + i * 8;   // acc_p, f_p, x_p^k, B^T z_u, D_S^{-1}, path flag
+        const bool intr = sv[5] == 1.0;
         const double *T = a.cls + (axis_class((int)(i % W), W) + 3 * axis_class((int)(i / W), a.n_rows)) * 7 * kCW;
         const double qp = intr ? ghost_q<false, S0, Tile2dArgs>(a, i, T) : ghost_q<true, S0, Tile2dArgs>(a, i, T);
-        const double *sv = a.s0buf + i * 4;
-        const double dv = aux[12];
-        double r = __dsub_rn(__fma_rn(a.s[a.t_off], aux[9], qp), sv[0]);   // epilogue_math's r_p
+        const double dv = sv[4];
+        double r = __dsub_rn(__fma_rn(a.s[a.t_off], sv[1], qp), sv[0]);   // epilogue_math's r_p
         if (dv == 0.0) r = 0.0;                 // Dirichlet pressure row (the epilogue's mask)
         sp = r * r;
         double xn;

@@ -269,8 +269,12 @@ __device__ __forceinline__ void finish(const Tile3dArgs &a, const double *po, co
     epilogue_math<3, kT3, CLS, MODE == MODE_ZOUT>(a.omega, acc, q, qp, single_load(F, sv), Dv, xs, nu, npn, outx, outz,
                                                   !a.p1_out);
     if ((MODE == MODE_UPDATE_P2 || MODE == MODE_P1_PASS1) && a.s0buf && t == 0) {   // deferred first step
-        a.s0buf[iA * 4 + 0] = acc[3][0];
-        a.s0buf[iA * 4 + 2] = xs[3][0];
+        double *sb = a.s0buf + iA * 8;
+        sb[0] = acc[3][0];
+        sb[1] = F[3];
+        sb[2] = xs[3][0];
+        sb[4] = Dv[3];
+        sb[5] = aux[23];
     }
     if constexpr (MODE == MODE_ZOUT) {       // GMRES start: z = P~2^{-1} r, x untouched
 #pragma unroll
@@ -342,7 +346,7 @@ __device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po,
     const int64_t P = a.pitch, row = i * 4 * P + 3 * P + a.t_off + t;
     const double2 rp = *reinterpret_cast<const double2 *>(col_ptr(po, sx, sy, lane) + 3 * kTc);
     const double x0 = xpre[0], x1 = xpre[1];   // x_p^k, prefetched when the node was started
-    if (a.s0buf && t == 0) a.s0buf[i * 4 + 3] = bt[0];   // deferred first step
+    if (a.s0buf && t == 0) a.s0buf[i * 8 + 3] = bt[0];   // deferred first step
     const double v0 = fma(a.omega, aux[22] * (bt[0] - rp.x), x0);
     const double v1 = fma(a.omega, aux[22] * (bt[1] - rp.y), x1);
     store2(a.xn + row, v0, v1, t, a.t_lo, a.n_tl);
@@ -555,15 +559,14 @@ __global__ void __launch_bounds__(256) tile3d_step0_kernel(const Tile3dArgs a, d
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double sp = 0.0;
     if (i < N) {
-        const double *aux = a.aux + i * kAuxRec;
-        const bool intr = aux[23] == 1.0;
+        const double *sv = a.s0buf + i * 8;   // acc_p, f_p, x_p^k, B^T z_u, D_S^{-1}, path flag
+        const bool intr = sv[5] == 1.0;
         const int x = (int)(i % n1), y = (int)((i / n1) % n1), z = (int)(i / (n1 * n1));
         const double *T = a.cls + (size_t)(axis_class(x, (int)n1) + 3 * axis_class(y, (int)n1) +
                                            9 * axis_class(z, (int)n1)) * (15 * kCW);
         const double qp = intr ? ghost_q<false, S0>(a.ghost, n1, i, a, T) : ghost_q<true, S0>(a.ghost, n1, i, a, T);
-        const double *sv = a.s0buf + i * 4;
-        const double dv = aux[22];
-        double r = __dsub_rn(__fma_rn(a.s[a.t_off], aux[18], qp), sv[0]);   // epilogue_math's r_p
+        const double dv = sv[4];
+        double r = __dsub_rn(__fma_rn(a.s[a.t_off], sv[1], qp), sv[0]);   // epilogue_math's r_p
         if (dv == 0.0) r = 0.0;
         sp = r * r;
         const double xn = MODE == MODE_P1_PASS1 ? fma(a.omega, dv * (sv[3] - r), sv[2])   // finish_bt
