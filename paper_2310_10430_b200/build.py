@@ -31,15 +31,21 @@ def _stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """out / defines: an experimental variant (-D flags) built beside the product library
+    (tools/build_variant.py; loaded through BIOT_LIB_OVERRIDE for A/B timing)."""
+    variant = out is not None
+    out = out or OUT
+    if not variant and not force and not _stale():
         return OUT
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD if not variant else BUILD + "_" + os.path.splitext(os.path.basename(out))[0]
+    os.makedirs(bdir, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
     def compile_one(src):
         path = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src + ".o")
+        obj = os.path.join(bdir, src + ".o")
         if src.endswith(".cu"):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *dflags,
                    "-Xptxas", "-v", "--expt-relaxed-constexpr", "-c", path, "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-fopenmp", "-Wall", "-c", path, "-o", obj]
@@ -58,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"compile failed: {src}")
         objs.append(obj)
-    tmp = OUT + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp, *objs,
            "-Xcompiler", "-fopenmp", "-lgomp", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -66,12 +72,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, OUT)
-    with open(os.path.join(BUILD, "ptxas.txt"), "w") as f:
+    os.replace(tmp, out)
+    with open(os.path.join(bdir, "ptxas.txt"), "w") as f:
         f.write("\n".join(report))
     if verbose:
         print("\n".join(report))
-    return OUT
+    return out
 
 
 if __name__ == "__main__":

@@ -724,8 +724,7 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
                                           const double *aux, const double *T, int64_t i, int t0, bool ghost,
                                           bool whole, bool own, double *carry, const double (&sv)[kT2],
                                           double (&acc)[3][kT2], double (&q)[kT2], double (&nu)[kT2],
-                                          double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2],
-                                          double (&zo)[2][kT2]) {
+                                          double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2]) {
     accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
     if constexpr (NL > 1) {
 #pragma unroll
@@ -758,8 +757,16 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
     for (int h = 0; h < 2; ++h) {
         double acc2[3][2], q2[2], xs2[3][2], nu2[2] = {0.0, 0.0}, np2[2] = {0.0, 0.0}, outx[3][2], outz[3][2];
         Loads<3, 2, 1> ld;
+#ifdef BIOT_P1_SV_REG
         ld.sv[0][0] = sv[2 * h];
         ld.sv[0][1] = sv[2 * h + 1];
+#else
+        {   // the load scales from L1 at the point of use: 8 registers fewer across the march
+            const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
+            ld.sv[0][0] = s2.x;
+            ld.sv[0][1] = s2.y;
+        }
+#endif
 #pragma unroll
         for (int c = 0; c < 3; ++c) ld.F[0][c] = aux[7 + c];
 #pragma unroll
@@ -784,11 +791,8 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
         // z_u published for the neighbours; the pressure part waits for B^T z_u:
         // x_p^{k+1} = x_p + omega D_S^{-1} (bt - r_p) = y + (omega D_S^{-1}) bt
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
+        for (int c = 0; c < 2; ++c)
             *reinterpret_cast<double2 *>(zd + c * kCT + h * (kCT / 2)) = make_double2(outz[c][0], outz[c][1]);
-            zo[c][2 * h] = outz[c][0];
-            zo[c][2 * h + 1] = outz[c][1];
-        }
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) y[2 * h + tt] = fma(-wdv, outz[2][tt], xs2[2][tt]);
         if (own) {
@@ -870,8 +874,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kSeg);
         }
-        mbar_init(&zbar[0], kSeg * 32);
-        mbar_init(&zbar[1], kSeg * 32);
+        mbar_init(&zbar[0], kSeg);   // one arrival per warp: a waiter wakes at most kSeg times
+        mbar_init(&zbar[1], kSeg);
         fence_barrier_init();
     }
     if (threadIdx.x < kAuxRecU) aux_u[threadIdx.x] = a.aux_u[threadIdx.x];
@@ -920,12 +924,17 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const bool whole = (chunk + 1) * kCT <= a.n_tl && (chunk > 0 || a.t_lo == 0);
             double nu[kT2], npn[kT2], sv[kT2];
             const bool first = tile == (int)blockIdx.x;
+#ifdef BIOT_P1_SV_REG
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
                 sv[2 * h] = s2.x;
                 sv[2 * h + 1] = s2.y;
             }
+#else
+#pragma unroll
+            for (int tt = 0; tt < kT2; ++tt) sv[tt] = 0.0;   // unused (finish_p1 reads a.s)
+#endif
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) nu[tt] = npn[tt] = 0.0;
             if (ghost && nchunks > 1 && ocol) {
@@ -960,9 +969,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 double *zrow = zbuf + (size_t)((m - 1) & 1) * (kSeg * 2 * kCT);
                 const bool orow1 = m - 1 >= ja && m - 1 < jb;       // node m-1 owned (row)
                 // (1) finish node m-1 and publish its z_u (zero off the mesh)
-                double zo[2][kT2];                       // this column's z_u of row m-1 (registers)
-#pragma unroll
-                for (int tt = 0; tt < kT2; ++tt) zo[0][tt] = zo[1][tt] = 0.0;
                 if (m >= ja) {
                     double *zd = zrow + (p - 1) * 2 * kCT + lane * 2;
                     if (kindP != 0) {
@@ -975,10 +981,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         wB = a.omega * aux[12];
                         if (kindP == 1)
                             finish_p1<false, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB, zo);
+                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
                         else
                             finish_p1<true, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB, zo);
+                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
                     } else {
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
@@ -992,8 +998,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 // (2) this thread's z_u of row m-1 is published (the chunk's first row step
                 // instead fences the z buffers against the previous chunk's last reads)
                 const int zb = (m - 1) & 1;
-                if (m >= ja) mbar_arrive(&zbar[zb]);
-                else named_barrier_sync(1, kSeg * 32);
+#ifdef BIOT_P1_MBAR
+                if (m >= ja) {
+                    __syncwarp();                                  // the warp's z_u stores, then one release
+                    if (lane == 0) mbar_arrive(&zbar[zb]);
+                } else {
+                    named_barrier_sync(1, kSeg * 32);
+                }
+#else
+                if (m < ja) named_barrier_sync(1, kSeg * 32);
+#endif
                 // (3) start node m (z rows ja-1..jb on the mesh): independent of the z_u
                 // exchange, so it overlaps the other warps' publishing
                 int kindC = 0;
@@ -1009,17 +1023,26 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 // (4) every z_u of row m-1 published: B^T contributions of row m-1's z_u to
                 // node m-2 (its +W slots; then complete), node m-1 (0 slots), node m (-W slots)
+#ifdef BIOT_P1_MBAR
                 if (m >= ja) {
                     mbar_wait_suspend(&zbar[zb], zph[zb]);
                     zph[zb] ^= 1u;
                 }
+#else
+                // a hardware barrier: waiting warps issue nothing (an mbarrier wait re-polls
+                // at every barrier event of the CTA -- ~24 polls per row step measured)
+                if (m >= ja) named_barrier_sync(2, kSeg * 32);
+#endif
                 if (m >= ja && ocol) {
                     // the z_u columns p-1, p (registers), p+1, each read once and applied to
                     // every node of this column that uses it, in ascending column order per node
                     // (node m-2: slots (+1, 0), (+1, +1); node m-1: (0, -1), (0, 0), (0, +1);
                     // node m: (-1, -1), (-1, 0))
                     const int kC = (kindC != 0 && m < jb) ? kindC : 0;
-                    double zn[2][kT2];
+                    // the own column re-read too: holding it in registers across the barrier
+                    // spills (4.84 -> 4.68 ms measured)
+                    double zn[2][kT2], zo[2][kT2];
+                    load_z(zo, zrow, p, lane);
                     if (kindA == 1 && kindB == 1 && kC == 1) {
                         // interior rows (the common case): one template path, no per-node branches
                         load_z(zn, zrow, p - 1, lane);
