@@ -204,6 +204,11 @@ struct biot_ctx {
     std::vector<CUtensorMap> gm_tmap;
     double **gm_Vdev = nullptr;
     double *gm_scratch = nullptr, *gm_small = nullptr;
+    // compact Krylov basis of narrow windows (Gauss-Seidel waves): k+1 vectors of
+    // rows x gm_vc_w doubles, rows adjacent (gmres_cycle)
+    double *gm_Vc = nullptr;
+    double **gm_Vcdev = nullptr;
+    int gm_vc_w = 0, gm_vc_n = 0;
     // Chebyshev inner inverses (biot_iterate_cheb): Gershgorin bounds of D^{-1} A and
     // D_S^{-1} S~p, the scaled-residual panel, d ping-pong and y panels
     double lmax_u = 0.0, lmax_p = 0.0;
@@ -273,7 +278,7 @@ void free_all(biot_ctx *c) {
                     (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->fin_tickets, (void *)c->gm_Vdev, (void *)c->gm_scratch,
-                    (void *)c->gm_small, (void *)c->d_iter})
+                    (void *)c->gm_small, (void *)c->gm_Vc, (void *)c->gm_Vcdev, (void *)c->d_iter})
         if (p) cudaFree(p);
     for (double *p : c->gm_Vbase) cudaFree(p);
     for (double *p : c->cb_base)
@@ -909,6 +914,38 @@ biot_status gmres_alloc(biot_ctx *ctx, int k) {
 
 namespace {
 
+// Compact basis for a window of nt <= kCompactMax columns: k + 1 vectors of rows x w
+// doubles, w = nt rounded up to 16 (reallocated when a wider window comes).  An allocation
+// failure is not an error: the cycle then keeps the basis in the panel layout.
+constexpr int kCompactMax = 64;
+bool gmres_compact_alloc(biot_ctx *ctx, int k, int nt) {
+    const int w = (nt + 15) / 16 * 16;
+    if (ctx->gm_Vc && ctx->gm_vc_w >= w && ctx->gm_vc_n >= k + 1) return true;
+    const int ww = std::max(w, ctx->gm_vc_w), nn = std::max(k + 1, ctx->gm_vc_n);
+    if (ctx->gm_Vc) cudaFree(ctx->gm_Vc);
+    if (ctx->gm_Vcdev) cudaFree(ctx->gm_Vcdev);
+    ctx->gm_Vc = nullptr;
+    ctx->gm_Vcdev = nullptr;
+    ctx->gm_vc_w = ctx->gm_vc_n = 0;
+    const size_t vec = (size_t)ctx->N * ctx->nc * ww;
+    if (cudaMalloc((void **)&ctx->gm_Vc, vec * nn * sizeof(double)) != cudaSuccess ||
+        cudaMalloc((void **)&ctx->gm_Vcdev, nn * sizeof(double *)) != cudaSuccess) {
+        cudaGetLastError();
+        if (ctx->gm_Vc) cudaFree(ctx->gm_Vc);
+        ctx->gm_Vc = nullptr;
+        return false;
+    }
+    std::vector<double *> ptrs(nn);
+    for (int i = 0; i < nn; ++i) ptrs[i] = ctx->gm_Vc + vec * i;
+    if (cudaMemcpy(ctx->gm_Vcdev, ptrs.data(), nn * sizeof(double *), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    ctx->gm_vc_w = ww;
+    ctx->gm_vc_n = nn;
+    return true;
+}
+
 // One GMRES(k) cycle for every step of a time window (R23): x_out = x_in + V y on
 // columns [t_off + t_lo, t_off + len), the residual (with its previous-step coupling and
 // norm partials) from panel xin through tensor map `tm`.  x_out may equal x_in.
@@ -928,14 +965,14 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
     double *d_H = d_y + (size_t)mv * ctx->n_tl;            // [(k+1) k][nt]
     double *const *Vd = ctx->gm_Vdev;
     auto hcol = [&](int i, int j) { return d_H + (size_t)(i + j * (k + 1)) * nt; };
+    const int64_t P = ctx->pitch;
+    const biot::GmresPitch full{P, P, P, 0};
     auto dots = [&](const double *a, double *const *bdev, int nb, double *out, double *hacc, bool norm) {
-        return biot::gmres_dots(a + c0, bdev, c0, nb, rows, ctx->pitch, nt, ctx->gm_scratch, out, hacc, norm,
-                                ctx->stream);
+        return biot::gmres_dots(a + c0, bdev, c0, nb, rows, P, nt, ctx->gm_scratch, out, hacc, norm, ctx->stream);
     };
     auto combine = [&](double *dst, const double *base, const double *coef, int nb, double sign,
                        const double *scale) {
-        return biot::gmres_combine(dst + c0, base + c0, Vd, c0, coef, nb, sign, scale, rows, ctx->pitch, nt,
-                                   ctx->stream);
+        return biot::gmres_combine(dst + c0, base + c0, Vd, c0, coef, nb, sign, scale, rows, full, nt, ctx->stream);
     };
     Window w = win;          // tile passes of the cycle never write the send slice
     w.send = nullptr;
@@ -964,6 +1001,55 @@ biot_status gmres_cycle(biot_ctx *ctx, int k, const CUtensorMap &tm, const doubl
         return biot::launch_pass2(ctx->d, ctx->path, ctx->S, p, ctx->pass2_grid, ctx->stream);
     };
     CU(cudaMemsetAsync(d_H, 0, (size_t)(k + 1) * k * nt * sizeof(double), ctx->stream));
+    if (nt <= kCompactMax && !std::getenv("BIOT_GMRES_NO_COMPACT") && gmres_compact_alloc(ctx, k, nt)) {
+        // Narrow window: the Krylov basis proper lives compact (row pitch nt, every dot and
+        // combination streams contiguous memory); the panel-layout V_j stay the tile passes'
+        // input/output only.  Per Arnoldi step: the matvec pass writes V_{j+1} (panel), one
+        // gather makes it compact, CGS2 and the norm run compact, and the normalising pass
+        // writes both copies.  Same arithmetic in the same order as the panel form (the dot
+        // order depends on the row chunking only): results are bitwise those of that form.
+        double *const *Vc = ctx->gm_Vcdev;
+        std::vector<double *> vc(k + 1);
+        for (int i = 0; i <= k; ++i) vc[i] = ctx->gm_Vc + (size_t)rows * ctx->gm_vc_w * i;
+        const int64_t cw = nt;   // compact row pitch: the window itself
+        auto cdots = [&](const double *a, double *const *bdev, int nb, double *out, double *hacc, bool norm) {
+            return biot::gmres_dots(a, bdev, 0, nb, rows, cw, nt, ctx->gm_scratch, out, hacc, norm, ctx->stream);
+        };
+        auto gather = [&](double *dst, const double *panel) {   // compact <- panel window
+            return biot::gmres_combine(dst, panel + c0, Vc, 0, nullptr, 0, 1.0, nullptr, rows,
+                                       biot::GmresPitch{cw, P, cw, 0}, nt, ctx->stream);
+        };
+        auto cnorm = [&](double *vcj, double *panel) {   // v = scale v, compact and panel copies
+            return biot::gmres_combine(vcj, vcj, Vc, 0, nullptr, 0, 1.0, d_scale, rows,
+                                       biot::GmresPitch{cw, cw, cw, P}, nt, ctx->stream, panel + c0);
+        };
+        CU(launch_main(ctx, biot::MODE_ZOUT, xin, nullptr, &w, &tm, ctx->gm_V[0]));
+        CU(p1_complete(ctx->gm_V[0]));
+        CU(gather(vc[0], ctx->gm_V[0]));
+        CU(cdots(vc[0], Vc, 1, d_scale, d_beta, true));
+        CU(cnorm(vc[0], ctx->gm_V[0]));
+        for (int j = 0; j < k; ++j) {
+            CU(launch_main(ctx, biot::MODE_MATVEC, ctx->gm_V[j], ctx->gm_V[j + 1], &w, &ctx->gm_tmap[j]));
+            CU(p1_complete(ctx->gm_V[j + 1]));
+            CU(gather(vc[j + 1], ctx->gm_V[j + 1]));
+            for (int pass = 0; pass < 2; ++pass) {
+                CU(cdots(vc[j + 1], Vc, j + 1, d_h, hcol(0, j), false));
+                CU(biot::gmres_combine(vc[j + 1], vc[j + 1], Vc, 0, d_h, j + 1, -1.0, nullptr, rows,
+                                       biot::GmresPitch{cw, cw, cw, 0}, nt, ctx->stream));
+            }
+            CU(cdots(vc[j + 1], Vc + (j + 1), 1, d_scale, hcol(j + 1, j), true));
+            if (j + 1 < k) {
+                CU(cnorm(vc[j + 1], ctx->gm_V[j + 1]));
+            } else {   // the last basis vector feeds no matvec pass: compact only
+                CU(biot::gmres_combine(vc[j + 1], vc[j + 1], Vc, 0, nullptr, 0, 1.0, d_scale, rows,
+                                       biot::GmresPitch{cw, cw, cw, 0}, nt, ctx->stream));
+            }
+        }
+        CU(biot::gmres_lsq(d_H, d_beta, k, nt, d_y, ctx->stream));
+        CU(biot::gmres_combine(xout + c0, xin + c0, Vc, 0, d_y, k, 1.0, nullptr, rows, biot::GmresPitch{P, P, cw, 0},
+                               nt, ctx->stream));
+        return BIOT_OK;
+    }
     // v_0 = P~2^{-1} (b - AA x_in) with b = A' x_prev + f, and the norms of b - AA x_in
     CU(launch_main(ctx, biot::MODE_ZOUT, xin, nullptr, &w, &tm, ctx->gm_V[0]));
     CU(p1_complete(ctx->gm_V[0]));

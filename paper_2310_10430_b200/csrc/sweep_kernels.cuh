@@ -181,9 +181,14 @@ int64_t gmres_dots_scratch(int64_t rows, int n_tl, int nb, int64_t *chunk, int *
 // (boff: column offset applied to the b panels -- a time window of them)
 cudaError_t gmres_dots(const double *a, const double *const *b_dev, int boff, int nb, int64_t rows, int64_t pitch,
                        int n_tl, double *scratch, double *out, double *hacc, bool norm, cudaStream_t st);
+// row pitches (doubles) of dst, base, the b panels and dst2: the full panel pitch, or the
+// window width for a compact basis (narrow Gauss-Seidel windows)
+struct GmresPitch {
+    int64_t dst, base, v, dst2;
+};
 cudaError_t gmres_combine(double *dst, const double *base, const double *const *b_dev, int boff, const double *coef,
-                          int nb, double sign, const double *scale, int64_t rows, int64_t pitch, int n_tl,
-                          cudaStream_t st);
+                          int nb, double sign, const double *scale, int64_t rows, GmresPitch pitch, int n_tl,
+                          cudaStream_t st, double *dst2 = nullptr);
 // per step t: y = argmin || beta_t e1 - H_t y ||, H_t (k+1) x k upper Hessenberg at
 // H[(i + j (k+1)) n_tl + t] (Givens rotations on the device, one thread per step)
 cudaError_t gmres_lsq(const double *H, const double *beta, int k, int n_tl, double *y, cudaStream_t st);

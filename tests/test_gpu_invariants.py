@@ -256,3 +256,24 @@ def test_aux_uniform_skip_bitwise(precond, monkeypatch):
     assert np.array_equal(res[0][0], res[1][0])
     assert all(np.array_equal(a, b) for a, b in zip(res[0][1], res[1][1]))
     assert np.array_equal(res[0][2], res[1][2])
+
+
+@pytest.mark.parametrize("precond,K", [(2, 4), (1, 3), (2, 16)])
+def test_gs_gmres_compact_basis_bitwise(precond, K, monkeypatch):
+    """Narrow Gauss-Seidel windows keep the Krylov basis compact (row pitch = window
+    width); iterates and history are bitwise those of the panel-layout basis
+    (BIOT_GMRES_NO_COMPACT=1): same arithmetic, same dot order."""
+    prob = config_problem(1)
+    nt, k = prob.n_t, 4
+    res = []
+    for compact in (False, True):
+        if compact:
+            monkeypatch.delenv("BIOT_GMRES_NO_COMPACT", raising=False)
+        else:
+            monkeypatch.setenv("BIOT_GMRES_NO_COMPACT", "1")
+        g = _seeded(prob, nt, precond=precond, omega=1.0)
+        g.iterate_gs_gmres(K, k)
+        res.append((g.solution(), [g.residual_history(i) for i in range(K)]))
+        g.close()
+    assert np.array_equal(res[0][0], res[1][0])
+    assert all(np.array_equal(a, b) for a, b in zip(res[0][1], res[1][1]))
