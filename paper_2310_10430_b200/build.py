@@ -38,7 +38,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     out = out or OUT
     if not variant and not force and not _stale():
         return OUT
-    bdir = BUILD if not variant else BUILD + "_" + os.path.splitext(os.path.basename(out))[0]
+    bdir = BUILD if not variant else os.path.join(BUILD, "variant_" + os.path.splitext(os.path.basename(out))[0])
     os.makedirs(bdir, exist_ok=True)
     dflags = [f"-D{d}" for d in defines]
     def compile_one(src):

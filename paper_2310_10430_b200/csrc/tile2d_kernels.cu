@@ -722,8 +722,7 @@ __device__ __forceinline__ void load_z(double (&z)[2][kT2], const double *zrow, 
 template <bool CLS, bool S0, int NL, class A>
 __device__ __forceinline__ void finish_p1(const A &a, const double *po, const double *pu, int p, int lane,
                                           const double *aux, const double *T, int64_t i, int t0, bool ghost,
-                                          bool whole, bool own, double *carry, const double (&sv)[kT2],
-                                          double (&acc)[3][kT2], double (&q)[kT2], double (&nu)[kT2],
+                                          bool whole, bool own, double *carry, double (&acc)[3][kT2], double (&q)[kT2], double (&nu)[kT2],
                                           double (&npn)[kT2], double *zd, double wdv, double (&y)[kT2]) {
     accum_row<1, CLS, S0, A>(a, pu, p, lane, aux, T, acc, q);
     if constexpr (NL > 1) {
@@ -757,16 +756,11 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
     for (int h = 0; h < 2; ++h) {
         double acc2[3][2], q2[2], xs2[3][2], nu2[2] = {0.0, 0.0}, np2[2] = {0.0, 0.0}, outx[3][2], outz[3][2];
         Loads<3, 2, 1> ld;
-#ifdef BIOT_P1_SV_REG
-        ld.sv[0][0] = sv[2 * h];
-        ld.sv[0][1] = sv[2 * h + 1];
-#else
         {   // the load scales from L1 at the point of use: 8 registers fewer across the march
             const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
             ld.sv[0][0] = s2.x;
             ld.sv[0][1] = s2.y;
         }
-#endif
 #pragma unroll
         for (int c = 0; c < 3; ++c) ld.F[0][c] = aux[7 + c];
 #pragma unroll
@@ -859,7 +853,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     constexpr uint32_t kAuxBytes = L::kAuxBytes, kStageBytes = L::kStageBytes;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
-    __shared__ uint64_t zbar[2];                                         // z_u row published (per buffer)
     __shared__ __align__(16) double aux_u[kAuxRecU];                     // the aux-uniform record
     double *zbuf = reinterpret_cast<double *>(smem + L::kZOff);          // [2][12][2][kCT]
     double *qcarry = reinterpret_cast<double *>(smem + L::kCarryOff);    // [kMaxRR + 1][kSeg]
@@ -874,8 +867,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], kSeg);
         }
-        mbar_init(&zbar[0], kSeg);   // one arrival per warp: a waiter wakes at most kSeg times
-        mbar_init(&zbar[1], kSeg);
         fence_barrier_init();
     }
     if (threadIdx.x < kAuxRecU) aux_u[threadIdx.x] = a.aux_u[threadIdx.x];
@@ -911,7 +902,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     const int p = warp + 1;                   // strip position: 1..12, owned 2..11
     const double *const cls_base = a.cls;     // class stencils (boundary nodes) from global memory
     uint32_t it = 0;
-    uint32_t zph[2] = {0u, 0u};               // phase of each z_u barrier
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int i0 = (tile % nseg) * kSegP1, ja = (tile / nseg) * rr, jb = min(nrows, ja + rr);
         const int col = i0 + p - 2;
@@ -922,19 +912,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const int t0 = chunk * kCT + lane * 2;
             const bool ghost = chunk == 0;
             const bool whole = (chunk + 1) * kCT <= a.n_tl && (chunk > 0 || a.t_lo == 0);
-            double nu[kT2], npn[kT2], sv[kT2];
+            double nu[kT2], npn[kT2];
             const bool first = tile == (int)blockIdx.x;
-#ifdef BIOT_P1_SV_REG
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const double2 s2 = __ldg(reinterpret_cast<const double2 *>(a.s + a.t_off + t0 + h * (kCT / 2)));
-                sv[2 * h] = s2.x;
-                sv[2 * h + 1] = s2.y;
-            }
-#else
-#pragma unroll
-            for (int tt = 0; tt < kT2; ++tt) sv[tt] = 0.0;   // unused (finish_p1 reads a.s)
-#endif
 #pragma unroll
             for (int tt = 0; tt < kT2; ++tt) nu[tt] = npn[tt] = 0.0;
             if (ghost && nchunks > 1 && ocol) {
@@ -981,10 +960,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         wB = a.omega * aux[12];
                         if (kindP == 1)
                             finish_p1<false, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                 whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                                                                 whole, own, carry, acc, q, nu, npn, zd, wB, yB);
                         else
                             finish_p1<true, S0, NL, Tile2dArgs>(a, pd, pm, p, lane, aux, T, i, t0, ghost && nchunks == 1,
-                                                                whole, own, carry, sv, acc, q, nu, npn, zd, wB, yB);
+                                                                whole, own, carry, acc, q, nu, npn, zd, wB, yB);
                     } else {
 #pragma unroll
                         for (int c = 0; c < 2; ++c)
@@ -995,21 +974,11 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 }
                 kindB = (orow1 && ocol) ? kindP : 0;
                 kindP = 0;
-                // (2) this thread's z_u of row m-1 is published (the chunk's first row step
-                // instead fences the z buffers against the previous chunk's last reads)
-                const int zb = (m - 1) & 1;
-#ifdef BIOT_P1_MBAR
-                if (m >= ja) {
-                    __syncwarp();                                  // the warp's z_u stores, then one release
-                    if (lane == 0) mbar_arrive(&zbar[zb]);
-                } else {
-                    named_barrier_sync(1, kSeg * 32);
-                }
-#else
+                // (2) the chunk's first row step fences the z buffers against the previous
+                // chunk's last reads
                 if (m < ja) named_barrier_sync(1, kSeg * 32);
-#endif
                 // (3) start node m (z rows ja-1..jb on the mesh): independent of the z_u
-                // exchange, so it overlaps the other warps' publishing
+                // exchange, so it runs before the barrier
                 int kindC = 0;
                 if (m <= jb && valid && m >= 0 && m < nrows) {
                     const double *aux = (NL == 1 && seg_uniform(a, m, i0 - 1)) ? aux_u
@@ -1021,18 +990,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     if (kindP == 1) start<false, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                     else start<true, S0, Tile2dArgs>(a, pd, pm, p, lane, aux, T, acc, q);
                 }
-                // (4) every z_u of row m-1 published: B^T contributions of row m-1's z_u to
-                // node m-2 (its +W slots; then complete), node m-1 (0 slots), node m (-W slots)
-#ifdef BIOT_P1_MBAR
-                if (m >= ja) {
-                    mbar_wait_suspend(&zbar[zb], zph[zb]);
-                    zph[zb] ^= 1u;
-                }
-#else
-                // a hardware barrier: waiting warps issue nothing (an mbarrier wait re-polls
-                // at every barrier event of the CTA -- ~24 polls per row step measured)
+                // (4) every z_u of row m-1 published (a hardware barrier: waiting warps issue
+                // nothing, where an mbarrier wait re-polled at every barrier event of the CTA,
+                // ~24 polls per row step measured; it also orders the buffer's reuse two row
+                // steps later): B^T contributions of row m-1's z_u to node m-2 (its +W slots;
+                // then complete), node m-1 (0 slots), node m (-W slots)
                 if (m >= ja) named_barrier_sync(2, kSeg * 32);
-#endif
                 if (m >= ja && ocol) {
                     // the z_u columns p-1, p (registers), p+1, each read once and applied to
                     // every node of this column that uses it, in ascending column order per node

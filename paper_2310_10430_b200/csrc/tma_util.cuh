@@ -32,25 +32,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 // wait with a suspend-time hint: the thread sleeps in the barrier unit until the
 // phase completes (or the hint expires) instead of spinning on issue slots
 __device__ __forceinline__ void mbar_wait_suspend(uint64_t *bar, uint32_t parity) {
-#if defined(BIOT_WAIT_NOHINT)
-    mbar_wait(bar, parity);
-#elif defined(BIOT_WAIT_TEST)
-    // test first: a completed phase costs one instruction, no sleep bookkeeping
-    uint32_t done = 0;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (done) return;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
-            : "memory");
-    }
-#else
     uint32_t done = 0;
     while (!done) {
         asm volatile(
@@ -59,7 +40,6 @@ __device__ __forceinline__ void mbar_wait_suspend(uint64_t *bar, uint32_t parity
             : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
             : "memory");
     }
-#endif
 }
 // producer-side wait: back off between polls so the spinning thread does not
 // take issue slots from the consumer warps sharing its scheduler
