@@ -1863,11 +1863,19 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
             if (r != CUDA_SUCCESS)
                 return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (4D) failed: " + std::to_string((int)r));
             if (k == 0 && ctx->z) {
-                r = encode(&ctx->tmapz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, ctx->z, dims, strides, bx, es,
+                // the P~1 second pass stages z_u only: {time, component, x, y, z}, box of 3
+                // components (r_p is read per node)
+                uint32_t bz[5];
+                biot::tile3d_box_z(bz);
+                cuuint64_t dz[5] = {(cuuint64_t)ctx->pitch, 4, (cuuint64_t)n1, (cuuint64_t)n1, (cuuint64_t)n1};
+                cuuint64_t sz[4] = {rb, rb * 4, rb * (cuuint64_t)(n1 * 4), rb * (cuuint64_t)(n1 * n1 * 4)};
+                cuuint32_t bxz[5] = {bz[0], bz[1], bz[2], bz[3], bz[4]};
+                cuuint32_t esz[5] = {1, 1, 1, 1, 1};
+                r = encode(&ctx->tmapz, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, ctx->z, dz, sz, bxz, esz,
                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
                 if (r != CUDA_SUCCESS)
-                    return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (4D, Z) failed: " + std::to_string((int)r));
+                    return fail(ctx, BIOT_E_CUDA, "cuTensorMapEncodeTiled (5D, Z) failed: " + std::to_string((int)r));
             }
         }
     } else {

@@ -165,6 +165,7 @@ int tile3d_chunk();
 int tile3d_max_zrows();
 int tile3d_min_n1();
 void tile3d_box(uint32_t *box);      // {time, x*4+c, y, z}
+void tile3d_box_z(uint32_t *box);    // {time, c, x, y, z}: the P~1 second pass's Z-panel box
 cudaError_t tile3d_shape(int device, LaunchShape *out);
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st);

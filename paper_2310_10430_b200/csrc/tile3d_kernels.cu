@@ -52,22 +52,34 @@ constexpr int kSX = kBX + 2, kSY = kBY + 2;   // staged incl. halo
 constexpr int kNodes = kBX * kBY;          // consumer warps (one node each)
 constexpr int kT3 = 2;                     // time steps per lane
 constexpr int kTc = 32 * kT3;              // time steps per chunk
-constexpr int kStages = 3;
 constexpr int kMaxZ = 24;                  // planes per tile (q carry capacity)
 constexpr int kCW = Tile3dArgs::kClsW;     // doubles per class-stencil slot
 constexpr int kClsD = 272;                 // doubles per class stencil in shared memory (15*18 padded)
 constexpr int kClsLocal = 8;               // classes a tile can touch: 2 (x) x 2 (y) x 2 (z; one z face per tile)
-constexpr uint32_t kXBytes = kSX * kSY * 4 * kTc * 8;                          // 61440
 constexpr uint32_t kAuxRec = Tile3dArgs::kAux;                                 // doubles per record
 constexpr uint32_t kAuxRowBytes = kBX * kAuxRec * 8;                           // 768
 constexpr uint32_t kAuxBytes = kBY * kAuxRowBytes;                             // 2304
-constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;      // 63744
-constexpr uint32_t kClsOff = kStages * kStageBytes;
-constexpr uint32_t kCarryOff = kClsOff + kClsLocal * kClsD * 8;
-constexpr uint32_t kSmemBytes = kCarryOff + kMaxZ * kNodes * 8;
+// Shared-memory layout by mode.  The sweep modes stage all 4 components of every column
+// of a plane (61 KB) in a 3-stage ring, one plane of lookahead.  The P~1 second pass
+// (B^T z_u, memory-bound: ~45 FMAs per node and step) stages only z_u's 3 components
+// through a 5D box {steps, comps 0-2, x, y, z} of the Z panel (46 KB; r_p, the fourth,
+// is read per node from global memory) in a 4-stage ring: two planes in flight.
+template <int MODE>
+struct Lay3 {
+    static constexpr int kNC = MODE == MODE_PASS2 ? 3 : 4;                              // staged components
+    static constexpr int kStages = MODE == MODE_PASS2 ? 4 : 3;
+    static constexpr uint32_t kXBytes = kSX * kSY * kNC * kTc * 8;                      // 61440 / 46080
+    static constexpr uint32_t kStageBytes = (kXBytes + kAuxBytes + 127) / 128 * 128;  // 63744 / 48384
+    static constexpr uint32_t kClsOff = kStages * kStageBytes;
+    static constexpr uint32_t kCarryOff = kClsOff + kClsLocal * kClsD * 8;
+    static constexpr uint32_t kSmemBytes = kCarryOff + kMaxZ * kNodes * 8;
+};
+constexpr uint32_t kSmemBytes = Lay3<MODE_UPDATE_P2>::kSmemBytes > Lay3<MODE_PASS2>::kSmemBytes
+                                    ? Lay3<MODE_UPDATE_P2>::kSmemBytes : Lay3<MODE_PASS2>::kSmemBytes;
+constexpr int kStagesMax = 4;
 constexpr int kThreads3 = (kNodes + 4) * 32;
 constexpr int kProducerRegs = 24, kConsumerRegs = 160;   // 4*32*24 + 12*32*160 <= 65536
-static_assert(kSmemBytes + kNodes * kTc * 2 * 8 + 2 * kStages * 8 <= 232448, "tile3d shared memory exceeds 227 KB");
+static_assert(kSmemBytes + kNodes * kTc * 2 * 8 + 2 * kStagesMax * 8 <= 232448, "tile3d shared memory exceeds 227 KB");
 
 // (dx, dy, dz) of the 15 BDIA slots in storage order (offsets sorted ascending,
 // self first): 0, -V-W-1, -V-W, -V-1, -V, -W-1, -W, -1, 1, W, W+1, V, V+1, V+W, V+W+1
@@ -142,8 +154,10 @@ __device__ __forceinline__ void fma_cls(double (&acc)[4][T], double (&q)[T], con
 }
 
 // staged column (sx, sy) of a plane: component cc at + cc * kTc, the lane's two steps at + 2 lane
+// (NC components staged per column)
+template <int NC = 4>
 __device__ __forceinline__ const double *col_ptr(const double *plane, int sx, int sy, int lane) {
-    return plane + (sy * kSX + sx) * 4 * kTc + 2 * lane;
+    return plane + (sy * kSX + sx) * NC * kTc + 2 * lane;
 }
 
 __device__ __forceinline__ void load_col(double (&v)[4][kT3], const double *cp) {
@@ -324,7 +338,7 @@ __device__ __forceinline__ void accum_plane_bt(const Tile3dArgs &a, const double
         for (int dx = -1; dx <= 1; ++dx) {
             const int s = slot_of(dx, dy, DZ);
             if (s < 0) continue;
-            const double *cp = col_ptr(pl, sx + dx, sy + dy, lane);
+            const double *cp = col_ptr<3>(pl, sx + dx, sy + dy, lane);
 #pragma unroll
             for (int cc = 0; cc < 3; ++cc) {
                 if constexpr (!CLS) {
@@ -341,11 +355,12 @@ __device__ __forceinline__ void accum_plane_bt(const Tile3dArgs &a, const double
 template <bool CLS, bool S0>
 __device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po, const double *pu,
                                           const double *aux, int64_t i, int sx, int sy, int lane, int t,
-                                          const double *T, double (&bt)[kT3], const double (&xpre)[kT3]) {
+                                          const double *T, double (&bt)[kT3], const double (&xpre)[kT3],
+                                          const double (&rpre)[kT3]) {
     accum_plane_bt<1, CLS, S0>(a, pu, sx, sy, lane, T, bt);
     const int64_t P = a.pitch, row = i * 4 * P + 3 * P + a.t_off + t;
-    const double2 rp = *reinterpret_cast<const double2 *>(col_ptr(po, sx, sy, lane) + 3 * kTc);
-    const double x0 = xpre[0], x1 = xpre[1];   // x_p^k, prefetched when the node was started
+    const double2 rp = make_double2(rpre[0], rpre[1]);   // r_p and x_p^k, prefetched when the
+    const double x0 = xpre[0], x1 = xpre[1];              // node was started
     if (a.s0buf && t == 0) a.s0buf[i * 8 + 3] = bt[0];   // deferred first step
     const double v0 = fma(a.omega, aux[22] * (bt[0] - rp.x), x0);
     const double v1 = fma(a.omega, aux[22] * (bt[1] - rp.y), x1);
@@ -380,6 +395,10 @@ __device__ __forceinline__ int axis_class(int v, int n1) { return v == 0 ? 0 : (
 template <bool S0, int MODE>
 __global__ void __launch_bounds__(kThreads3, 1)
     tile3d_kernel(const __grid_constant__ CUtensorMap tmx, const Tile3dArgs a) {
+    using L = Lay3<MODE>;
+    constexpr int kStages = L::kStages;
+    constexpr uint32_t kXBytes = L::kXBytes, kStageBytes = L::kStageBytes;
+    constexpr uint32_t kClsOff = L::kClsOff, kCarryOff = L::kCarryOff;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ uint64_t full[kStages], empty[kStages];
     __shared__ double red[kNodes][kTc][2];
@@ -414,7 +433,10 @@ __global__ void __launch_bounds__(kThreads3, 1)
                         unsigned char *base = smem + (size_t)st * kStageBytes;
                         const bool real = (z >= 0 && z < g.n1);
                         mbar_expect_tx(&full[st], kXBytes + (real ? (uint32_t)ny * kAuxRowBytes : 0u));
-                        load_4d(base, &tmx, a.t_off + chunk * kTc, (x0 - 1) * 4, y0 - 1, z, &full[st]);
+                        if constexpr (MODE == MODE_PASS2)
+                            load_5d(base, &tmx, a.t_off + chunk * kTc, 0, x0 - 1, y0 - 1, z, &full[st]);
+                        else
+                            load_4d(base, &tmx, a.t_off + chunk * kTc, (x0 - 1) * 4, y0 - 1, z, &full[st]);
                         if (real)
                             for (int yy = 0; yy < ny; ++yy)
                                 bulk_g2s(base + kXBytes + yy * kAuxRowBytes,
@@ -475,8 +497,8 @@ __global__ void __launch_bounds__(kThreads3, 1)
                         const int64_t iA = ((int64_t)(m - 1) * g.n1 + y) * g.n1 + xA;
                         double *carry = qcarry + (m - 1 - za) * kNodes + warp;
                         if constexpr (MODE == MODE_PASS2) {   // bt rides in q
-                            if (kindP == 1) finish_bt<false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3]);
-                            else finish_bt<true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3]);
+                            if (kindP == 1) finish_bt<false, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3], acc[2]);
+                            else finish_bt<true, S0>(a, pd, pm, aux, iA, sx, sy, lane, t, TAp, q, acc[3], acc[2]);
                         } else {
                             if (kindP == 1)
                                 finish<false, S0, MODE>(a, pd, pm, aux, iA, sx, sy, lane, t, ghost, carry, sv, TAp, acc, q,
@@ -499,13 +521,18 @@ __global__ void __launch_bounds__(kThreads3, 1)
                             // prefetch x_p^k of the node (used at its finish, one plane later): its
                             // global-load latency then overlaps the plane march instead of stalling it
                             const int64_t rowp = (((int64_t)m * g.n1 + y) * g.n1 + xA) * 4 * a.pitch + 3 * a.pitch + a.t_off + t;
-                            acc[3][0] = acc[3][1] = 0.0;
+                            // (and r_p from the Z panel's fourth component, which the box does not stage)
+                            acc[3][0] = acc[3][1] = acc[2][0] = acc[2][1] = 0.0;
                             if (t + 1 < a.n_tl) {
                                 const double2 xv = __ldg(reinterpret_cast<const double2 *>(a.x + rowp));
+                                const double2 rv = __ldg(reinterpret_cast<const double2 *>(a.zbuf + rowp));
                                 acc[3][0] = xv.x;
                                 acc[3][1] = xv.y;
+                                acc[2][0] = rv.x;
+                                acc[2][1] = rv.y;
                             } else if (t < a.n_tl) {
                                 acc[3][0] = __ldg(a.x + rowp);
+                                acc[2][0] = __ldg(a.zbuf + rowp);
                             }
                             if (kindP == 1) {
                                 accum_plane_bt<-1, false, S0>(a, pd, sx, sy, lane, TAp, q);
@@ -602,6 +629,15 @@ void tile3d_box(uint32_t *box) {
     box[1] = kSX * 4;
     box[2] = kSY;
     box[3] = 1;
+}
+
+// box of the 5D Z-panel map {steps, component, x, y, z} the P~1 second pass stages
+void tile3d_box_z(uint32_t *box) {
+    box[0] = kTc;
+    box[1] = Lay3<MODE_PASS2>::kNC;
+    box[2] = kSX;
+    box[3] = kSY;
+    box[4] = 1;
 }
 
 cudaError_t tile3d_shape(int device, LaunchShape *out) {
