@@ -232,6 +232,12 @@ struct biot_ctx {
     int64_t *d_iter = nullptr;        // device copy of `iterations`
     cudaGraphExec_t gexec[2] = {nullptr, nullptr};
     cudaEvent_t gev[4] = {nullptr, nullptr, nullptr, nullptr};   // sweep spans inside the graph
+    // the captured graphs (kept: their event-record nodes re-target per replay) and those
+    // nodes in gev order; gev_pool: the spans of sampled replays of the current call
+    cudaGraph_t gsrc[2] = {nullptr, nullptr};
+    cudaGraphNode_t gnode[2][4] = {{nullptr, nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr, nullptr}};
+    std::vector<cudaEvent_t> gev_pool;
+    bool gpool_set[2] = {false, false};   // the exec's nodes currently target gev_pool events
     cudaStream_t cap_stream = nullptr;
     cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     std::vector<cudaEvent_t> ev_s;                 // 2 per iteration of the current call
@@ -287,6 +293,10 @@ void free_all(biot_ctx *c) {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : c->ev_s) cudaEventDestroy(e);
     for (cudaEvent_t e : c->gev)
+        if (e) cudaEventDestroy(e);
+    for (cudaGraph_t g : c->gsrc)
+        if (g) cudaGraphDestroy(g);
+    for (cudaEvent_t e : c->gev_pool)
         if (e) cudaEventDestroy(e);
     for (cudaGraphExec_t g : c->gexec)
         if (g) cudaGraphExecDestroy(g);
@@ -796,8 +806,25 @@ biot_status build_graph(biot_ctx *ctx, int cur) {
     }
     if (e3 != cudaSuccess) return fail(ctx, BIOT_E_CUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e3));
     e = cudaGraphInstantiate(&ctx->gexec[cur], g, 0);
-    cudaGraphDestroy(g);
-    if (e != cudaSuccess) return fail(ctx, BIOT_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(ctx, BIOT_E_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    // the sweep-span event-record nodes, so that biot_iterate can time sampled replays
+    size_t nn = 0;
+    CU(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    CU(cudaGraphGetNodes(g, nodes.data(), &nn));
+    for (cudaGraphNode_t n : nodes) {
+        cudaGraphNodeType ty;
+        CU(cudaGraphNodeGetType(n, &ty));
+        if (ty != cudaGraphNodeTypeEventRecord) continue;
+        cudaEvent_t ev = nullptr;
+        CU(cudaGraphEventRecordNodeGetEvent(n, &ev));
+        for (int h = 0; h < 4; ++h)
+            if (ev == ctx->gev[h]) ctx->gnode[cur][h] = n;
+    }
+    ctx->gsrc[cur] = g;
     return BIOT_OK;
 }
 
@@ -1972,9 +1999,37 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
         ctx->ev_s.push_back(e);
     }
     CU(cudaEventRecord(ctx->ev_a, ctx->stream));
+    // the sweep spans of up to 8 replays spread over the call are kept (each sampled replay
+    // records into its own events; the others into gev, re-targeted only when the target
+    // changes: a few host calls per call), so last_timing's sweep time is an average over
+    // the whole call, not the final replay alone
+    const int cg = ctx->cur;
+    const bool sample = pairs > 0 && ctx->gnode[cg][0] && ctx->gnode[cg][1] && ctx->gnode[cg][2] && ctx->gnode[cg][3];
+    const int32_t stride = std::max<int32_t>(1, (pairs + 7) / 8);
+    int32_t nsamp = 0;
+    if (sample) {
+        const size_t need = 4 * (size_t)((pairs + stride - 1) / stride);
+        while (ctx->gev_pool.size() < need) {
+            cudaEvent_t e;
+            CU(cudaEventCreate(&e));
+            ctx->gev_pool.push_back(e);
+        }
+    }
     if (pairs > 0) {
         CU(biot::launch_counter(ctx->d_iter, ctx->iterations, false, ctx->stream));
-        for (int32_t k = 0; k < pairs; ++k) CU(cudaGraphLaunch(ctx->gexec[ctx->cur], ctx->stream));
+        bool on_pool = ctx->gpool_set[cg];
+        for (int32_t k = 0; k < pairs; ++k) {
+            const bool take = sample && (pairs - 1 - k) % stride == 0;   // the last replay is always sampled
+            if (take || on_pool) {
+                for (int h = 0; h < 4; ++h)
+                    CU(cudaGraphExecEventRecordNodeSetEvent(ctx->gexec[cg], ctx->gnode[cg][h],
+                                                            take ? ctx->gev_pool[4 * nsamp + h] : ctx->gev[h]));
+                on_pool = take;
+            }
+            CU(cudaGraphLaunch(ctx->gexec[cg], ctx->stream));
+            if (take) ++nsamp;
+        }
+        ctx->gpool_set[cg] = on_pool;
         ctx->iterations += 2 * pairs;
     }
     for (int32_t k = 0; k < eager; ++k) {
@@ -2001,7 +2056,14 @@ biot_status biot_iterate(biot_ctx *ctx, int32_t K) {
         sweep_ms += ms;
         ++spans;
     }
-    if (pairs > 0)
+    for (int32_t k = 0; k < nsamp; ++k)
+        for (int h = 0; h < 2; ++h) {
+            float ms = 0.f;
+            CU(cudaEventElapsedTime(&ms, ctx->gev_pool[4 * k + 2 * h], ctx->gev_pool[4 * k + 2 * h + 1]));
+            sweep_ms += ms;
+            ++spans;
+        }
+    if (pairs > 0 && nsamp == 0)
         for (int h = 0; h < 2; ++h) {
             float ms = 0.f;
             CU(cudaEventElapsedTime(&ms, ctx->gev[2 * h], ctx->gev[2 * h + 1]));

@@ -68,8 +68,15 @@ __global__ void __launch_bounds__(kCThreads) cheb_step_kernel(const ChebArgs a) 
     const int64_t n_warps = a.n_nodes * n_chunks;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+#ifdef BIOT_CHEB_NODE_MAJOR
         const int64_t i = w / n_chunks;
         const int t0 = (int)(w % n_chunks) * kChunk + lane * kT;
+#else
+        // chunk-major: the warps of a block (and of neighbouring blocks) take consecutive
+        // nodes of one chunk, so the gathered neighbour columns are shared in L1 / L2
+        const int64_t i = w % a.n_nodes;
+        const int t0 = (int)(w / a.n_nodes) * kChunk + lane * kT;
+#endif
         if (t0 >= a.n_tl) continue;
         const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
         double acc[NC][kT];
@@ -161,8 +168,15 @@ __global__ void __launch_bounds__(kCThreads) cheb_p1_rhs_kernel(const ChebArgs a
     const int64_t n_warps = a.n_nodes * n_chunks;
     for (int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; w < n_warps;
          w += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+#ifdef BIOT_CHEB_NODE_MAJOR
         const int64_t i = w / n_chunks;
         const int t0 = (int)(w % n_chunks) * kChunk + lane * kT;
+#else
+        // chunk-major: the warps of a block (and of neighbouring blocks) take consecutive
+        // nodes of one chunk, so the gathered neighbour columns are shared in L1 / L2
+        const int64_t i = w % a.n_nodes;
+        const int t0 = (int)(w / a.n_nodes) * kChunk + lane * kT;
+#endif
         if (t0 >= a.n_tl) continue;
         const double *__restrict__ bp = a.blk + i * (int64_t)(S * W);
         double bt[kT] = {0.0, 0.0, 0.0, 0.0};

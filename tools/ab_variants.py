@@ -26,13 +26,14 @@ def child(args):
     nt = prob.n_t
     g = BiotSolver(prob, precond=args.precond, omega=args.omega, load_scale=load_scales(nt, parity=True))
     g.set_iterate(1, initial_iterate(prob.dirichlet, np.arange(1, nt + 1), 5))
-    g.iterate(args.K)
+    run = (lambda k: g.iterate_cheb(k, args.cheb_m)) if args.cheb_m else g.iterate
+    run(args.K)
     x = g.solution()
     h = hashlib.sha1(np.ascontiguousarray(x).tobytes()).hexdigest()
-    g.iterate(3)
+    run(3)
     its, sws = [], []
     for _ in range(args.repeats):
-        g.iterate(args.steps)
+        run(args.steps)
         it, sw = g.last_timing()
         its.append(it)
         sws.append(sw)
@@ -51,6 +52,7 @@ def main():
     ap.add_argument("--K", type=int, default=3)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--repeats", type=int, default=5)
+    ap.add_argument("--cheb-m", type=int, default=0, help="time biot_iterate_cheb(K, m) instead")
     ap.add_argument("--child", action="store_true")
     a = ap.parse_args()
     if a.omega is None:
@@ -65,7 +67,7 @@ def main():
             env["BIOT_LIB_OVERRIDE"] = os.path.abspath(lib)
         cmd = [sys.executable, os.path.abspath(__file__), "--child", "--config", str(a.config), "--precond",
                str(a.precond), "--omega", str(a.omega), "--K", str(a.K), "--steps", str(a.steps), "--repeats",
-               str(a.repeats), "x"]
+               str(a.repeats), "--cheb-m", str(a.cheb_m), "x"]
         r = subprocess.run(cmd, env=env, capture_output=True, text=True)
         if r.returncode != 0:
             print(f"{lib}: FAILED\n{r.stderr[-2000:]}", flush=True)
