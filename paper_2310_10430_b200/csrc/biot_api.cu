@@ -185,6 +185,7 @@ struct biot_ctx {
     // fused single-pass P~1 (tile2d MODE_P1_FUSED): its own tile shape and partial groups
     bool p1_fused = false;
     int32_t rows_per_tile_p1 = 0;
+    int32_t n_rblk = 0;               // tile2d (P~2 family): balanced row blocks (Tile2dArgs::n_rblk)
     int64_t groups_p1 = 0;
     double *aux_base = nullptr;       // aux records with front padding (tile2d halo columns)
     int32_t aux_geo = 0, ux0 = 0, ux1 = -1, uy0 = 0, uy1 = -1;   // tile2d aux-uniform rectangle
@@ -595,7 +596,11 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         a.uy0 = c->uy0;
         a.uy1 = c->uy1;
         std::memcpy(a.aux_u, c->aux_u, sizeof(a.aux_u));
-        if (mode == biot::MODE_P1_FUSED) a.rows_per_tile = c->rows_per_tile_p1;
+        a.n_rblk = c->n_rblk;
+        if (mode == biot::MODE_P1_FUSED) {
+            a.rows_per_tile = c->rows_per_tile_p1;
+            a.n_rblk = 0;
+        }
         a.ghost_stride = 1;
         a.t_off = 0;
         a.t_lo = 0;
@@ -1646,23 +1651,40 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
     } else if (ctx->kern == 4) {
         CU(biot::tile2d_shape(ctx->device, &ctx->shape));
         reserve_comm_sms(ctx);
-        // rows per tile: minimise (waves of tiles) x (rows + halo cost)
+        // row blocks: n_rblk balanced blocks (sizes floor / ceil of n_rows / n_rblk, at most
+        // the kernel's row capacity), chosen to minimise the rows streamed per CTA -- every
+        // block reads its two halo rows again (mostly from HBM: measured) -- plus
+        // half the excess of the busiest CTA (the last round of tiles)
         const int64_t n_seg = (ctx->row_w + biot::tile2d_seg() - 1) / biot::tile2d_seg();
-        int64_t rpt = 1;
+        const int64_t cap = biot::tile2d_max_rows(), G = ctx->shape.grid;
+        int64_t nrb = (ctx->n_rows + cap - 1) / cap;
         double best = 1e300;
-        for (int64_t rr = 1; rr <= biot::tile2d_max_rows(); ++rr) {
-            const int64_t waves = (n_seg * ((ctx->n_rows + rr - 1) / rr) + ctx->shape.grid - 1) / ctx->shape.grid;
-            const double cost = (double)waves * ((double)std::min<int64_t>(rr, ctx->n_rows) + 0.25);
-            if (cost < best - 1e-9) { best = cost; rpt = rr; }
+        for (int64_t nb = (ctx->n_rows + cap - 1) / cap; nb <= ctx->n_rows; ++nb) {
+            const int64_t tiles = n_seg * nb, rounds = (tiles + G - 1) / G;
+            const double avg = (double)n_seg * (double)(ctx->n_rows + 2 * nb) / (double)G;
+            const double crit = (double)rounds * (double)((ctx->n_rows + nb - 1) / nb + 2);
+            const double cost = avg + 0.5 * std::max(0.0, crit - avg);
+            if (cost < best - 1e-9) { best = cost; nrb = nb; }
+            if (rounds > 64) break;
         }
-        if (const char *e = std::getenv("BIOT_MARCH_ROWS")) rpt = std::max(1, std::atoi(e));
+        int64_t rpt = (ctx->n_rows + nrb - 1) / nrb;
+        ctx->n_rblk = (int32_t)nrb;
+        if (const char *e = std::getenv("BIOT_MARCH_ROWS")) {   // uniform blocks of this many rows
+            rpt = std::max(1, std::atoi(e));
+            ctx->n_rblk = 0;
+        }
+        if (const char *e = std::getenv("BIOT_ROW_BLOCKS")) {   // this many balanced blocks
+            ctx->n_rblk = std::max(1, std::atoi(e));
+            rpt = (ctx->n_rows + ctx->n_rblk - 1) / ctx->n_rblk;
+        }
         if (rpt > biot::tile2d_max_rows())
-            return fail(ctx, BIOT_E_INVALID, "BIOT_MARCH_ROWS exceeds the tile kernel's row capacity");
+            return fail(ctx, BIOT_E_INVALID, "row blocks exceed the tile kernel's row capacity");
         ctx->rows_per_tile = (int32_t)rpt;
         biot::Tile2dArgs tmp{};
         tmp.row_w = ctx->row_w;
         tmp.n_rows = ctx->n_rows;
         tmp.rows_per_tile = ctx->rows_per_tile;
+        tmp.n_rblk = ctx->n_rblk;
         ctx->groups = biot::tile2d_groups(tmp, ctx->shape.grid);
         {
             // fused P~1: 10 owned columns per tile, 2 extra z_u rows and 4 extra x rows per tile

@@ -98,6 +98,10 @@ struct Tile2dArgs : SweepArgs {
     // (pp entries against fixed pressure columns may differ: they multiply x = 0), so row
     // strips inside it skip the aux bulk copy and read aux_u (staged once in shared memory)
     int32_t aux_geo, ux0, ux1, uy0, uy1;
+    // P~2-family tile kernels: the grid rows split into n_rblk blocks of floor/ceil(n_rows /
+    // n_rblk) rows (block r: rows [r n_rows / n_rblk, (r+1) n_rows / n_rblk)); rows_per_tile
+    // is then the largest block. 0: uniform blocks of rows_per_tile rows (the fused P~1)
+    int32_t n_rblk;
     double aux_u[kAuxRecU];
 };
 

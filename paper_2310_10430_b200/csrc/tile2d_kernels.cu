@@ -425,20 +425,27 @@ __device__ __forceinline__ void finish_mv(const A &a, const double *pu, int p, i
 
 struct Geo2 {
     int W, nrows, nseg, nrr, ntiles, nchunks, rr;
+    bool rb_even;                 // balanced row blocks (n_rblk)
     __device__ explicit Geo2(const Tile2dArgs &a) {
         W = (int)a.row_w;
         nrows = a.n_rows;
         rr = a.rows_per_tile;
         nseg = (W + kSeg - 1) / kSeg;
-        nrr = (nrows + rr - 1) / rr;
+        rb_even = a.n_rblk > 0;
+        nrr = rb_even ? a.n_rblk : (nrows + rr - 1) / rr;
         ntiles = nseg * nrr;
         nchunks = (a.n_tl + kCT - 1) / kCT;
     }
     __device__ void decode(int tile, int &i0, int &ja, int &jb) const {
         const int seg = tile % nseg, r = tile / nseg;
         i0 = seg * kSeg;
-        ja = r * rr;
-        jb = min(nrows, ja + rr);
+        if (rb_even) {
+            ja = (int)((int64_t)r * nrows / nrr);
+            jb = (int)((int64_t)(r + 1) * nrows / nrr);
+        } else {
+            ja = r * rr;
+            jb = min(nrows, ja + rr);
+        }
     }
 };
 
@@ -1128,7 +1135,8 @@ int tile2d_max_rows() { return kMaxRR; }
 int64_t tile2d_tiles(const Tile2dArgs &a) {
     const int seg = a.mode == MODE_P1_FUSED ? kSegP1 : kSeg;
     const int64_t n_seg = (a.row_w + seg - 1) / seg;
-    const int64_t n_rr = (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
+    const int64_t n_rr = (a.mode != MODE_P1_FUSED && a.n_rblk > 0) ? a.n_rblk
+                                                                      : (a.n_rows + a.rows_per_tile - 1) / a.rows_per_tile;
     return n_seg * n_rr;
 }
 
