@@ -550,6 +550,7 @@ struct Window {
     const double *ghost = nullptr;
     int64_t stride = 1;
     double *send = nullptr;             // send slice (only when the window ends at the slab's last step)
+    bool lead = false;                  // the window starts 2 steps early (see gs_window): no ghost
 };
 
 // tmo / zb (tile kernels only): the tensor map of xin and the Z panel, when they are not
@@ -577,6 +578,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost_stride = win->stride;
             a.sendbuf = win->send;
             if (win->ghost != c->ghost) a.ghost_zero = 0;
+            if (win->lead) a.ghost_zero = 1;
         }
         if (zb) a.zbuf = zb;
         if (tmo) return biot::launch_tile3d(*tmo, a, c->shape, c->stream);
@@ -612,6 +614,7 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
             a.ghost_stride = win->stride;
             a.sendbuf = win->send;
             if (win->ghost != c->ghost) a.ghost_zero = 0;
+            if (win->lead) a.ghost_zero = 1;
         }
         a.s0 = c->s0;
         a.dry = c->tile_dry;
@@ -2183,6 +2186,18 @@ biot_status gs_window(biot_ctx *ctx, int w, int K, int64_t kbase) {
     } else {
         win.ghost = ctx->x[r] + (win.t_off - 1);
         win.stride = ctx->pitch;
+    }
+    // tile kernels (2D P~2 / fused P~1, 3D): start the window two steps early (steps below lo
+    // computed, not stored or counted). q(lo-1) then comes out of the march itself -- lane
+    // 0's second step, in the march's FMA order, which is ghost_q's order: bitwise the same --
+    // instead of lane 0 gathering the ghost column through L2 at every node of the pass
+    if ((ctx->kern == 4 || ctx->kern == 6) && ctx->gs_k == 0 && win.t_off >= 2 && !std::getenv("BIOT_GS_NO_LEAD")) {
+        win.t_off -= 2;
+        win.t_lo = lo - win.t_off;
+        win.len = hi - win.t_off + 1;
+        win.ghost = ctx->x[r] + (win.t_off - 1 >= 0 ? win.t_off - 1 : 0);   // not read: ghost_zero
+        win.stride = ctx->pitch;
+        win.lead = true;
     }
     win.send = (ctx->world > 1 && hi == L - 1 && !ctx->sweep_mode) ? ctx->sendbuf : nullptr;
     int64_t wave_groups = ctx->groups;

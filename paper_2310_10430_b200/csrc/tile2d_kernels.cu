@@ -283,7 +283,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
         }
         if constexpr (MODE == MODE_ZOUT) {
             const int th = t0 + h * (kCT / 2);
-            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl && th + 1 >= a.t_lo;
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 double *dst = a.zbuf + row + c * P + h * (kCT / 2);
@@ -297,7 +297,7 @@ __device__ __forceinline__ void finish(const A &a, const double *po, const doubl
         } else if constexpr (MODE != MODE_RESIDUAL) {
             constexpr int ncw = MODE == MODE_UPDATE_P2 ? 3 : 2;   // P~1: pressure written by pass 2
             const int th = t0 + h * (kCT / 2);
-            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl && th + 1 >= a.t_lo;
 #pragma unroll
             for (int c = 0; c < ncw; ++c) {
                 double *dst = a.xn + row + c * P + h * (kCT / 2);
@@ -386,7 +386,7 @@ __device__ __forceinline__ void finish_bt(const A &a, const double *po, const do
             *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
         } else {
             if (th < a.n_tl && th >= a.t_lo) dst[0] = v0;
-            if (th + 1 < a.n_tl) dst[1] = v1;
+            if (th + 1 < a.n_tl && th + 1 >= a.t_lo) dst[1] = v1;
         }
         if (a.sendbuf) {
             if (th == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v0;
@@ -802,7 +802,7 @@ __device__ __forceinline__ void finish_p1(const A &a, const double *po, const do
                 nu[2 * h + tt] += nu2[tt];       // = the in-place accumulation: nu + (0 + su)
                 npn[2 * h + tt] += np2[tt];
             }
-            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl;
+            const bool st0 = th < n_tl && th >= a.t_lo, st1 = th + 1 < n_tl && th + 1 >= a.t_lo;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
                 double *dst = a.xn + row + c * P + h * (kCT / 2);
@@ -839,7 +839,7 @@ __device__ __forceinline__ void finish_zp(const A &a, int64_t i, int t0, bool wh
             *reinterpret_cast<double2 *>(dst) = make_double2(v0, v1);
         } else {
             if (th < a.n_tl && th >= a.t_lo) dst[0] = v0;
-            if (th + 1 < a.n_tl) dst[1] = v1;
+            if (th + 1 < a.n_tl && th + 1 >= a.t_lo) dst[1] = v1;
         }
         if (a.sendbuf) {
             if (th == a.n_tl - 1) a.sendbuf[i * 3 + 2] = v0;
