@@ -219,8 +219,6 @@ struct biot_ctx {
     int32_t gs_K = 0, gs_w = 0, gs_k = 0;   // gs_k > 0: each window update is a GMRES(gs_k) cycle
     int64_t gs_k0 = 0;
     int32_t n1 = 0, z_rows = 0;
-    int32_t *t3_tab = nullptr, *t3_off = nullptr;   // tile3d schedule (tile3d_schedule): tiles, CTA ranges
-    int32_t t3_ncta = 0;
     int tile_dry = 0;                 // BIOT_TILE_DRY=1: memory-pipeline measurement only
     int64_t gbase[8] = {0};
     int32_t slot[8][3] = {{0}};
@@ -287,8 +285,7 @@ void free_all(biot_ctx *c) {
                     (void *)c->part0, (void *)c->partial, (void *)c->hist,
                     (void *)c->norms, (void *)c->nonfinite, (void *)c->staging, (void *)c->aux_base,
                     (void *)c->cls, (void *)c->fin_scratch, (void *)c->fin_tickets, (void *)c->gm_Vdev, (void *)c->gm_scratch,
-                    (void *)c->gm_small, (void *)c->gm_Vc, (void *)c->gm_Vcdev, (void *)c->d_iter, (void *)c->t3_tab,
-                    (void *)c->t3_off})
+                    (void *)c->gm_small, (void *)c->gm_Vc, (void *)c->gm_Vcdev, (void *)c->d_iter})
         if (p) cudaFree(p);
     for (double *p : c->gm_Vbase) cudaFree(p);
     for (double *p : c->cb_base)
@@ -568,9 +565,6 @@ cudaError_t launch_main(biot_ctx *c, int mode, const double *xin, double *xout, 
         a.cls = c->cls;
         a.n1 = c->n1;
         a.z_rows = c->z_rows;
-        a.ttab = c->t3_tab;
-        a.toff = c->t3_off;
-        a.n_cta = c->t3_ncta;
         a.s0 = c->s0;
         a.dry = c->tile_dry;
         a.ghost_stride = 1;
@@ -1839,37 +1833,10 @@ biot_status biot_setup(const biot_mesh *mesh, const biot_material *mat, const bi
         if (best_zr > biot::tile3d_max_zrows() || best_zr >= n1)
             return fail(ctx, BIOT_E_INVALID, "BIOT_ZROWS must be < n1 and <= the tile kernel's plane capacity");
         ctx->z_rows = (int32_t)best_zr;
-        // static list schedule of the (patch, plane range) tiles over the CTAs: the tail of
-        // the round-robin order cut into shorter plane ranges so the CTAs finish together
-        // (config 4: 1122 tiles of 21-22 planes = 7.6 rounds; cost = planes + h per tile)
-        {
-            double h = 1.0;   // A/B on config 4 (h = 0.25 / 0.5 / 1.0 within 0.5%)
-            if (const char *e = std::getenv("BIOT_T3_H")) h = std::atof(e);
-            std::vector<int32_t> tab, off;
-            double ms = 0, ms_rr = 0;
-            ctx->t3_ncta = biot::tile3d_schedule((int)n1, ctx->z_rows, ctx->shape.grid, h < 0 ? 0.0 : h, tab, off, &ms,
-                                                 &ms_rr);
-            if (h < 0) {   // dev/A-B only: plain round robin of the uncut tiles
-                tab.clear();
-                off.assign(1, 0);
-                std::vector<int32_t> t2, o2;
-                ctx->t3_ncta = biot::tile3d_schedule((int)n1, ctx->z_rows, 1, 0.0, t2, o2);
-                const int64_t nt = (int64_t)t2.size() / 4, G = std::min<int64_t>(nt, ctx->shape.grid);
-                for (int64_t c = 0; c < G; ++c) {
-                    for (int64_t k = c; k < nt; k += G) tab.insert(tab.end(), t2.begin() + 4 * k, t2.begin() + 4 * k + 4);
-                    off.push_back((int32_t)(tab.size() / 4));
-                }
-                ctx->t3_ncta = (int32_t)G;
-            }
-            ctx->groups = (int64_t)(tab.size() / 4);
-            ALLOC(ctx->t3_tab, tab.size() * sizeof(int32_t));
-            CU(h2d(ctx, ctx->t3_tab, tab.data(), tab.size() * sizeof(int32_t)));
-            ALLOC(ctx->t3_off, off.size() * sizeof(int32_t));
-            CU(h2d(ctx, ctx->t3_off, off.data(), off.size() * sizeof(int32_t)));
-            if (std::getenv("BIOT_DEBUG"))
-                std::fprintf(stderr, "[biot] tile3d schedule: %lld tiles over %d CTAs, makespan %.2f planes (round robin %.2f)\n",
-                             (long long)ctx->groups, ctx->t3_ncta, ms, ms_rr);
-        }
+        biot::Tile3dArgs tmp{};
+        tmp.n1 = ctx->n1;
+        tmp.z_rows = ctx->z_rows;
+        ctx->groups = biot::tile3d_groups(tmp);
         // interior template (centre node) + per-node aux records
         const int S = 15, WB = biot::block_width(4), KA = biot::Tile3dArgs::kAux;
         const int64_t c1 = n1 / 2, tnode = (c1 * n1 + c1) * n1 + c1;

@@ -2,7 +2,6 @@
 // Internal header shared by sweep_kernels.cu and biot_api.cu.
 #pragma once
 #include <cstdint>
-#include <vector>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -118,10 +117,7 @@ struct Tile3dArgs : SweepArgs {
     int32_t t_off;                    // first panel column of the time window (Gauss-Seidel waves)
     int32_t t_lo;                     // window steps below t_lo are computed but not stored or counted
     int32_t n1;                      // nodes per axis
-    int32_t z_rows;                   // planes marched per tile (upper bound; the tile table decides)
-    const int32_t *ttab;              // tile table [n_tiles][4] = {x0, y0, za, zb}, CTA-major (tile3d_schedule)
-    const int32_t *toff;              // CTA b marches tiles toff[b] .. toff[b+1]-1; launch grid = n_cta
-    int32_t n_cta;
+    int32_t z_rows;                   // planes marched per tile
     int32_t s0;                       // zero-storage structural-zero variant
     int32_t dry;                      // dev/measurement only: stream the ring without computing
 };
@@ -167,13 +163,7 @@ int tile2d_step0_blocks(int64_t n_nodes);
 cudaError_t launch_tile2d_step0(const Tile2dArgs &a, double *part, cudaStream_t st);
 
 // 3D TMA tile kernel: 4x2 (x,y) node patches x 64-step chunks, marching z
-// Static list schedule of the tile3d work (host): base tiles = (x, y) patch x z block of
-// z_rows planes in patch-fastest order; the tiles past the first `full` rounds are cut into
-// shorter plane ranges and every tile goes, in order, to the least-loaded CTA (cost =
-// planes + h), the cut chosen by the simulated makespan. Fills tab (4 ints per tile) and
-// off (n_cta + 1), returns n_cta.
-int tile3d_schedule(int n1, int z_rows, int grid, double h, std::vector<int32_t> &tab, std::vector<int32_t> &off,
-                    double *makespan = nullptr, double *makespan_rr = nullptr);
+int64_t tile3d_groups(const Tile3dArgs &a);
 int64_t tile3d_patches(int64_t n1);   // (x, y) patches of an n1^3 mesh
 int tile3d_chunk();
 int tile3d_max_zrows();

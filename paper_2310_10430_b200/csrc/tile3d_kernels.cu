@@ -33,8 +33,6 @@
 // in chunk 0 recomputes it from the ghost vector x_{first-1} in the same FMA order (so
 // iterates are bitwise independent of the time-slab split).
 #include <cuda.h>
-#include <algorithm>
-#include <set>
 #include <cstdint>
 #include <cstdlib>
 
@@ -374,18 +372,21 @@ __device__ __forceinline__ void finish_bt(const Tile3dArgs &a, const double *po,
 }
 
 struct Geo3 {
-    int n1, nchunks;
+    int n1, npx, npy, nzr, ntiles, nchunks;
     __device__ explicit Geo3(const Tile3dArgs &a) {
         n1 = a.n1;
+        npx = (n1 + kBX - 1) / kBX;
+        npy = (n1 + kBY - 1) / kBY;
+        nzr = (n1 + a.z_rows - 1) / a.z_rows;
+        ntiles = npx * npy * nzr;
         nchunks = (a.n_tl + kTc - 1) / kTc;
     }
-    // tile k of the host-built table (tile3d_schedule): patch origin and plane range
-    __device__ static void decode(const Tile3dArgs &a, int tile, int &x0, int &y0, int &za, int &zb) {
-        const int4 e = __ldg(reinterpret_cast<const int4 *>(a.ttab) + tile);
-        x0 = e.x;
-        y0 = e.y;
-        za = e.z;
-        zb = e.w;
+    __device__ void decode(int tile, int zrows, int &x0, int &y0, int &za, int &zb) const {
+        const int px = tile % npx, py = (tile / npx) % npy, zr = tile / (npx * npy);
+        x0 = px * kBX;
+        y0 = py * kBY;
+        za = zr * zrows;
+        zb = min(n1, za + zrows);
     }
 };
 
@@ -421,9 +422,9 @@ __global__ void __launch_bounds__(kThreads3, 1)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kProducerRegs));
         if (warp == kNodes && lane == 0) {
             uint32_t it = 0;
-            for (int tile = a.toff[blockIdx.x]; tile < a.toff[blockIdx.x + 1]; ++tile) {
+            for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
                 int x0, y0, za, zb;
-                g.decode(a, tile, x0, y0, za, zb);
+                g.decode(tile, a.z_rows, x0, y0, za, zb);
                 const int ny = min(kBY, g.n1 - y0);
                 for (int chunk = 0; chunk < g.nchunks; ++chunk)
                     for (int z = za - 1; z <= zb; ++z, ++it) {
@@ -452,15 +453,14 @@ __global__ void __launch_bounds__(kThreads3, 1)
     const int px = warp % kBX, py = warp / kBX;
     const int sx = px + 1, sy = py + 1;
     uint32_t it = 0;
-    const int tile0 = a.toff[blockIdx.x];
-    for (int tile = tile0; tile < a.toff[blockIdx.x + 1]; ++tile) {
+    for (int tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
         int x0, y0, za, zb;
-        g.decode(a, tile, x0, y0, za, zb);
+        g.decode(tile, a.z_rows, x0, y0, za, zb);
         // class stencils this tile can touch: x class in {cxl, cxl+1}, y in {cyl, cyl+1}, z in
         // {interior, the one z face the tile's plane range reaches (z_rows < n1)}; every
         // consumer is done with the previous tile's copy first
         const int cxl = x0 == 0 ? 0 : 1, cyl = y0 == 0 ? 0 : 1, czf = za == 0 ? 0 : 2;
-        if (tile != tile0) asm volatile("bar.sync 1, %0;" ::"r"(kNodes * 32) : "memory");
+        if (tile != (int)blockIdx.x) asm volatile("bar.sync 1, %0;" ::"r"(kNodes * 32) : "memory");
         for (int k = threadIdx.x; k < kClsLocal * kClsD; k += kNodes * 32) {
             const int L = k / kClsD, w = k - L * kClsD;
             const int cz = (L >> 2) ? czf : 1, cy = cyl + ((L >> 1) & 1), cx = cxl + (L & 1);
@@ -613,76 +613,10 @@ __global__ void __launch_bounds__(256) tile3d_step0_kernel(const Tile3dArgs a, d
 
 }  // namespace
 
-int tile3d_schedule(int n1, int z_rows, int grid, double h, std::vector<int32_t> &tab, std::vector<int32_t> &off,
-                    double *makespan, double *makespan_rr) {
-    struct T { int32_t x0, y0, za, zb; };
-    const int npx = (n1 + kBX - 1) / kBX, npy = (n1 + kBY - 1) / kBY, nzr = (n1 + z_rows - 1) / z_rows;
-    std::vector<T> base;
-    for (int k = 0; k < nzr; ++k)
-        for (int py = 0; py < npy; ++py)
-            for (int px = 0; px < npx; ++px)
-                base.push_back({px * kBX, py * kBY, k * z_rows, std::min(n1, (k + 1) * z_rows)});
-    const int n = (int)base.size(), G = std::max(1, std::min(grid, n));
-    // pieces: base[0, full*G) whole, the rest of the first tail half cut in s1, the second in s2
-    auto cut = [&](int full, int s1, int s2, std::vector<T> &out) {
-        out.clear();
-        const int t0 = std::min(n, full * G), mid = t0 + (n - t0) / 2;
-        for (int i = 0; i < n; ++i) {
-            const int s = i < t0 ? 1 : i < mid ? s1 : s2, len = base[i].zb - base[i].za;
-            int a = base[i].za;
-            for (int j = 1; j <= s; ++j) {
-                const int b = base[i].za + (int)((int64_t)len * j / s);
-                if (b > a) out.push_back({base[i].x0, base[i].y0, a, b});
-                a = b;
-            }
-        }
-    };
-    // greedy list schedule: each piece in order to the least-loaded CTA (lowest index on ties,
-    // so equal pieces go round robin and concurrently marched tiles stay spatial neighbours)
-    auto simulate = [&](const std::vector<T> &p, std::vector<int> *owner) {
-        std::set<std::pair<double, int>> q;   // (load, CTA)
-        for (int c = 0; c < G; ++c) q.insert({0.0, c});
-        double ms = 0.0;
-        if (owner) owner->resize(p.size());
-        for (size_t i = 0; i < p.size(); ++i) {
-            auto [l, c] = *q.begin();
-            q.erase(q.begin());
-            l += (p[i].zb - p[i].za) + h;
-            q.insert({l, c});
-            ms = std::max(ms, l);
-            if (owner) (*owner)[i] = c;
-        }
-        return ms;
-    };
-    std::vector<T> p, best_p;
-    cut(n, 1, 1, p);
-    const double rr = simulate(p, nullptr);
-    double best = rr;
-    best_p = p;
-    for (int full = std::max(0, n / G - 3); full <= n / G; ++full)
-        for (int s1 = 1; s1 <= 4; ++s1)
-            for (int s2 = s1; s2 <= 6; ++s2) {
-                cut(full, s1, s2, p);
-                const double ms = simulate(p, nullptr);
-                if (ms < best - 1e-9) { best = ms; best_p = p; }
-            }
-    std::vector<int> owner;
-    simulate(best_p, &owner);
-    off.assign(G + 1, 0);
-    for (int c : owner) off[c + 1]++;
-    for (int c = 0; c < G; ++c) off[c + 1] += off[c];
-    tab.assign(best_p.size() * 4, 0);
-    std::vector<int32_t> fill(off.begin(), off.end() - 1);
-    for (size_t i = 0; i < best_p.size(); ++i) {
-        const int k = fill[owner[i]]++;
-        tab[4 * k] = best_p[i].x0;
-        tab[4 * k + 1] = best_p[i].y0;
-        tab[4 * k + 2] = best_p[i].za;
-        tab[4 * k + 3] = best_p[i].zb;
-    }
-    if (makespan) *makespan = best;
-    if (makespan_rr) *makespan_rr = rr;
-    return G;
+int64_t tile3d_groups(const Tile3dArgs &a) {
+    const int64_t npx = (a.n1 + kBX - 1) / kBX, npy = (a.n1 + kBY - 1) / kBY;
+    const int64_t nzr = (a.n1 + a.z_rows - 1) / a.z_rows;
+    return npx * npy * nzr;
 }
 
 int64_t tile3d_patches(int64_t n1) { return ((n1 + kBX - 1) / kBX) * ((n1 + kBY - 1) / kBY); }
@@ -748,8 +682,8 @@ cudaError_t launch_tile3d_step0(const Tile3dArgs &a, double *part, cudaStream_t 
 cudaError_t launch_tile3d(const CUtensorMap &tmx, const Tile3dArgs &a, const LaunchShape &sh,
                           cudaStream_t st) {
     if (a.z_rows < 1 || a.z_rows > kMaxZ || a.z_rows >= a.n1 || a.n1 < kBX + 1) return cudaErrorInvalidValue;
-    if (!a.ttab || !a.toff || a.n_cta < 1 || a.n_cta > sh.grid) return cudaErrorInvalidValue;
-    const int grid = a.n_cta;
+    const int64_t tiles = tile3d_groups(a);
+    const int grid = (int)(tiles < sh.grid ? tiles : sh.grid);
     const dim3 block(kThreads3);
 #define BIOT_T3(S0_, M_) tile3d_kernel<S0_, M_><<<grid, block, sh.smem, st>>>(tmx, a)
     if (a.mode == MODE_UPDATE_P2) { if (a.s0) BIOT_T3(true, MODE_UPDATE_P2); else BIOT_T3(false, MODE_UPDATE_P2); }
