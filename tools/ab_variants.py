@@ -5,6 +5,11 @@ per process):
 
     python tools/ab_variants.py --config 4 --precond 2 lib_a.so lib_b.so ...
     ('-' = the product library)
+
+Compare against the library of the previous commit (build it from a checkout of that
+commit into paper_2310_10430_b200/build/ab/), not only against a switch inside the new
+build: the reverted tile3d list schedule gained 1.3% over its own fallback order while the
+whole build was 3.5% slower than its predecessor (profiles/r02_ab_tile3d_schedule.txt).
 """
 import argparse
 import hashlib
